@@ -1,0 +1,209 @@
+"""Pins for the oracle's scheduler / partition-manager event loop (Alg. 4 PAPER.md:597-617,
+OOM restart PAPER.md:569, early restart PAPER.md:571/:757/:763, baseline PAPER.md:635-637).
+
+Independent references: the hand-derived schedule of example W (tests/golden/config1_w.json), the throughput
+ceilings the paper states (7x for 5 GB jobs PAPER.md:687, 2x for 20 GB jobs PAPER.md:684), closed-form energy,
+the early-restart analogue of "6 vs 94" (example E), a pure-Python brute-force replay of every decision on tiny
+queues (tests/bruteforce.py), and conservation invariants on generated traces.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from bruteforce import Replay, fcr_table
+from conftest import GOLDEN_DIR, geom_path
+from oracle import oracle as orc
+from tracegen import tracegen as tg
+
+POLICY = {"BASELINE": 0, "STATIC": 1, "DYNAMIC": 2, "FUSION_FISSION": 3}
+
+
+def spec_of(name):
+    with open(geom_path(name)) as f:
+        return json.load(f)
+
+
+def w_fixture():
+    with open(os.path.join(GOLDEN_DIR, "config1_w.json")) as f:
+        fx = json.load(f)
+    tr = [tg.pack_job(j["est_gb"] * 1024, j["true_gb"] * 1024, j["iters"], 0, j["iter_ticks"]) for j in fx["jobs_gb"]]
+    return fx, tg.pack_traces([tr])
+
+
+@pytest.mark.parametrize("pname", list(POLICY))
+def test_example_w(pname):
+    fx, (jobs, ext, off) = w_fixture()
+    g = orc.Geometry(geom_path(fx["geometry"]))
+    r, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=POLICY[pname], **fx["policy_common"]), records=True)
+    r = r[0, 0]
+    for k, v in fx["expected"][pname].items():
+        if isinstance(v, int):
+            assert int(r[k]) == v, (pname, k)
+    dec = int(r["placements"]) + int(r["waits"]) + int(r["rejected"])
+    assert dec == 15  # 15 decisions under every policy
+    if pname == "FUSION_FISSION":
+        got = [(d["tick"], d["job"], d["kind"], d["start"]) for d in recs if d["kind"] not in ("COMPLETE",)]
+        assert got[:4] == [(0, 0, "ALLOC", 2), (0, 1, "ALLOC", 1), (0, 2, "ALLOC", 0), (0, 3, "WAIT", 15)]
+        assert (160, 4, "OOM", 3) in got and (160, 7, "REUSE", 3) in got and (180, 4, "RECONF", 2) in got
+    # FF vs BASELINE: throughput 450/220, energy 58500/27100
+
+
+def test_throughput_ceilings():
+    # 7 identical 5 GB jobs -> 7.00x; 2 identical 20 GB jobs -> 2.00x.
+    g = orc.Geometry(geom_path("a100-40gb"))
+    for n, gb in [(7, 4), (2, 19)]:
+        tr = [tg.pack_job(gb * 1024, gb * 1024, 10, 0, 1000) for _ in range(n)]
+        jobs, ext, off = tg.pack_traces([tr])
+        kw = dict(ctx_mib=512, reconfig_ticks=0)
+        ff = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, **kw))[0, 0]
+        dyn = orc.simulate(g, jobs, ext, off, orc.policy(kind=2, **kw))[0, 0]
+        base = orc.simulate(g, jobs, ext, off, orc.policy(kind=0, **kw))[0, 0]
+        assert base["makespan"] / ff["makespan"] == pytest.approx(float(n), abs=0.01)
+        assert base["makespan"] / dyn["makespan"] == pytest.approx(float(n), abs=0.01)
+
+
+def test_energy_closed_form():
+    # single 10 s job on a flat 100 W GPU -> 1000 J; general: idle*makespan + w*sum(compute*len).
+    g = orc.Geometry(geom_path("a100-40gb"))
+    jobs, ext, off = tg.pack_traces([[tg.pack_job(1024, 1024, 10, 0, 1000)]])
+    r = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, idle_w=100, w_per_slice=0, reconfig_ticks=0))[0, 0]
+    assert r["makespan"] == 10000 and r["energy_wticks"] * 1e-3 == 1000.0
+    r = orc.simulate(g, jobs, ext, off, orc.policy(kind=0, idle_w=30, w_per_slice=25, reconfig_ticks=0))[0, 0]
+    assert r["energy_wticks"] == 30 * 10000 + 25 * 7 * 10000  # baseline uses all 7 compute slices
+
+
+def dyn_job(b, slope, T, ticks, sigma=0, qslope=0, ws=0):
+    return tg.pack_job(b, 65536, T, tg_dynamic(), ticks, ws=ws, slope_q8=slope * 256, sigma=sigma, qslope=qslope)
+
+
+def tg_dynamic():
+    return 2
+
+
+def test_early_restart_example_E():
+    # Example E: req_i = 1000 + 100 i, T = 50, 10 ticks/iter, starts on 1g.5gb (5120 MiB,
+    # PAPER.md:757). Without prediction: OOM at iteration 42 (5200 > 5120) -> rerun on 2g.10gb. With prediction:
+    # converged at n = 6 with 6000 > 5120 -> PREEMPT at 60 ticks. Wasted iterations 6 vs 42 ("6 vs 94").
+    g = orc.Geometry(geom_path("a100-40gb"))
+    jobs, ext, off = tg.pack_traces([[dyn_job(1000, 100, 50, 10)]])
+    kw = dict(ctx_mib=0, reconfig_ticks=0)
+    r, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, **kw), records=True)
+    assert [(d["tick"], d["kind"], d["profile"]) for d in recs] == [
+        (0, "ALLOC", 0), (420, "OOM", 0), (420, "ALLOC", 1), (920, "COMPLETE", 1)]
+    assert r[0, 0]["busy_slice_ticks"] == 420 * 1 + 500 * 2
+    r, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, flags=orc.EARLY_RESTART, **kw), records=True)
+    assert [(d["tick"], d["kind"], d["profile"]) for d in recs] == [
+        (0, "ALLOC", 0), (60, "PREEMPT", 0), (60, "ALLOC", 1), (560, "COMPLETE", 1)]
+    assert r[0, 0]["preempts"] == 1 and r[0, 0]["ooms"] == 0 and r[0, 0]["makespan"] == 560
+
+
+def test_head_of_line_wait():
+    # "if a workload that occupies half the GPU is running and the next job requires the full GPU,
+    # scheme B would wait for the first workload to finish, even though there might be workloads that can fit".
+    g = orc.Geometry(geom_path("a100-40gb"))
+    tr = [tg.pack_job(15000, 15000, 1, 0, 1000), tg.pack_job(35000, 35000, 1, 0, 100), tg.pack_job(1000, 1000, 1, 0, 10)]
+    jobs, ext, off = tg.pack_traces([tr])
+    _, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, reconfig_ticks=0), records=True)
+    starts = {d["job"]: d["tick"] for d in recs if d["kind"] in ("ALLOC", "RECONF", "REUSE")}
+    assert starts[1] == 1000 and starts[2] == 1100  # the 5 GB job waits behind the 40 GB head (not at t=0)
+
+
+def test_merge_and_split():
+    g = orc.Geometry(geom_path("a100-40gb"))
+    # split: an idle 7g is destroyed to create a 1g at the argmax slot
+    tr = [tg.pack_job(30000, 30000, 1, 0, 100), tg.pack_job(1000, 1000, 1, 0, 100)]
+    jobs, ext, off = tg.pack_traces([tr])
+    _, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, reconfig_ticks=0), records=True)
+    assert (100, "RECONF", 6, 1) in [(d["tick"], d["kind"], d["start"], d["n_destroyed"]) for d in recs]
+    # merge: two idle 1g are merged into a 2g
+    tr = [tg.pack_job(1000, 1000, 1, 0, 100)] * 7 + [tg.pack_job(8000, 8000, 1, 0, 100)]
+    jobs, ext, off = tg.pack_traces([tr])
+    _, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, reconfig_ticks=0), records=True)
+    last = [d for d in recs if d["job"] == 7 and d["kind"] == "RECONF"][0]
+    assert last["n_destroyed"] == 2 and last["profile"] == 1
+
+
+def test_failed_and_rejected_and_empty():
+    g = orc.Geometry(geom_path("a100-40gb"))
+    tr = [tg.pack_job(30000, 50000, 3, 0, 10),  # fits 7g by estimate, true 50 GB: OOM on 40 GB -> FAILED
+          tg.pack_job(50000, 50000, 3, 0, 10)]  # estimate above the GPU: REJECTED
+    jobs, ext, off = tg.pack_traces([tr, []])
+    r = orc.simulate(g, jobs, ext, off, [orc.policy(kind=k) for k in range(4)])
+    for p in range(4):
+        if p == 1:  # STATIC: no layout slice holds 40 GB -> both rejected (R11)
+            assert r[0, p]["failed"] == 0 and r[0, p]["rejected"] == 2
+        else:
+            assert r[0, p]["failed"] == 1 and r[0, p]["rejected"] == 1 and r[0, p]["completed"] == 0
+        e = r[1, p]
+        assert e["makespan"] == 0 and e["n_jobs"] == 0 and e["decision_hash"] == 0xcbf29ce484222325
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_conservation_invariants_generated(cfg):
+    n = 60
+    jobs, ext, off = tg.generate_host(cfg, n)
+    g = orc.Geometry(geom_path(tg.CONFIG_GEOMETRY[cfg]))
+    pols = [orc.policy(kind=k) for k in range(4)] + [orc.policy(kind=3, flags=orc.EARLY_RESTART)]
+    r = orc.simulate(g, jobs, ext, off, pols, seed=tg.seed_of(cfg))  # oracle asserts no overlap / capacity inside
+    assert np.all(r["completed"] + r["rejected"] + r["failed"] == r["n_jobs"])
+    assert np.all(r["restarts"] == r["ooms"] - r["failed"] + r["preempts"])
+    assert np.all(r["energy_wticks"] == 30 * r["makespan"].astype(np.uint64) + 25 * r["busy_slice_ticks"])
+    assert np.all(r["preempts"][:, :4] == 0)  # only the early-restart policy preempts
+    # determinism
+    r2 = orc.simulate(g, jobs, ext, off, pols, seed=tg.seed_of(cfg))
+    assert np.array_equal(r, r2)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 5])
+def test_fifo_start_order(cfg):
+    # Scheme B fairness: first starts are in queue order (head-of-line); requeues go to the tail.
+    jobs, ext, off = tg.generate_host(cfg, 8)
+    g = orc.Geometry(geom_path(tg.CONFIG_GEOMETRY[cfg]))
+    for k in range(4):
+        for t in range(8):
+            _, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=k), seed=tg.seed_of(cfg), t0=t, t1=t + 1,
+                                   records=True)
+            first = []
+            for d in recs:
+                if d["kind"] in ("REUSE", "ALLOC", "RECONF", "PLACE_STATIC", "PLACE_BASELINE", "REJECT") and \
+                        d["job"] not in first:
+                    first.append(d["job"])
+            assert first == sorted(first)
+
+
+@pytest.mark.parametrize("geo,cfg", [("a30-24gb", None), ("a100-40gb", 2), ("a100-40gb", 5)])
+def test_bruteforce_replay_tiny_queues(geo, cfg):
+    # Every decision on tiny queues equals the brute-force optimum over all candidate successors, and only valid
+    # partition states are visited (north_star: brute-force enumeration of every reachable partition state).
+    spec = spec_of(geo)
+    S, fcr = fcr_table(spec)
+    g = orc.Geometry(spec)
+    rng = np.random.default_rng(11)
+    slot = spec["slot_mib"]
+    traces = []
+    if cfg is None:
+        for _ in range(300):
+            tr = []
+            for _ in range(int(rng.integers(1, 5))):
+                est = int(rng.integers(1, spec["total_memory_slots"] * slot))
+                tru = est if rng.random() < 0.7 else int(rng.integers(1, spec["total_memory_slots"] * slot + 2000))
+                tr.append(tg.pack_job(est, tru, int(rng.integers(1, 4)), 0, int(rng.integers(1, 6)) * 10))
+            traces.append(tr)
+        jobs, ext, off = tg.pack_traces(traces)
+        seed = 0
+    else:
+        jobs, ext, off = tg.generate_host(cfg, 40)
+        seed = tg.seed_of(cfg)
+    visited = set()
+    for k in range(4):
+        for flags in ([0, 1] if k == 3 else [0]):
+            pol = orc.policy(kind=k, flags=flags, ctx_mib=0 if cfg is None else 512, reconfig_ticks=0 if cfg is None else 500)
+            for t in range(len(off) - 1):
+                _, recs = orc.simulate(g, jobs, ext, off, pol, seed=seed, t0=t, t1=t + 1, records=True)
+                rp = Replay(spec, k, fcr)
+                for d in recs:
+                    rp.step(d)
+                visited |= set(rp.visited)
+    assert visited <= set(S)
