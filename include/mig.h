@@ -1,0 +1,208 @@
+/* mig.h — C ABI of libmig.so: batched simulation of the MIGM dynamic MIG partition manager + scheduler
+ * (arXiv 2508.18556, "Managing Multi Instance GPUs for High Throughput and Energy Savings") over very many
+ * independent synthetic job queues ("traces"), on B200 (sm_100a).
+ *
+ * The calls follow the paper's problem statement: jobs with a memory footprint, duration and compute need arrive at
+ * a scheduler, which asks the partition manager for a slice.
+ *
+ *   mig_geometry_load    GPU geometry + Alg. 1 reachability table            [host]
+ *   mig_estimate_memory  per-job memory estimation: compile-time / model-size estimates
+ *                         and the time-series predictor Alg. 3
+ *                                                                               [device, async]
+ *   mig_simulate         right-sized request, Alg. 2 placement,
+ *                        Scheme B + fusion/fission, OOM restart,
+ *                        early restart, metrics                  [device, async]
+ *   mig_simulate_host    the same from HOST buffers (H2D, estimate, simulate, D2H pipelined)       [host, sync]
+ *
+ * Conventions
+ *   - Every entry point returns a mig_status; mig_last_error() gives a thread-local message for the last failure.
+ *   - Units: time = integer ticks (1 tick = 1 ms), memory = integer MiB, power = integer W, energy = W*ticks.
+ *   - Ownership: the library never frees or retains caller memory beyond a call (device calls: beyond the
+ *     stream-ordered work they enqueue). A mig_geometry owns its host tables and per-device copies.
+ *   - Asynchrony: device entry points are stream-ordered; outputs are valid once the stream is synchronised.
+ *   - Semantic outcomes (rejected or failed jobs) are counted in results, never reported as errors. Call errors
+ *     are malformed arguments (MIG_E_INVALID_ARG), geometry problems (MIG_E_IO / PARSE / VALIDATION / CAPACITY),
+ *     trace-format violations detected on the device (reported in mig_policy_totals.error_flags), and CUDA
+ *     failures (MIG_E_CUDA).
+ *   - No CPU fallback: without a CUDA device the device entry points fail with MIG_E_CUDA.
+ *   - Determinism: results are a pure function of (geometry, traces, policies).
+ */
+#ifndef MIG_H
+#define MIG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MIG_OK = 0,
+    MIG_E_INVALID_ARG = 1,
+    MIG_E_IO = 2,
+    MIG_E_PARSE = 3,
+    MIG_E_VALIDATION = 4,
+    MIG_E_CAPACITY = 5, /* geometry state space too large */
+    MIG_E_CUDA = 6,
+    MIG_E_UNSUPPORTED = 7
+} mig_status;
+
+/* Message for the last non-OK status on this thread (valid until the next call on this thread). */
+const char* mig_last_error(void);
+
+/* ------------------------------------------------------------------------------------------------------------------
+ * Geometry (profiles and placement rules; Alg. 1)
+ * ---------------------------------------------------------------------------------------------------------------- */
+typedef struct mig_geometry mig_geometry; /* opaque; immutable after load; shareable across threads and streams */
+
+#define MIG_MAX_SLOTS 8
+#define MIG_MAX_PROFILES 15
+#define MIG_MAX_LEVELS 5 /* distinct profile memory sizes */
+
+typedef struct {
+    char gpu_name[64];
+    uint32_t n_slots;      /* memory slots (8 on A100/H100, 4 on A30) */
+    uint32_t slot_mib;     /* MiB per memory slot */
+    uint32_t n_compute;    /* compute slices of the GPU */
+    uint32_t n_profiles;   /* profiles, sorted by (memory, compute) ascending */
+    uint32_t n_levels;     /* distinct profile memory sizes */
+    uint32_t n_placements; /* legal (profile, start) pairs */
+    uint32_t n_states;     /* |S|: valid partition states (sets of placed instances) */
+    uint32_t n_finals;     /* |F|: fully configured states (no legal allocation remains) */
+    uint32_t fcr_s0;       /* fcr(empty GPU) */
+    uint32_t full_mem_mib; /* memory of the whole GPU */
+    uint32_t n_layout;     /* instances of the static layout (policy MIG_STATIC) */
+    uint32_t idle_w, w_per_slice; /* default power model (W idle; W per busy compute slice) */
+} mig_geometry_info;
+
+/* Load a geometry from a JSON file path, or "builtin:<name>" for the tables shipped next to libmig.so
+ * (a30-24gb, a100-40gb, a100-40gb-1g10, a100-80gb, h100-80gb). Validates the placement table (every placement
+ * inside the slots; profiles sorted by memory then compute; at most MIG_MAX_* of each), enumerates the valid
+ * states, and builds the fcr table indexed by the occupancy bitmask (bit i = memory slot i busy).
+ * Errors: MIG_E_IO (file), MIG_E_PARSE (JSON; message names the offset), MIG_E_VALIDATION (message names the
+ * field), MIG_E_CAPACITY. *out is set only on MIG_OK; free with mig_geometry_free. */
+mig_status mig_geometry_load(const char* json_path_or_builtin, mig_geometry** out);
+void mig_geometry_free(mig_geometry* g);
+mig_status mig_geometry_query(const mig_geometry* g, mig_geometry_info* out);
+
+/* Profile p (0 <= p < n_profiles): memory MiB, compute slices, memory slots, name (<= 31 chars + NUL). */
+mig_status mig_geometry_profile(const mig_geometry* g, uint32_t p, uint32_t* mem_mib, uint32_t* compute,
+                                uint32_t* slots, char name[32]);
+
+/* fcr of an occupancy mask: number of fully configured states reachable from it. 0 for masks that
+ * are not the occupancy of any valid state. Host-only test hook. */
+mig_status mig_geometry_fcr(const mig_geometry* g, uint32_t occ_mask, uint32_t* fcr);
+
+/* Alg. 2 allocate_partition on an occupancy mask: the start slot of the legal placement of
+ * `profile` maximising fcr (equal fcr: highest start), or -1 = FAIL. Host-only test hook. */
+mig_status mig_geometry_place(const mig_geometry* g, uint32_t occ_mask, uint32_t profile, int32_t* start);
+
+/* ------------------------------------------------------------------------------------------------------------------
+ * Traces (job queues). All jobs of a trace arrive at t = 0 (batch).
+ * Record format (tracegen/tracegen.h documents the same layout):
+ *   jobs[j]     = {x, y, z, w} u32:
+ *                 STATIC/MODEL: x = est_mib (compile-time / model-size estimate), y = true_mib (footprint)
+ *                 DYNAMIC:      x = b_mib (intercept), y = q0_q16 (inverse reuse ratio at t=0, Q16)
+ *                 z = iters (bits 0-15) | class (bits 16-23: 0 STATIC, 1 MODEL, 2 DYNAMIC) | 0 (bits 24-31)
+ *                 w = iter_ticks
+ *   jobs_ext[j] = {ws_mib, warps, slope_q8, sigma_mib | qslope_q16 << 16} or NULL (all zero).
+ *   DYNAMIC jobs report per-iteration samples (requested MiB, inverse reuse Q16) drawn in-kernel from the
+ *   counter-based generator of tracegen.h keyed by (seed, trace_id0 + trace, job index in trace).
+ * ---------------------------------------------------------------------------------------------------------------- */
+typedef struct {
+    const void* jobs;           /* 16 B per job; points at the record of job trace_off[0]                */
+    const void* jobs_ext;       /* 16 B per job or NULL                                                  */
+    const uint64_t* trace_off;  /* n_traces + 1 CSR offsets (non-decreasing)                             */
+    uint64_t n_traces;
+    uint64_t trace_id0;         /* global id of trace 0 (sample-generator counter)                       */
+    uint64_t seed;              /* sample-generator seed                                                 */
+    uint64_t n_jobs;            /* trace_off[n_traces] - trace_off[0] (sizes internal estimate scratch)  */
+    uint32_t max_jobs;          /* upper bound on jobs per trace, 1..MIG_MAX_JOBS_PER_TRACE               */
+    uint32_t reserved;          /* must be 0                                                             */
+} mig_traces;
+
+#define MIG_MAX_JOBS_PER_TRACE 768 /* on-chip (shared-memory) staging limit of one trace */
+
+/* ------------------------------------------------------------------------------------------------------------------
+ * Policies
+ * ---------------------------------------------------------------------------------------------------------------- */
+enum {
+    MIG_BASELINE = 0,      /* non-partitioned GPU, one job at a time, queue order       */
+    MIG_STATIC = 1,        /* fixed slice layout, no reconfiguration                      */
+    MIG_DYNAMIC = 2,       /* create a tight slice on demand (Alg. 2), destroy it at run end               */
+    MIG_FUSION_FISSION = 3 /* Scheme B: reuse idle tight slice, Alg. 2, merge/split idle slices, wait      */
+};
+enum {
+    MIG_EARLY_RESTART = 1, /* preempt when the converged forecast exceeds the slice   */
+    MIG_WARP_FOLD = 2,     /* tight fit keeps the full-GPU wave count                        */
+    MIG_EWMA_REUSE = 4     /* EWMA of the inverse reuse ratio instead of its trend (north_star; not in paper) */
+};
+
+typedef struct {
+    uint32_t kind, flags;
+    uint32_t ctx_mib;        /* CUDA context per job                                  */
+    uint32_t reconfig_ticks; /* delay before a job starts on a newly created instance                   */
+    uint32_t idle_w, w_per_slice;
+    double z;                /* z-score of the one-sided 99% bound, default 2.326          */
+    uint32_t eps_num, eps_den; /* convergence: |dP| * eps_den < P * eps_num (default 1/100)               */
+    uint32_t conv_k;         /* consecutive small changes (default 3, 1..8)                              */
+    uint32_t min_n;          /* first iteration with a prediction (default 3, >= 3)                      */
+} mig_policy;
+
+/* ------------------------------------------------------------------------------------------------------------------
+ * Outputs
+ * ---------------------------------------------------------------------------------------------------------------- */
+#define MIG_NEVER 0xFFFFu
+
+typedef struct {             /* 48 B, one per job                                                          */
+    uint32_t req0_mib;       /* first memory requirement: est + ws + ctx, or the smallest slice (DYNAMIC) */
+    uint32_t pred_mib;       /* converged forecast incl. ws + ctx (DYNAMIC), else 0                       */
+    uint16_t conv_iter;      /* iteration at which the forecast converged (DYNAMIC), 0 = never            */
+    uint16_t n_levels;
+    uint16_t fe[6];          /* first iteration whose physical memory exceeds memory level l; MIG_NEVER   */
+    double phi, a, sigma;    /* diagnostics of the last fit (DYNAMIC)                                     */
+} mig_job_estimate;
+
+typedef struct {             /* 80 B, one per (trace, policy)                                             */
+    uint32_t makespan, n_jobs, completed, rejected, failed, ooms, preempts, restarts, placements, waits,
+        creates, destroys;
+    uint64_t energy_wticks, turnaround_sum, busy_slice_ticks, decision_hash;
+} mig_trace_result;
+
+#define MIG_ERR_TRACE_TOO_LONG 1ull /* a trace has more than max_jobs jobs                             */
+#define MIG_ERR_BAD_RECORD 2ull     /* class > 2, iters > 4096, or a sample outside the predictor's range */
+
+typedef struct {             /* 160 B, one per policy: sums over traces (integer, exact in any order)     */
+    uint64_t n_traces, n_jobs, completed, rejected, failed, ooms, preempts, restarts, placements, waits,
+        creates, destroys, makespan_sum, makespan_max, energy_wticks, turnaround_sum, busy_slice_ticks,
+        decision_hash_sum, error_flags, reserved;
+} mig_policy_totals;
+
+/* Per-job estimates for every job of the traces (DEVICE buffers; out has trace_off[n]-trace_off[0] entries).
+ * stream: a cudaStream_t (NULL = legacy default stream). */
+mig_status mig_estimate_memory(const mig_geometry* g, const mig_traces* traces, const mig_policy* policy,
+                               mig_job_estimate* out, void* stream);
+
+/* Simulate every trace under each of n_policies policies (host array). Policies must agree on the estimation
+ * parameters (ctx_mib, z, eps, conv_k, min_n, EWMA flag). est: per-job estimates from mig_estimate_memory
+ * (DEVICE) or NULL (computed internally into stream-ordered scratch). out: DEVICE [n_traces][n_policies] or NULL.
+ * totals: DEVICE [n_policies] or NULL; zeroed and accumulated by the call. */
+mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const mig_policy* policies,
+                        uint32_t n_policies, const mig_job_estimate* est, mig_trace_result* out,
+                        mig_policy_totals* totals, void* stream);
+
+/* Same as mig_simulate with every pointer of `traces`, `out` and `totals` in HOST memory (page-locked memory
+ * recommended). Copies in, estimates, simulates and copies back in chunks pipelined over two streams on the
+ * current device; returns after the results are in host memory. */
+mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, const mig_policy* policies,
+                             uint32_t n_policies, mig_trace_result* out, mig_policy_totals* totals);
+
+/* Number of kernel launches issued by the last device call on this thread (bench accounting). */
+uint32_t mig_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MIG_H */

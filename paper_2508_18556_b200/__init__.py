@@ -1,0 +1,247 @@
+"""paper_2508_18556_b200 — Python binding of libmig.so (include/mig.h).
+
+Argument marshalling only: every step of the hot path (memory estimation, tight fit, Alg. 2 placement,
+fusion/fission, OOM and early restart, event loop, metric reduction) runs in the sm_100a kernels of libmig.so.
+PyTorch is used for device memory and streams. There is no CPU fallback: importing this package fails loudly if
+libmig.so has not been built, and the device entry points fail without a CUDA device.
+
+Names follow the C ABI: mig_geometry_load, mig_estimate_memory, mig_simulate, mig_simulate_host, ...
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmig.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` (no CPU fallback exists)")
+_lib = C.CDLL(LIB_PATH)
+
+MIG_BASELINE, MIG_STATIC, MIG_DYNAMIC, MIG_FUSION_FISSION = 0, 1, 2, 3
+MIG_EARLY_RESTART, MIG_WARP_FOLD, MIG_EWMA_REUSE = 1, 2, 4
+MIG_MAX_JOBS_PER_TRACE = 768
+MIG_NEVER = 0xFFFF
+STATUS = {0: "MIG_OK", 1: "MIG_E_INVALID_ARG", 2: "MIG_E_IO", 3: "MIG_E_PARSE", 4: "MIG_E_VALIDATION",
+          5: "MIG_E_CAPACITY", 6: "MIG_E_CUDA", 7: "MIG_E_UNSUPPORTED"}
+
+RESULT_DTYPE = np.dtype([
+    ("makespan", "<u4"), ("n_jobs", "<u4"), ("completed", "<u4"), ("rejected", "<u4"), ("failed", "<u4"),
+    ("ooms", "<u4"), ("preempts", "<u4"), ("restarts", "<u4"), ("placements", "<u4"), ("waits", "<u4"),
+    ("creates", "<u4"), ("destroys", "<u4"), ("energy_wticks", "<u8"), ("turnaround_sum", "<u8"),
+    ("busy_slice_ticks", "<u8"), ("decision_hash", "<u8")])
+ESTIMATE_DTYPE = np.dtype([
+    ("req0_mib", "<u4"), ("pred_mib", "<u4"), ("conv_iter", "<u2"), ("n_levels", "<u2"), ("fe", "<u2", (6,)),
+    ("phi", "<f8"), ("a", "<f8"), ("sigma", "<f8")])
+TOTALS_FIELDS = ["n_traces", "n_jobs", "completed", "rejected", "failed", "ooms", "preempts", "restarts",
+                 "placements", "waits", "creates", "destroys", "makespan_sum", "makespan_max", "energy_wticks",
+                 "turnaround_sum", "busy_slice_ticks", "decision_hash_sum", "error_flags", "reserved"]
+TOTALS_DTYPE = np.dtype([(f, "<u8") for f in TOTALS_FIELDS])
+assert RESULT_DTYPE.itemsize == 80 and ESTIMATE_DTYPE.itemsize == 48 and TOTALS_DTYPE.itemsize == 160
+
+
+class MigError(RuntimeError):
+    pass
+
+
+class mig_geometry_info(C.Structure):
+    _fields_ = [("gpu_name", C.c_char * 64)] + [(n, C.c_uint32) for n in (
+        "n_slots", "slot_mib", "n_compute", "n_profiles", "n_levels", "n_placements", "n_states", "n_finals",
+        "fcr_s0", "full_mem_mib", "n_layout", "idle_w", "w_per_slice")]
+
+
+class mig_traces(C.Structure):
+    _fields_ = [("jobs", C.c_void_p), ("jobs_ext", C.c_void_p), ("trace_off", C.c_void_p), ("n_traces", C.c_uint64),
+                ("trace_id0", C.c_uint64), ("seed", C.c_uint64), ("n_jobs", C.c_uint64), ("max_jobs", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+class mig_policy(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("flags", C.c_uint32), ("ctx_mib", C.c_uint32),
+                ("reconfig_ticks", C.c_uint32), ("idle_w", C.c_uint32), ("w_per_slice", C.c_uint32),
+                ("z", C.c_double), ("eps_num", C.c_uint32), ("eps_den", C.c_uint32), ("conv_k", C.c_uint32),
+                ("min_n", C.c_uint32)]
+
+
+_lib.mig_last_error.restype = C.c_char_p
+_lib.mig_last_launch_count.restype = C.c_uint32
+_lib.mig_geometry_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+_lib.mig_geometry_free.argtypes = [C.c_void_p]
+_lib.mig_geometry_query.argtypes = [C.c_void_p, C.POINTER(mig_geometry_info)]
+_lib.mig_geometry_profile.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                      C.POINTER(C.c_uint32), C.c_char_p]
+_lib.mig_geometry_fcr.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]
+_lib.mig_geometry_place.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_int32)]
+_lib.mig_estimate_memory.argtypes = [C.c_void_p, C.POINTER(mig_traces), C.POINTER(mig_policy), C.c_void_p,
+                                     C.c_void_p]
+_lib.mig_simulate.argtypes = [C.c_void_p, C.POINTER(mig_traces), C.POINTER(mig_policy), C.c_uint32, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p]
+_lib.mig_simulate_host.argtypes = [C.c_void_p, C.POINTER(mig_traces), C.POINTER(mig_policy), C.c_uint32,
+                                   C.c_void_p, C.c_void_p]
+
+
+def _check(status):
+    if status != 0:
+        raise MigError(f"{STATUS.get(status, status)}: {_lib.mig_last_error().decode()}")
+
+
+def mig_last_launch_count() -> int:
+    return int(_lib.mig_last_launch_count())
+
+
+class Geometry:
+    """A loaded geometry (opaque mig_geometry*), with its info and profile table."""
+
+    def __init__(self, handle):
+        self.h = handle
+        info = mig_geometry_info()
+        _check(_lib.mig_geometry_query(self.h, C.byref(info)))
+        self.info = info
+        self.name = info.gpu_name.decode()
+        self.profiles = []
+        for p in range(info.n_profiles):
+            m, c, s = C.c_uint32(), C.c_uint32(), C.c_uint32()
+            nm = C.create_string_buffer(32)
+            _check(_lib.mig_geometry_profile(self.h, p, C.byref(m), C.byref(c), C.byref(s), nm))
+            self.profiles.append(dict(name=nm.value.decode(), mem_mib=m.value, compute=c.value, slots=s.value))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.mig_geometry_free(self.h)
+            self.h = None
+
+
+def mig_geometry_load(path_or_builtin: str) -> Geometry:
+    h = C.c_void_p()
+    _check(_lib.mig_geometry_load(path_or_builtin.encode(), C.byref(h)))
+    return Geometry(h)
+
+
+def mig_geometry_fcr(g: Geometry, occ: int) -> int:
+    out = C.c_uint32()
+    _check(_lib.mig_geometry_fcr(g.h, occ, C.byref(out)))
+    return out.value
+
+
+def mig_geometry_place(g: Geometry, occ: int, profile: int) -> int:
+    out = C.c_int32()
+    _check(_lib.mig_geometry_place(g.h, occ, profile, C.byref(out)))
+    return out.value
+
+
+def policy(g: Geometry | None = None, kind=MIG_FUSION_FISSION, flags=0, ctx_mib=512, reconfig_ticks=500,
+           idle_w=None, w_per_slice=None, z=2.326, eps_num=1, eps_den=100, conv_k=3, min_n=3) -> mig_policy:
+    """A mig_policy; the power model defaults to the geometry's (idle_w, w_per_slice)."""
+    if idle_w is None:
+        idle_w = g.info.idle_w if g is not None else 30
+    if w_per_slice is None:
+        w_per_slice = g.info.w_per_slice if g is not None else 25
+    return mig_policy(kind, flags, ctx_mib, reconfig_ticks, idle_w, w_per_slice, z, eps_num, eps_den, conv_k,
+                      min_n)
+
+
+class Traces:
+    """Device-resident traces: keeps the tensors alive and carries the mig_traces descriptor."""
+
+    def __init__(self, jobs, ext, trace_off, n_traces, seed=0, trace_id0=0, max_jobs=None, n_jobs=None):
+        self.jobs, self.ext, self.trace_off = jobs, ext, trace_off
+        self.n_traces = int(n_traces)
+        self.n_jobs = int(jobs.shape[0]) if n_jobs is None else int(n_jobs)
+        if max_jobs is None:
+            if self.n_traces:
+                max_jobs = int((trace_off[1:] - trace_off[:-1]).max().item())
+            max_jobs = max(1, max_jobs or 1)
+        self.max_jobs = int(max_jobs)
+        self.desc = mig_traces(jobs.data_ptr() if self.n_jobs else None,
+                               ext.data_ptr() if ext is not None else None, trace_off.data_ptr(), self.n_traces,
+                               trace_id0, seed, self.n_jobs, self.max_jobs, 0)
+
+
+def traces_from_numpy(jobs, ext, trace_off, seed=0, trace_id0=0, device=None, max_jobs=None) -> Traces:
+    import torch
+
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    j = torch.from_numpy(np.ascontiguousarray(jobs, np.uint32).view(np.int32)).reshape(-1, 4).to(dev)
+    e = None if ext is None else torch.from_numpy(np.ascontiguousarray(ext, np.uint32).view(np.int32)).reshape(-1, 4).to(dev)
+    o = torch.from_numpy(np.ascontiguousarray(trace_off, np.uint64).view(np.int64)).to(dev)
+    if max_jobs is None:
+        lens = np.diff(np.asarray(trace_off, np.int64))
+        max_jobs = max(1, int(lens.max())) if len(lens) else 1
+    return Traces(j, e, o, len(trace_off) - 1, seed, trace_id0, max_jobs)
+
+
+def _stream_ptr(stream):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _policies(pols):
+    if isinstance(pols, mig_policy):
+        pols = [pols]
+    return (mig_policy * len(pols))(*pols), len(pols)
+
+
+def mig_estimate_memory(g: Geometry, tr: Traces, pol: mig_policy, out=None, stream=None):
+    """Per-job estimates on the device. Returns a uint8 CUDA tensor [n_jobs, 48] (view with ESTIMATE_DTYPE)."""
+    import torch
+
+    if out is None:
+        out = torch.empty((tr.n_jobs, 48), dtype=torch.uint8, device=tr.jobs.device)
+    _check(_lib.mig_estimate_memory(g.h, C.byref(tr.desc), C.byref(pol), C.c_void_p(out.data_ptr()),
+                                    _stream_ptr(stream)))
+    return out
+
+
+def mig_simulate(g: Geometry, tr: Traces, pols, est=None, out=None, totals=None, write_results=True, stream=None):
+    """Simulate every trace under each policy on the device. Returns (results uint8 [n_traces*n_pol, 80] or None,
+    totals uint8 [n_pol, 160]); view on the host with RESULT_DTYPE / TOTALS_DTYPE."""
+    import torch
+
+    parr, n = _policies(pols)
+    dev = tr.jobs.device
+    if out is None and write_results:
+        out = torch.empty((tr.n_traces * n, 80), dtype=torch.uint8, device=dev)
+    if totals is None:
+        totals = torch.empty((n, 160), dtype=torch.uint8, device=dev)
+    _check(_lib.mig_simulate(g.h, C.byref(tr.desc), parr, n,
+                             None if est is None else C.c_void_p(est.data_ptr()),
+                             None if out is None else C.c_void_p(out.data_ptr()), C.c_void_p(totals.data_ptr()),
+                             _stream_ptr(stream)))
+    return out, totals
+
+
+def mig_simulate_host(g: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, max_jobs=None, out=None,
+                      totals=None):
+    """HOST buffers in, HOST results out (page-locked numpy views recommended). Returns (results [n_traces, n_pol]
+    RESULT_DTYPE, totals [n_pol] TOTALS_DTYPE)."""
+    parr, n = _policies(pols)
+    n_traces = len(trace_off) - 1
+    if max_jobs is None:
+        lens = np.diff(np.asarray(trace_off, np.int64))
+        max_jobs = max(1, int(lens.max())) if len(lens) else 1
+    if out is None:
+        out = np.zeros((n_traces, n), RESULT_DTYPE)
+    if totals is None:
+        totals = np.zeros(n, TOTALS_DTYPE)
+    desc = mig_traces(jobs.ctypes.data if len(jobs) else None, None if ext is None else ext.ctypes.data,
+                      trace_off.ctypes.data, n_traces, trace_id0, seed, int(trace_off[-1] - trace_off[0]), max_jobs, 0)
+    _check(_lib.mig_simulate_host(g.h, C.byref(desc), parr, n, out.ctypes.data, totals.ctypes.data))
+    return out, totals
+
+
+def results_numpy(res_tensor, n_pol):
+    """Device results tensor -> numpy [n_traces, n_pol] RESULT_DTYPE."""
+    a = res_tensor.cpu().numpy()
+    return a.view(RESULT_DTYPE).reshape(-1, n_pol)
+
+
+def totals_numpy(tot_tensor):
+    return tot_tensor.cpu().numpy().view(TOTALS_DTYPE).reshape(-1)
+
+
+def estimates_numpy(est_tensor):
+    return est_tensor.cpu().numpy().view(ESTIMATE_DTYPE).reshape(-1)

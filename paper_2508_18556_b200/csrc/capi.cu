@@ -1,0 +1,323 @@
+// capi.cu — the extern "C" entry points of libmig.so (include/mig.h): argument validation, per-device geometry
+// upload, stream-ordered scratch, kernel launches, and the host-buffer pipeline of mig_simulate_host.
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "device_common.cuh"
+
+namespace mig {
+cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_policy& pol, mig_job_estimate* out,
+                            unsigned long long* scratch, int sm_count, bool dyn_only, cudaStream_t stream);
+cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
+                            const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
+                            unsigned long long* counter, const unsigned long long* est_err, int sm_count,
+                            cudaStream_t stream);
+}  // namespace mig
+
+namespace {
+thread_local std::string t_err;
+thread_local uint32_t t_launches = 0;
+
+mig_status cuda_fail(cudaError_t e, const char* what) {
+    return mig_set_error(MIG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int sm_count_of(int dev) {
+    static int cache[64] = {0};
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 148;
+    }
+    return cache[dev];
+}
+
+// Keep stream-ordered scratch in the device's default pool between calls (no release at synchronisation).
+void configure_pool(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+mig_status device_geometry(const mig_geometry* gc, mig::DevGeom** out, int* dev_out) {
+    mig_geometry* g = const_cast<mig_geometry*>(gc);
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "no CUDA device (libmig has no CPU fallback)");
+    if (dev < 0 || dev >= 64) return mig_set_error(MIG_E_UNSUPPORTED, "device ordinal >= 64");
+    std::lock_guard<std::mutex> lock(g->mu);
+    if (!g->dev[dev]) {
+        mig::DevGeom* p = nullptr;
+        e = cudaMalloc(&p, sizeof(mig::DevGeom));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(geometry)");
+        e = cudaMemcpy(p, &g->dg, sizeof(mig::DevGeom), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return cuda_fail(e, "cudaMemcpy(geometry)");
+        }
+        g->dev[dev] = p;
+    }
+    *out = g->dev[dev];
+    *dev_out = dev;
+    configure_pool(dev);
+    return MIG_OK;
+}
+
+mig_status check_traces(const mig_traces* tr) {
+    if (!tr) return mig_set_error(MIG_E_INVALID_ARG, "traces is NULL");
+    if (tr->n_traces > 0 && (!tr->jobs || !tr->trace_off))
+        return mig_set_error(MIG_E_INVALID_ARG, "traces.jobs and traces.trace_off are required");
+    if (tr->max_jobs < 1 || tr->max_jobs > MIG_MAX_JOBS_PER_TRACE)
+        return mig_set_error(MIG_E_INVALID_ARG, "traces.max_jobs must be 1.." +
+                                                    std::to_string(MIG_MAX_JOBS_PER_TRACE));
+    if (tr->reserved != 0) return mig_set_error(MIG_E_INVALID_ARG, "traces.reserved must be 0");
+    return MIG_OK;
+}
+
+mig_status check_policy(const mig_policy& p) {
+    if (p.kind > MIG_FUSION_FISSION) return mig_set_error(MIG_E_INVALID_ARG, "policy.kind out of range");
+    if (p.flags & ~7u) return mig_set_error(MIG_E_INVALID_ARG, "unknown policy flag");
+    if (p.flags & MIG_EWMA_REUSE)
+        return mig_set_error(MIG_E_UNSUPPORTED, "MIG_EWMA_REUSE is not implemented on the device path");
+    if (p.min_n < 3) return mig_set_error(MIG_E_INVALID_ARG, "policy.min_n must be >= 3");
+    if (p.conv_k < 1 || p.conv_k > 32) return mig_set_error(MIG_E_INVALID_ARG, "policy.conv_k must be 1..32");
+    if (p.eps_den == 0) return mig_set_error(MIG_E_INVALID_ARG, "policy.eps_den must be > 0");
+    if (!(p.z >= 0.0 && p.z < 1e6)) return mig_set_error(MIG_E_INVALID_ARG, "policy.z must be in [0, 1e6)");
+    return MIG_OK;
+}
+
+mig_status check_policies(const mig_geometry* g, const mig_policy* pols, uint32_t n) {
+    if (!pols || n < 1 || n > (uint32_t)mig::kMaxPolicies)
+        return mig_set_error(MIG_E_INVALID_ARG, "n_policies must be 1..8");
+    for (uint32_t i = 0; i < n; ++i) {
+        mig_status s = check_policy(pols[i]);
+        if (s != MIG_OK) return s;
+        if (pols[i].kind == MIG_STATIC && g->dg.n_layout == 0)
+            return mig_set_error(MIG_E_INVALID_ARG, "MIG_STATIC needs a geometry with a static_layout");
+        const mig_policy& a = pols[0];
+        const mig_policy& b = pols[i];
+        if (a.ctx_mib != b.ctx_mib || a.z != b.z || a.eps_num != b.eps_num || a.eps_den != b.eps_den ||
+            a.conv_k != b.conv_k || a.min_n != b.min_n)
+            return mig_set_error(MIG_E_INVALID_ARG,
+                                 "policies of one mig_simulate call must share ctx_mib, z, eps, conv_k, min_n");
+    }
+    return MIG_OK;
+}
+
+// Device path shared by mig_simulate and the host pipeline. scratch must hold 3 zeroed u64 counters.
+mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, const mig_traces& tr,
+                           const mig_policy* pols, uint32_t n_pol, const mig_job_estimate* est,
+                           mig_job_estimate* est_scratch, mig_trace_result* out, mig_policy_totals* totals,
+                           unsigned long long* counters, cudaStream_t s) {
+    cudaError_t e;
+    uint32_t launches = 0;
+    if (!est) {
+        e = mig::launch_estimate(g->dg, tr, pols[0], est_scratch, counters, sm_count_of(dev), true, s);
+        if (e != cudaSuccess) return cuda_fail(e, "k_estimate launch");
+        ++launches;
+        est = est_scratch;
+    }
+    e = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1, sm_count_of(dev), s);
+    if (e != cudaSuccess) return cuda_fail(e, "k_simulate launch");
+    ++launches;
+    t_launches += launches;
+    return MIG_OK;
+}
+
+}  // namespace
+
+mig_status mig_set_error(mig_status s, const std::string& msg) {
+    t_err = msg;
+    return s;
+}
+
+void mig_note_launches(uint32_t n) { t_launches += n; }
+
+mig_geometry::~mig_geometry() {
+    for (int d = 0; d < 64; ++d)
+        if (dev[d]) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(d);
+            cudaFree(dev[d]);
+            cudaSetDevice(cur);
+        }
+}
+
+extern "C" {
+
+const char* mig_last_error(void) { return t_err.c_str(); }
+
+uint32_t mig_last_launch_count(void) { return t_launches; }
+
+mig_status mig_estimate_memory(const mig_geometry* g, const mig_traces* traces, const mig_policy* policy,
+                               mig_job_estimate* out, void* stream) {
+    t_launches = 0;
+    if (!g || !policy) return mig_set_error(MIG_E_INVALID_ARG, "mig_estimate_memory: null argument");
+    mig_status st = check_traces(traces);
+    if (st != MIG_OK) return st;
+    st = check_policy(*policy);
+    if (st != MIG_OK) return st;
+    if (traces->n_traces == 0) return MIG_OK;
+    if (!out) return mig_set_error(MIG_E_INVALID_ARG, "mig_estimate_memory: out is NULL");
+    mig::DevGeom* Gdev;
+    int dev;
+    st = device_geometry(g, &Gdev, &dev);
+    if (st != MIG_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, 2 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scratch)");
+    cudaMemsetAsync(scratch, 0, 2 * sizeof(unsigned long long), s);
+    e = mig::launch_estimate(g->dg, *traces, *policy, out, scratch, sm_count_of(dev), false, s);
+    cudaFreeAsync(scratch, s);
+    if (e != cudaSuccess) return cuda_fail(e, "k_estimate launch");
+    t_launches = 1;
+    return MIG_OK;
+}
+
+mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const mig_policy* policies,
+                        uint32_t n_policies, const mig_job_estimate* est, mig_trace_result* out,
+                        mig_policy_totals* totals, void* stream) {
+    t_launches = 0;
+    if (!g) return mig_set_error(MIG_E_INVALID_ARG, "mig_simulate: geometry is NULL");
+    mig_status st = check_traces(traces);
+    if (st != MIG_OK) return st;
+    st = check_policies(g, policies, n_policies);
+    if (st != MIG_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    mig::DevGeom* Gdev;
+    int dev;
+    st = device_geometry(g, &Gdev, &dev);
+    if (st != MIG_OK) return st;
+    if (totals) {
+        cudaError_t e = cudaMemsetAsync(totals, 0, sizeof(mig_policy_totals) * n_policies, s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(totals)");
+    }
+    if (traces->n_traces == 0) return MIG_OK;
+    size_t est_bytes = est ? 0 : traces->n_jobs * sizeof(mig_job_estimate);
+    uint8_t* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, 64 + est_bytes, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scratch)");
+    e = cudaMemsetAsync(scratch, 0, 64, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(scratch)");
+    st = simulate_device(g, Gdev, dev, *traces, policies, n_policies, est,
+                         est ? nullptr : reinterpret_cast<mig_job_estimate*>(scratch + 64), out, totals,
+                         reinterpret_cast<unsigned long long*>(scratch), s);
+    cudaFreeAsync(scratch, s);
+    return st;
+}
+
+mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, const mig_policy* policies,
+                             uint32_t n_policies, mig_trace_result* out, mig_policy_totals* totals) {
+    t_launches = 0;
+    if (!g) return mig_set_error(MIG_E_INVALID_ARG, "mig_simulate_host: geometry is NULL");
+    mig_status st = check_traces(traces);
+    if (st != MIG_OK) return st;
+    st = check_policies(g, policies, n_policies);
+    if (st != MIG_OK) return st;
+    mig::DevGeom* Gdev;
+    int dev;
+    st = device_geometry(g, &Gdev, &dev);
+    if (st != MIG_OK) return st;
+    const mig_traces& T = *traces;
+    if (totals) memset(totals, 0, sizeof(mig_policy_totals) * n_policies);
+    if (T.n_traces == 0) return MIG_OK;
+    // chunking: ~16M jobs per chunk, two chunks in flight on two streams
+    uint64_t chunk_jobs = 16ull << 20;
+    if (const char* env = getenv("MIG_HOST_CHUNK_JOBS")) chunk_jobs = std::max<uint64_t>(1, strtoull(env, nullptr, 10));
+    const uint64_t chunk_traces = std::max<uint64_t>(1, chunk_jobs / T.max_jobs);
+    const uint64_t n_chunks = (T.n_traces + chunk_traces - 1) / chunk_traces;
+    const uint64_t chunk_jobs_cap = chunk_traces * T.max_jobs;
+    const size_t jb = chunk_jobs_cap * 16, eb = T.jobs_ext ? chunk_jobs_cap * 16 : 0,
+                 ob = (chunk_traces + 1) * 8, esb = chunk_jobs_cap * sizeof(mig_job_estimate),
+                 rb = chunk_traces * n_policies * sizeof(mig_trace_result),
+                 tb = n_policies * sizeof(mig_policy_totals);
+    const size_t per = jb + eb + ob + esb + rb + tb + 64;
+    cudaStream_t ss[2];
+    uint8_t* buf[2] = {nullptr, nullptr};
+    std::vector<mig_policy_totals> host_tot(n_chunks * n_policies);
+    cudaError_t e = cudaSuccess;
+    for (int k = 0; k < 2; ++k) {
+        if ((e = cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(e, "cudaStreamCreate");
+        if ((e = cudaMallocAsync(&buf[k], per, ss[k])) != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    }
+    const uint64_t* off = T.trace_off;
+    for (uint64_t c = 0; c < n_chunks && st == MIG_OK; ++c) {
+        const int k = (int)(c & 1);
+        cudaStream_t s = ss[k];
+        uint8_t* b = buf[k];
+        const uint64_t t0 = c * chunk_traces, t1 = std::min<uint64_t>(T.n_traces, t0 + chunk_traces);
+        const uint64_t nt = t1 - t0, jlo = off[t0] - off[0], jhi = off[t1] - off[0], nj = jhi - jlo;
+        if (nj > chunk_jobs_cap) {
+            st = mig_set_error(MIG_E_INVALID_ARG, "a trace exceeds max_jobs");
+            break;
+        }
+        uint8_t* d_jobs = b;
+        uint8_t* d_ext = b + jb;
+        uint64_t* d_off = reinterpret_cast<uint64_t*>(b + jb + eb);
+        mig_job_estimate* d_est = reinterpret_cast<mig_job_estimate*>(b + jb + eb + ob);
+        mig_trace_result* d_out = reinterpret_cast<mig_trace_result*>(b + jb + eb + ob + esb);
+        mig_policy_totals* d_tot = reinterpret_cast<mig_policy_totals*>(b + jb + eb + ob + esb + rb);
+        unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(b + jb + eb + ob + esb + rb + tb);
+        e = cudaMemcpyAsync(d_jobs, (const uint8_t*)T.jobs + jlo * 16, nj * 16, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && T.jobs_ext)
+            e = cudaMemcpyAsync(d_ext, (const uint8_t*)T.jobs_ext + jlo * 16, nj * 16, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_off, off + t0, (nt + 1) * 8, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, 64, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_tot, 0, tb, s);
+        if (e != cudaSuccess) {
+            st = cuda_fail(e, "host pipeline H2D");
+            break;
+        }
+        mig_traces ct = T;
+        ct.jobs = d_jobs;
+        ct.jobs_ext = T.jobs_ext ? d_ext : nullptr;
+        ct.trace_off = d_off;
+        ct.n_traces = nt;
+        ct.trace_id0 = T.trace_id0 + t0;
+        ct.n_jobs = nj;
+        st = simulate_device(g, Gdev, dev, ct, policies, n_policies, nullptr, d_est, d_out, d_tot, d_cnt, s);
+        if (st != MIG_OK) break;
+        if (out)
+            e = cudaMemcpyAsync(out + t0 * n_policies, d_out, nt * n_policies * sizeof(mig_trace_result),
+                                cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(host_tot.data() + c * n_policies, d_tot, tb, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) st = cuda_fail(e, "host pipeline D2H");
+    }
+    for (int k = 0; k < 2; ++k) {
+        cudaFreeAsync(buf[k], ss[k]);
+        e = cudaStreamSynchronize(ss[k]);
+        if (e != cudaSuccess && st == MIG_OK) st = cuda_fail(e, "host pipeline");
+        cudaStreamDestroy(ss[k]);
+    }
+    if (st != MIG_OK) return st;
+    if (totals) {
+        for (uint64_t c = 0; c < n_chunks; ++c)
+            for (uint32_t p = 0; p < n_policies; ++p) {
+                const uint64_t* src = reinterpret_cast<const uint64_t*>(&host_tot[c * n_policies + p]);
+                uint64_t* dst = reinterpret_cast<uint64_t*>(&totals[p]);
+                for (int f = 0; f < 20; ++f) {
+                    if (f == 13) dst[f] = std::max(dst[f], src[f]);
+                    else if (f == 18) dst[f] |= src[f];
+                    else dst[f] += src[f];
+                }
+            }
+    }
+    return MIG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+// estimate.cu — k_estimate: per-job memory estimation.
+//
+//   STATIC / MODEL jobs: req0 = estimate + workspace + context (compile-time analysis PAPER.md:210, model-size
+//   estimation PAPER.md:214, :569; context PAPER.md:345-346; workspace PAPER.md:358-362). The true footprint
+//   exceeds a memory level l at iteration 1 or never (R12).
+//   DYNAMIC jobs: Alg. 3 PeakMemoryPrediction over the per-iteration samples, plus the
+//   first-exceed iteration of every memory level (where the job would OOM).
+//
+// Layout: one warp per trace (persistent CTAs, atomic trace counter). Lanes take the trace's jobs 32 at a time;
+// each DYNAMIC job is then processed by the whole warp, lanes over iterations: lane i draws sample base+i+1
+// in-kernel (counter-based generator, tracegen.h), the exact integer moments Sum y, Sum t*y, Sum y^2, Sum q,
+// Sum t*q are warp inclusive scans (__shfl_up_sync), every lane evaluates the forecast P_n for its own n, the
+// convergence rule becomes a run of conv_k set bits in a 64-bit window of two __ballot_sync masks, and each
+// level's first exceed is one __ballot_sync + __ffs. Arithmetic follows DESIGN.md "Canonical arithmetic"
+// (exact int64/int128 moments, one fixed sequence of IEEE double operations, no FMA contraction).
+#include "device_common.cuh"
+#include "../../tracegen/tracegen.h"  // input generator only: the samples a dynamic job reports
+
+namespace mig {
+
+struct EstParams {
+    const uint4* jobs;
+    const uint4* ext;
+    const uint64_t* off;
+    uint64_t n_traces, trace_id0, seed;
+    mig_job_estimate* out;
+    unsigned long long* counter;
+    unsigned long long* err;
+    uint32_t ctx, eps_num, eps_den, conv_k, min_n;
+    uint32_t dyn_only;  // skip writing STATIC/MODEL estimates (mig_simulate recomputes them while staging)
+    double z;
+};
+
+struct FitOut {
+    int64_t P;
+    double phi, a, sigma;
+};
+
+// One fit + forecast at n samples (oracle: fit_and_predict).
+__device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int64_t Syy, int64_t Sq, int64_t Stq,
+                                         int64_t T, double z, int64_t ws_ctx) {
+    const int64_t n2m1 = n * n - 1;
+    const int64_t D = n * n2m1;
+    const int64_t Ky = 2 * Sty - (n + 1) * Sy;
+    const int64_t Kq = 2 * Stq - (n + 1) * Sq;
+    const int64_t h = 2 * T - n - 1;
+    __int128 numY = (__int128)Sy * n2m1 + (__int128)3 * Ky * h;
+    __int128 ssrN = (__int128)n2m1 * ((__int128)n * Syy - (__int128)Sy * Sy) - (__int128)3 * Ky * Ky;
+    __int128 numQ = (__int128)Sq * n2m1 + (__int128)3 * Kq * h;
+    const double den = __ll2double_rn(D);
+    FitOut f;
+    double yT = __ddiv_rn(i128_to_double(numY), den);
+    double var = __ddiv_rn(i128_to_double(ssrN), __ll2double_rn(D * (n - 2)));
+    f.sigma = __dsqrt_rn(var);
+    double u = __dadd_rn(yT, __dmul_rn(z, f.sigma));
+    if (u < 0.0) u = 0.0;
+    double V = __ddiv_rn(__ddiv_rn(i128_to_double(numQ), den), 65536.0);
+    if (V < 1.0) V = 1.0;
+    f.phi = __ddiv_rn(u, V);
+    f.a = __ddiv_rn(__ll2double_rn(6 * Ky), den);
+    f.P = (int64_t)ceil(f.phi) + ws_ctx;
+    return f;
+}
+
+__device__ __forceinline__ void store_estimate(mig_job_estimate* dst, uint32_t req0, uint32_t pred, uint32_t conv,
+                                               uint32_t n_levels, const uint32_t fe[5], double phi, double a,
+                                               double sigma) {
+    uint4 w0 = make_uint4(req0, pred, (conv & 0xFFFFu) | (n_levels << 16), fe[0] | (fe[1] << 16));
+    uint4 w1 = make_uint4(fe[2] | (fe[3] << 16), fe[4] | (kNever << 16), __double2loint(phi), __double2hiint(phi));
+    uint4 w2 = make_uint4(__double2loint(a), __double2hiint(a), __double2loint(sigma), __double2hiint(sigma));
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    d[0] = w0;
+    d[1] = w1;
+    d[2] = w2;
+}
+
+// Whole-warp estimation of one DYNAMIC job (lanes over iterations).
+__device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t trace_id, uint32_t jidx, uint4 r,
+                                 uint4 e, uint32_t lane, mig_job_estimate* dst) {
+    const uint32_t T = r.z & 0xFFFFu;
+    const uint32_t b = r.x, q0 = r.y, ws = e.x, slope = e.z, sigma_n = e.w & 0xFFFFu, qs = e.w >> 16;
+    const uint64_t key = tg_key(P.seed, trace_id, jidx);
+    const int64_t ws_ctx = (int64_t)ws + P.ctx;
+    int64_t thr[kMaxLevels];
+    uint32_t fe[5] = {kNever, kNever, kNever, kNever, kNever};
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) thr[l] = (int64_t)G.level_mem[l] - ws_ctx;  // phys > L <=> floor > thr
+    uint32_t fe_left = G.n_levels;
+    int64_t Sy = 0, Sty = 0, Syy = 0, Sq = 0, Stq = 0, Plast = 0;
+    uint32_t okprev = 0, conv = 0, pred = 0;
+    double phi = 0.0, a = 0.0, sig = 0.0;
+    bool done_pred = T < P.min_n;
+    bool bad = false;
+    for (uint32_t base = 0; base < T; base += 32) {
+        if (done_pred && fe_left == 0) break;
+        const uint32_t n = base + lane + 1;
+        const bool valid = n <= T;
+        uint32_t y = 0, q = 0;
+        if (valid) {
+            tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
+            bad |= (q == 0) | (y >= (1u << 18));
+        }
+        // first-exceed iteration of every memory level (R12): phys(i) = floor(y*65536/q) + ws + ctx > L
+        if (fe_left) {
+#pragma unroll
+            for (int l = 0; l < kMaxLevels; ++l) {
+                if (l < (int)G.n_levels && fe[l] == kNever) {
+                    bool over = valid && (thr[l] < 0 || (uint64_t)y * 65536ull >= (uint64_t)(thr[l] + 1) * q);
+                    uint32_t m = __ballot_sync(FULL, over);
+                    if (m) {
+                        fe[l] = base + __ffs(m);
+                        --fe_left;
+                    }
+                }
+            }
+        }
+        if (done_pred) continue;
+        // exact integer moments at n = base + lane + 1 (inclusive warp scans + carried totals)
+        const int64_t yi = y, qi = q, ni = n;
+        const int64_t sy = Sy + warp_scan_i64(yi, lane);
+        const int64_t sty = Sty + warp_scan_i64(valid ? ni * yi : 0, lane);
+        const int64_t syy = Syy + warp_scan_i64(yi * yi, lane);
+        const int64_t sq = Sq + warp_scan_i64(qi, lane);
+        const int64_t stq = Stq + warp_scan_i64(valid ? ni * qi : 0, lane);
+        const bool has = valid && n >= P.min_n;
+        FitOut f = {0, 0.0, 0.0, 0.0};
+        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx);
+        int64_t Pprev = __shfl_up_sync(FULL, f.P, 1);
+        if (lane == 0) Pprev = Plast;
+        const bool prev_has = n >= P.min_n + 1;
+        const int64_t diff = f.P > Pprev ? f.P - Pprev : Pprev - f.P;
+        const bool ok = has && prev_has && (int64_t)P.eps_den * diff < (int64_t)P.eps_num * Pprev;
+        const uint32_t M = __ballot_sync(FULL, ok);
+        // converged at n <=> the last conv_k relative changes (n-conv_k+1 .. n) were all small (R24)
+        const uint64_t X = ((uint64_t)M << 32) | okprev;
+        uint64_t Y = X;
+        for (uint32_t d = 1; d < P.conv_k; ++d) Y &= X << d;
+        const uint32_t cm = (uint32_t)(Y >> 32);
+        const uint32_t last_lane = (T - 1 - base) < 32 ? (T - 1 - base) : 31;
+        const uint32_t src = cm ? (uint32_t)(__ffs(cm) - 1) : last_lane;
+        const int64_t Ps = __shfl_sync(FULL, f.P, src);
+        const double phs = __shfl_sync(FULL, f.phi, src), as = __shfl_sync(FULL, f.a, src),
+                     ss = __shfl_sync(FULL, f.sigma, src);
+        if (cm) {
+            conv = base + src + 1;
+            pred = (uint32_t)Ps;
+            phi = phs;
+            a = as;
+            sig = ss;
+            done_pred = true;
+        } else {
+            if (base + 32 >= T && T >= P.min_n) {  // last chunk, never converged: diagnostics of the fit at n = T
+                phi = phs;
+                a = as;
+                sig = ss;
+            }
+            Sy = __shfl_sync(FULL, sy, 31);
+            Sty = __shfl_sync(FULL, sty, 31);
+            Syy = __shfl_sync(FULL, syy, 31);
+            Sq = __shfl_sync(FULL, sq, 31);
+            Stq = __shfl_sync(FULL, stq, 31);
+            Plast = __shfl_sync(FULL, f.P, 31);
+            okprev = M;
+        }
+    }
+    if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
+    if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig);
+}
+
+__global__ void __launch_bounds__(256) k_estimate(const DevGeom G, const EstParams P) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t j_base = P.off[0];
+    for (;;) {
+        unsigned long long tr = 0;
+        if (lane == 0) tr = atomicAdd(P.counter, 1ull);
+        tr = __shfl_sync(FULL, tr, 0);
+        if (tr >= P.n_traces) break;
+        const uint64_t j0 = P.off[tr] - j_base;
+        const uint32_t n = (uint32_t)(P.off[tr + 1] - P.off[tr]);
+        for (uint32_t c = 0; c < n; c += 32) {
+            const uint32_t j = c + lane;
+            const bool valid = j < n;
+            uint4 r = make_uint4(0, 0, 0, 0), e = make_uint4(0, 0, 0, 0);
+            if (valid) {
+                r = __ldg(P.jobs + j0 + j);
+                if (P.ext) e = __ldg(P.ext + j0 + j);
+            }
+            const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
+            if (valid && (cls > 2 || T > 4096 || (r.z >> 24) != 0)) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
+            if (valid && cls != kClassDynamic && !P.dyn_only) {
+                const uint64_t phys = (uint64_t)r.y + e.x + P.ctx;
+                uint32_t fe[5];
+#pragma unroll
+                for (int l = 0; l < kMaxLevels; ++l)
+                    fe[l] = (l < (int)G.n_levels && T >= 1 && phys > G.level_mem[l]) ? 1u : kNever;
+                store_estimate(P.out + j0 + j, r.x + e.x + P.ctx, 0, 0, G.n_levels, fe, 0.0, 0.0, 0.0);
+            }
+            uint32_t dm = __ballot_sync(FULL, valid && cls == kClassDynamic);
+            while (dm) {
+                const uint32_t L = (uint32_t)__ffs(dm) - 1;
+                dm &= dm - 1;
+                uint4 rr, ee;
+                rr.x = __shfl_sync(FULL, r.x, L);
+                rr.y = __shfl_sync(FULL, r.y, L);
+                rr.z = __shfl_sync(FULL, r.z, L);
+                rr.w = __shfl_sync(FULL, r.w, L);
+                ee.x = __shfl_sync(FULL, e.x, L);
+                ee.y = __shfl_sync(FULL, e.y, L);
+                ee.z = __shfl_sync(FULL, e.z, L);
+                ee.w = __shfl_sync(FULL, e.w, L);
+                estimate_dynamic(G, P, P.trace_id0 + tr, c + L, rr, ee, lane, P.out + j0 + c + L);
+            }
+        }
+    }
+}
+
+cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_policy& pol, mig_job_estimate* out,
+                            unsigned long long* scratch /* [counter, err] zeroed */, int sm_count,
+                            bool dyn_only, cudaStream_t stream) {
+    EstParams P;
+    P.jobs = (const uint4*)tr.jobs;
+    P.ext = (const uint4*)tr.jobs_ext;
+    P.off = tr.trace_off;
+    P.n_traces = tr.n_traces;
+    P.trace_id0 = tr.trace_id0;
+    P.seed = tr.seed;
+    P.out = out;
+    P.counter = scratch;
+    P.err = scratch + 1;
+    P.ctx = pol.ctx_mib;
+    P.eps_num = pol.eps_num;
+    P.eps_den = pol.eps_den;
+    P.conv_k = pol.conv_k;
+    P.min_n = pol.min_n;
+    P.z = pol.z;
+    P.dyn_only = dyn_only ? 1u : 0u;
+    const int threads = 256;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate, threads, 0);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t want = (tr.n_traces + 7) / 8;
+    uint64_t blocks = (uint64_t)per_sm * sm_count;
+    if (want < blocks) blocks = want;
+    if (blocks < 1) blocks = 1;
+    k_estimate<<<(unsigned)blocks, threads, 0, stream>>>(G, P);
+    return cudaGetLastError();
+}
+
+}  // namespace mig

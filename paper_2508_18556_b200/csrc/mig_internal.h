@@ -1,0 +1,52 @@
+// mig_internal.h — internal structures of libmig.so (not part of the C ABI).
+#pragma once
+
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mig.h"
+
+namespace mig {
+
+constexpr int kMaxSlots = MIG_MAX_SLOTS;
+constexpr int kMaxProf = MIG_MAX_PROFILES;
+constexpr int kMaxLevels = MIG_MAX_LEVELS;
+constexpr int kMaxPlace = 8;  // starts per profile (<= slots)
+
+// Geometry parameter block passed BY VALUE to every kernel (lives in the constant bank; uniform-index reads are
+// free, lane-divergent tables are copied to shared memory by the kernel prologue).
+struct DevGeom {
+    uint32_t n_slots, slot_mib, n_compute, n_prof, n_levels, full_prof, full_mem;
+    uint32_t n_layout;
+    uint32_t mem[16];        // profile memory MiB
+    uint32_t comp[16];       // profile compute slices
+    uint32_t lenmask[16];    // (1 << memory_slots) - 1
+    uint32_t level[16];      // index of mem[p] among the distinct memory levels
+    uint32_t wave_cap[16];   // sms_per_slice * comp * warps_per_sm (warp folding, R30)
+    uint32_t n_place[16];    // legal starts per profile
+    uint32_t place[16][8];   // start | (mask << 8)
+    uint32_t level_mem[8];   // distinct memories, ascending
+    uint32_t level_next[8];  // next larger memory after level l (0 = none, R14)
+    uint32_t layout_prof[8], layout_start[8];
+    uint16_t fcr[256];       // fcr by occupancy mask (0 = not a valid occupancy)
+};
+
+}  // namespace mig
+
+struct mig_geometry {
+    std::string name;
+    mig_geometry_info info;
+    std::vector<std::string> prof_names;
+    mig::DevGeom dg;
+    uint32_t sms_per_slice = 0, warps_per_sm = 0;
+    std::mutex mu;                     // guards dev[]
+    mig::DevGeom* dev[64] = {};        // per-device copy, uploaded on first use
+    ~mig_geometry();
+};
+
+// error helpers (capi.cu)
+mig_status mig_set_error(mig_status s, const std::string& msg);
+void mig_note_launches(uint32_t n);

@@ -1,0 +1,204 @@
+"""GPU parity: the CUDA path (libmig.so through its C ABI) against the CPU oracle, element by element.
+
+Bar (north_star): every integer field of every (trace, policy) result — makespan, counts, energy W*ticks,
+turnaround, busy slice-ticks and the 64-bit hash of every placement decision and event time — is bit-exact.
+Estimate doubles (phi, a, sigma) must agree within 1e-6 relative (they are expected to be bit-identical: both
+sides run the same canonical IEEE sequence).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN_DIR, geom_path
+from oracle import oracle as orc
+from tracegen import tracegen as tg
+
+import paper_2508_18556_b200 as mig
+
+pytestmark = pytest.mark.gpu
+
+SPECS = [dict(kind=0), dict(kind=1), dict(kind=2), dict(kind=3), dict(kind=3, flags=1)]
+
+
+def run_pair(geo, jobs, ext, off, specs, seed=0, common=None, max_jobs=None):
+    common = common or {}
+    g = mig.mig_geometry_load(f"builtin:{geo}")
+    og = orc.Geometry(geom_path(geo))
+    pols = [mig.policy(g, **s, **common) for s in specs]
+    opols = [orc.policy(**s, **common) for s in specs]
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=seed, max_jobs=max_jobs)
+    res, tot = mig.mig_simulate(g, tr, pols)
+    torch.cuda.synchronize()
+    got = mig.results_numpy(res, len(pols))
+    want = orc.simulate(og, jobs, ext, off, opols, seed=seed)
+    return got, want, mig.totals_numpy(tot)
+
+
+def assert_same(got, want):
+    assert got.shape == want.shape
+    for f in orc.RESULT_DTYPE.names:
+        if not np.array_equal(got[f], want[f]):
+            bad = tuple(np.argwhere(got[f] != want[f])[0])
+            pytest.fail(f"field {f} differs at (trace, policy) {bad}: gpu {got[f][bad]} oracle {want[f][bad]}")
+
+
+def check_totals(got, tot):
+    for p in range(got.shape[1]):
+        r = got[:, p]
+        t = tot[p]
+        assert t["n_traces"] == len(r) and t["error_flags"] == 0
+        for f in ["n_jobs", "completed", "rejected", "failed", "ooms", "preempts", "restarts", "placements",
+                  "waits", "creates", "destroys", "energy_wticks", "turnaround_sum", "busy_slice_ticks"]:
+            assert int(t[f]) == int(r[f].astype(np.uint64).sum()), f
+        assert int(t["makespan_sum"]) == int(r["makespan"].astype(np.uint64).sum())
+        assert int(t["makespan_max"]) == int(r["makespan"].max(initial=0))
+        assert int(t["decision_hash_sum"]) == int(r["decision_hash"].astype(np.uint64).sum(dtype=np.uint64))
+
+
+def test_config1_example_w_all_policies():
+    with open(os.path.join(GOLDEN_DIR, "config1_w.json")) as f:
+        fx = json.load(f)
+    tr = [tg.pack_job(j["est_gb"] * 1024, j["true_gb"] * 1024, j["iters"], 0, j["iter_ticks"]) for j in fx["jobs_gb"]]
+    jobs, ext, off = tg.pack_traces([tr])
+    specs = [dict(kind=k) for k in range(4)]
+    got, want, tot = run_pair("a30-24gb", jobs, ext, off, specs, common=fx["policy_common"])
+    assert_same(got, want)
+    assert got[0, 3]["makespan"] == 220 and got[0, 3]["energy_wticks"] == 27100
+    check_totals(got, tot)
+
+
+@pytest.mark.parametrize("cfg,n", [(2, 400), (3, 600), (4, 3000), (5, 300)])
+def test_generated_configs_all_policies(cfg, n):
+    jobs, ext, off = tg.generate_host(cfg, n)
+    got, want, tot = run_pair(tg.CONFIG_GEOMETRY[cfg], jobs, ext, off, SPECS, seed=tg.seed_of(cfg))
+    assert_same(got, want)
+    check_totals(got, tot)
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 300), (4, 2000), (5, 200)])
+def test_estimates_match_oracle(cfg, n):
+    jobs, ext, off = tg.generate_host(cfg, n)
+    geo = tg.CONFIG_GEOMETRY[cfg]
+    g = mig.mig_geometry_load(f"builtin:{geo}")
+    og = orc.Geometry(geom_path(geo))
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=tg.seed_of(cfg))
+    est = mig.estimates_numpy(mig.mig_estimate_memory(g, tr, mig.policy(g)))
+    want = orc.estimate(og, jobs, ext, off, orc.policy(), seed=tg.seed_of(cfg))
+    for f in ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe"]:
+        assert np.array_equal(est[f], want[f]), f
+    for f in ["phi", "a", "sigma"]:
+        np.testing.assert_allclose(est[f], want[f], rtol=1e-6, atol=1e-9)
+        assert np.array_equal(est[f], want[f]), f"{f} not bit-identical"
+    dyn = ((jobs[:, 2] >> 16) & 0xFF) == 2
+    assert dyn.any() and (est["conv_iter"][dyn] > 0).any()
+
+
+def random_tiny_traces(rng, geo_spec, n_traces, max_len, dyn_frac=0.3):
+    slot = geo_spec["slot_mib"]
+    full = geo_spec["total_memory_slots"] * slot
+    traces = []
+    for _ in range(n_traces):
+        tr = []
+        for _ in range(int(rng.integers(0, max_len + 1))):
+            if rng.random() < dyn_frac:
+                b = int(rng.integers(100, full // 3))
+                T = int(rng.integers(1, 300))
+                tr.append(tg.pack_job(b, 65536, T, 2, int(rng.integers(1, 50)), ws=int(rng.integers(0, 64)),
+                                      slope_q8=int(rng.integers(0, 200 * 256)), sigma=int(rng.integers(0, 200)),
+                                      qslope=int(rng.integers(0, 100))))
+            else:
+                est = int(rng.integers(1, full + 4000))
+                tru = est if rng.random() < 0.6 else int(rng.integers(1, full + 4000))
+                tr.append(tg.pack_job(est, tru, int(rng.integers(0, 6)), int(rng.integers(0, 2)),
+                                      int(rng.integers(1, 2000)), ws=int(rng.integers(0, 100)),
+                                      warps=int(rng.integers(0, 20000))))
+        traces.append(tr)
+    return tg.pack_traces(traces)
+
+
+@pytest.mark.parametrize("geo", ["a30-24gb", "a100-40gb", "a100-40gb-1g10", "h100-80gb"])
+def test_random_ragged_traces_edge_cases(geo):
+    # empty traces, ragged lengths, zero-iteration jobs, rejections, failures at the full GPU, warp folding
+    spec = json.load(open(geom_path(geo)))
+    rng = np.random.default_rng(5)
+    jobs, ext, off = random_tiny_traces(rng, spec, 500, 40)
+    specs = SPECS + [dict(kind=3, flags=2), dict(kind=3, flags=3), dict(kind=1, flags=3)]
+    for common in [dict(ctx_mib=0, reconfig_ticks=0), dict(ctx_mib=512, reconfig_ticks=500, z=1.0)]:
+        got, want, tot = run_pair(geo, jobs, ext, off, specs, seed=99, common=common)
+        assert_same(got, want)
+        check_totals(got, tot)
+
+
+def test_max_length_trace():
+    rng = np.random.default_rng(8)
+    tr = []
+    for _ in range(mig.MIG_MAX_JOBS_PER_TRACE):
+        tr.append(tg.pack_job(int(rng.integers(1, 30000)), int(rng.integers(1, 30000)), 1, 0,
+                              int(rng.integers(1, 100))))
+    jobs, ext, off = tg.pack_traces([tr, [], tr[:17]])
+    got, want, tot = run_pair("a100-40gb", jobs, ext, off, SPECS, max_jobs=mig.MIG_MAX_JOBS_PER_TRACE)
+    assert_same(got, want)
+
+
+def test_trace_longer_than_max_jobs_is_flagged():
+    tr = [tg.pack_job(1000, 1000, 1, 0, 10)] * 10
+    jobs, ext, off = tg.pack_traces([tr])
+    g = mig.mig_geometry_load("builtin:a100-40gb")
+    t = mig.traces_from_numpy(jobs, ext, off, max_jobs=4)
+    _, tot = mig.mig_simulate(g, t, [mig.policy(g)])
+    assert mig.totals_numpy(tot)[0]["error_flags"] & 1
+
+
+def test_host_pipeline_matches_device(monkeypatch):
+    monkeypatch.setenv("MIG_HOST_CHUNK_JOBS", "5000")  # force many pipelined chunks
+    cfg, n = 3, 700
+    jobs, ext, off = tg.generate_host(cfg, n)
+    g = mig.mig_geometry_load(f"builtin:{tg.CONFIG_GEOMETRY[cfg]}")
+    pols = [mig.policy(g, **s) for s in SPECS]
+    hres, htot = mig.mig_simulate_host(g, jobs, ext, off, pols, seed=tg.seed_of(cfg))
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=tg.seed_of(cfg))
+    res, tot = mig.mig_simulate(g, tr, pols)
+    assert np.array_equal(hres, mig.results_numpy(res, len(pols)))
+    assert np.array_equal(htot, mig.totals_numpy(tot))
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_device_generator_equals_host(cfg):
+    n = 3000
+    hj, he, ho = tg.generate_host(cfg, n, trace_id0=12345)
+    dj, de, do = tg.generate_device(cfg, n, trace_id0=12345)
+    torch.cuda.synchronize()
+    assert np.array_equal(dj.cpu().numpy().view(np.uint32), hj)
+    if he is not None:
+        assert np.array_equal(de.cpu().numpy().view(np.uint32), he)
+    assert np.array_equal(do.cpu().numpy().view(np.uint64), ho)
+
+
+@pytest.mark.parametrize("cfg,n_full,n_sample", [(2, 1_000_000, 1500), (3, 1_000_000, 1500), (4, 2_000_000, 4000)])
+def test_full_size_sampled_parity(cfg, n_full, n_sample):
+    """BASELINE.json sizes (C4 at 1/5 to bound memory) in the launch configuration bench.py uses: device-generated
+    traces, all policies in one call; sampled traces are regenerated on the host and run through the oracle."""
+    geo = tg.CONFIG_GEOMETRY[cfg]
+    g = mig.mig_geometry_load(f"builtin:{geo}")
+    og = orc.Geometry(geom_path(geo))
+    seed = tg.seed_of(cfg)
+    dj, de, do = tg.generate_device(cfg, n_full)
+    tr = mig.Traces(dj, de, do, n_full, seed=seed, max_jobs=tg.jobs_per_trace(cfg))
+    pols = [mig.policy(g, **s) for s in SPECS]
+    res, tot = mig.mig_simulate(g, tr, pols)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(cfg)
+    idx = np.unique(np.concatenate([rng.integers(0, n_full, n_sample), [0, n_full - 1]]))
+    got_all = res.view(-1, len(pols), 80)
+    got = got_all[torch.from_numpy(idx).to(res.device)].cpu().numpy().view(mig.RESULT_DTYPE).reshape(-1, len(pols))
+    want = np.zeros((len(idx), len(pols)), orc.RESULT_DTYPE)
+    for k, t in enumerate(idx):
+        hj, he, ho = tg.generate_host(cfg, 1, trace_id0=int(t))
+        want[k] = orc.simulate(og, hj, he, ho, [orc.policy(**s) for s in SPECS], seed=seed, trace_id0=int(t))[0]
+    assert_same(got, want)
+    # totals over the whole launch equal the sum of the per-trace results
+    allres = mig.results_numpy(res, len(pols))
+    check_totals(allres, mig.totals_numpy(tot))
