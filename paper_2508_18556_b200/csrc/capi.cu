@@ -239,10 +239,11 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
     const uint64_t chunk_traces = std::max<uint64_t>(1, chunk_jobs / T.max_jobs);
     const uint64_t n_chunks = (T.n_traces + chunk_traces - 1) / chunk_traces;
     const uint64_t chunk_jobs_cap = chunk_traces * T.max_jobs;
-    const size_t jb = chunk_jobs_cap * 16, eb = T.jobs_ext ? chunk_jobs_cap * 16 : 0,
-                 ob = (chunk_traces + 1) * 8, esb = chunk_jobs_cap * sizeof(mig_job_estimate),
-                 rb = chunk_traces * n_policies * sizeof(mig_trace_result),
-                 tb = n_policies * sizeof(mig_policy_totals);
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };  // every sub-buffer 256 B aligned
+    const size_t jb = al(chunk_jobs_cap * 16), eb = T.jobs_ext ? al(chunk_jobs_cap * 16) : 0,
+                 ob = al((chunk_traces + 1) * 8), esb = al(chunk_jobs_cap * sizeof(mig_job_estimate)),
+                 rb = al(chunk_traces * n_policies * sizeof(mig_trace_result)),
+                 tb = al(n_policies * sizeof(mig_policy_totals));
     const size_t per = jb + eb + ob + esb + rb + tb + 64;
     cudaStream_t ss[2];
     uint8_t* buf[2] = {nullptr, nullptr};
@@ -277,7 +278,7 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(d_off, off + t0, (nt + 1) * 8, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, 64, s);
-        if (e == cudaSuccess) e = cudaMemsetAsync(d_tot, 0, tb, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_tot, 0, n_policies * sizeof(mig_policy_totals), s);
         if (e != cudaSuccess) {
             st = cuda_fail(e, "host pipeline H2D");
             break;
@@ -295,7 +296,8 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
             e = cudaMemcpyAsync(out + t0 * n_policies, d_out, nt * n_policies * sizeof(mig_trace_result),
                                 cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(host_tot.data() + c * n_policies, d_tot, tb, cudaMemcpyDeviceToHost, s);
+            e = cudaMemcpyAsync(host_tot.data() + c * n_policies, d_tot, n_policies * sizeof(mig_policy_totals),
+                                cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) st = cuda_fail(e, "host pipeline D2H");
     }
     for (int k = 0; k < 2; ++k) {
