@@ -193,8 +193,12 @@ mig_status load_geometry(const std::string& text, mig_geometry* g) {
         d.level_mem[l] = L[l];
         d.level_next[l] = l + 1 < d.n_levels ? L[l + 1] : 0u;
     }
-    for (uint32_t p = 0; p < d.n_prof; ++p)
+    for (uint32_t p = 0; p < d.n_prof; ++p) {
         d.level[p] = (uint32_t)(std::find(L.begin(), L.end(), d.mem[p]) - L.begin());
+        if (d.comp[p] > 15) return mig_set_error(MIG_E_VALIDATION, "compute_slices above 15 unsupported");
+        d.pinfo[p] = d.level[p] | (d.comp[p] << 4) | (d.lenmask[p] << 8) |
+                     ((uint32_t)__builtin_popcount(d.lenmask[p]) << 16) | (p << 20);
+    }
     // Alg. 1: fcr for every valid occupancy mask
     const uint32_t all = (1u << d.n_slots) - 1u;
     uint32_t comp_max = 0;

@@ -4,17 +4,22 @@
 // One warp per trace (persistent CTAs, atomic trace counter). The trace's jobs are staged into shared memory
 // (coalesced 128-bit loads, 32 B per job: iterations, class, tight-fit profile, iteration ticks, first
 // requirement, warps, forecast, convergence iteration and the first-exceed iteration of every memory level).
-// The partition state is lane-resident: lane s owns the instance that starts at memory slot s (profile, busy,
-// job, end tick, end kind), and the occupancy is a warp-uniform bitmask. Every decision is lane-parallel:
-//   tight fit / reuse / static choice ....... __ballot_sync over profiles or instances, __ffs / __clz
-//   Alg. 2 ............... lane k scores placement k as (fcr[occ|mask] << 8 | start) from the
-//                                             shared-memory fcr table and __reduce_max_sync picks the winner
-//   fusion / fission ......... lane k scores (fcr[occ'] << 16 | (15 - #destroyed) << 8 | start)
-//   next event ............................... __reduce_min_sync over the busy instances' end ticks, ties by
-//                                             (kind, job) with a second __reduce_min_sync
-// Counters are lane-distributed (lane c holds counter c); the per-trace decision stream is folded into an
-// FNV-1a-64 hash. Per-trace results (80 B) are written with 128-bit stores and per-policy totals are reduced in
-// shared memory then added to global memory once per CTA.
+// The partition state is held in registers:
+//   lane s (s < slots) ...... the instance that starts at memory slot s: packed profile info (memory level,
+//                             compute, slot mask, profile id, valid/busy bits), end tick, job and end kind
+//   warp-uniform ............ occupancy bitmask occ, instance-start mask SM, instance-end mask EM, busy-slot
+//                             mask BM (fusion/fission and busy tests are bit arithmetic, no shuffles)
+// Every decision is lane-parallel:
+//   reuse / static choice ... __ballot_sync over instances (+ __clz for the highest start)
+//   Alg. 2 lane k scores placement k as (fcr[occ|mask] << 8 | start) from the shared-memory
+//                             fcr table; __reduce_max_sync picks the argmax, ties to the highest start (R5)
+//   fusion / fission ........ lane k scores (fcr[occ'] << 16 | (15 - #destroyed) << 8 | start), occ' from the
+//                             instance boundaries around placement k (R8)
+//   next event .............. __reduce_min_sync over busy instances' end ticks; ties by (kind, job) (R28)
+// The policy kind is a template parameter (no per-decision policy branches). Counters are packed 16-bit fields
+// in four warp-uniform registers; the decision stream is folded into an FNV-1a-64 hash. Per-trace results
+// (80 B) are written with 128-bit stores; per-policy totals are reduced in shared memory and added to global
+// memory once per CTA.
 #include "device_common.cuh"
 
 namespace mig {
@@ -34,24 +39,11 @@ struct SimParams {
     mig_policy pol[kMaxPolicies];
 };
 
-// counters held by lane c
-enum : uint32_t {
-    C_COMPLETED = 0, C_REJECTED, C_FAILED, C_OOMS, C_PREEMPTS, C_RESTARTS, C_PLACEMENTS, C_WAITS, C_CREATES,
-    C_DESTROYS, C_TURNAROUND, C_BUSY
-};
-#define CBIT(c) (1u << (c))
-
-// Shared-memory image of the geometry (copied from the device-resident DevGeom once per CTA; lane-divergent
-// table reads such as fcr[occ | mask] then hit shared memory instead of serialising on the constant bank).
 constexpr size_t kGeomBytes = (sizeof(DevGeom) + 15) & ~size_t(15);
 constexpr size_t kPolBytes = (kMaxPolicies * sizeof(mig_policy) + 15) & ~size_t(15);
 constexpr size_t kTotBytes = kMaxPolicies * 20 * 8;
-
 constexpr int kWarps = 8;  // warps (traces in flight) per CTA
-
-__device__ __forceinline__ void bump(uint64_t& cnt, uint32_t lane, uint32_t mask, uint64_t v) {
-    if ((mask >> lane) & 1u) cnt += v;
-}
+constexpr uint32_t kValid = 1u << 31, kBusy = 1u << 30;
 
 // Tight fit (R6, R30), lanes over profiles.
 __device__ __forceinline__ uint32_t tight_fit_warp(const DevGeom& G, uint32_t req, uint32_t warps, bool fold,
@@ -79,18 +71,264 @@ __device__ __forceinline__ uint32_t tight_fit_lane(const DevGeom& G, uint32_t re
     return 0xFFu;
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
+__device__ __forceinline__ void rec(uint64_t& h, uint32_t tick, uint32_t lo) {
+    h = (h ^ (((uint64_t)tick << 32) | lo)) * kFnvPrime;
+}
+
+// Occupied slots of the instances a placement [lo, hi] overlaps, expanded to their boundaries (FF only).
+__device__ __forceinline__ uint32_t overlap_extent(uint32_t occ, uint32_t SM, uint32_t EM, uint32_t lo, uint32_t hi) {
+    const uint32_t a = ((occ >> lo) & 1u) ? 31u - __clz(SM & ((2u << lo) - 1u)) : lo;
+    const uint32_t b = ((occ >> hi) & 1u) ? (uint32_t)__ffs(EM & ~((1u << hi) - 1u)) - 1u : hi;
+    return occ & ((2u << b) - 1u) & ~((1u << a) - 1u);
+}
+
+struct TraceOut {
+    uint32_t K0, K1, K2, K3;  // placements|creates<<16, destroys|waits<<16, rejected|ooms<<16, preempts|failed<<16
+    uint64_t turn, busy, hash;
+    uint32_t makespan;
+};
+
+// One trace under one policy kind (Alg. 4 PAPER.md:601-617 + the partition manager).
+template <int KIND>
+__device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t lane, uint32_t n, uint4* jobA,
+                                                   const uint4* jobB, uint16_t* ring, uint32_t ring_cap, bool er,
+                                                   bool fold, uint32_t reconfig, uint32_t full_mem) {
+    uint32_t ii = 0, iend = 0, ijk = 0;  // lane-resident instance (slot = lane)
+    uint32_t occ = 0, SM = 0, EM = 0, BM = 0;
+    if (KIND == MIG_BASELINE) {
+        const uint32_t fp = G.full_prof;
+        if (lane == 0) ii = kValid | G.pinfo[fp];
+        occ = G.lenmask[fp];
+    } else if (KIND == MIG_STATIC) {
+        for (uint32_t i = 0; i < G.n_layout; ++i) {
+            const uint32_t p = G.layout_prof[i], s = G.layout_start[i];
+            if (lane == s) ii = kValid | G.pinfo[p];
+            occ |= G.lenmask[p] << s;
+        }
+    }
+    TraceOut o;
+    o.K0 = o.K1 = o.K2 = o.K3 = 0;
+    o.turn = o.busy = 0;
+    o.hash = kFnvOffset;
+    uint32_t t = 0, qh = 0, rh = 0, rn = 0;  // queue = jobs[qh..n) ++ ring[rh .. rh+rn) (requeues at the tail, R13)
+
+    for (;;) {
+        // ---------------- scheduler pass at tick t (head-of-line; wake on every event tick, R9) ----------------
+        while (qh < n || rn != 0) {
+            const uint32_t j = qh < n ? qh : (uint32_t)ring[rh];
+            const uint32_t need = jobA[j].x >> 24;
+            const uint32_t jsh = j << 16;
+            if (need == 0xFFu) {  // no profile can ever hold the job: REJECT
+                rec(o.hash, t, jsh | (K_REJECT << 12) | 0xFF0u);
+                o.K2 += 1u;
+            } else {
+                const uint32_t pn = G.pinfo[need];
+                const uint32_t nlev = pn & 0xFu, ncomp = (pn >> 4) & 0xFu;
+                uint32_t s = 0, si = 0, kd = 0, nd = 0;
+                bool created = false;
+                if (KIND == MIG_BASELINE) {  // one job at a time on the whole GPU
+                    if (BM) {
+                        rec(o.hash, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                        o.K1 += 1u << 16;
+                        break;
+                    }
+                    si = __shfl_sync(FULL, ii, 0);
+                    kd = K_PLACE_BASELINE;
+                } else if (KIND == MIG_STATIC) {  // smallest idle fitting layout slice, tie -> highest start (R11)
+                    const uint32_t ilev = ii & 0xFu;
+                    const bool cand = (ii & kValid) && ilev >= nlev && ((ii >> 4) & 0xFu) >= ncomp;
+                    const uint32_t key = (cand && !(ii & kBusy)) ? (((15u - ilev) << 5) | lane) + 1u : 0u;
+                    const uint32_t km = __reduce_max_sync(FULL, key);
+                    if (!km) {
+                        if (__ballot_sync(FULL, cand)) {
+                            rec(o.hash, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                            o.K1 += 1u << 16;
+                            break;
+                        }
+                        rec(o.hash, t, jsh | (K_REJECT << 12) | 0xF00u | (need << 4));
+                        o.K2 += 1u;
+                        goto pop;
+                    }
+                    s = (km - 1u) & 31u;
+                    si = __shfl_sync(FULL, ii, s);
+                    kd = K_PLACE_STATIC;
+                } else {
+                    if (KIND == MIG_FUSION_FISSION) {  // an idle slice that tightly fits (R7)
+                        const bool cand = (ii >> 30) == 2u && (ii & 0xFu) == nlev && ((ii >> 4) & 0xFu) >= ncomp;
+                        const uint32_t m = __ballot_sync(FULL, cand);
+                        if (m) {
+                            s = 31u - __clz(m);
+                            si = __shfl_sync(FULL, ii, s);
+                            kd = K_REUSE;
+                        }
+                    }
+                    if (!kd) {
+                        // Alg. 2: C = legal placements of the tight profile; argmax fcr; tie -> highest start
+                        const uint32_t pl = G.place[need][lane & 7u];
+                        const uint32_t qm = pl >> 8;
+                        const uint32_t score =
+                            (pl && !(occ & qm)) ? ((uint32_t)G.fcr[occ | qm] << 8) | (pl & 0xFFu) : 0u;
+                        const uint32_t best = __reduce_max_sync(FULL, score);
+                        const uint32_t nlen = (pn >> 16) & 0xFu;
+                        if (best) {
+                            s = best & 0xFFu;
+                            kd = K_ALLOC;
+                        } else if (KIND == MIG_FUSION_FISSION) {
+                            // fusion / fission: destroy the idle instances placement k overlaps (none busy, >= 1),
+                            // best (fcr(result), -#destroyed, start) (R8)
+                            uint32_t sc = 0;
+                            if (pl && !(qm & BM) && (qm & occ)) {
+                                const uint32_t lo = pl & 0xFFu;
+                                const uint32_t rm = overlap_extent(occ, SM, EM, lo, lo + nlen - 1u);
+                                sc = ((uint32_t)G.fcr[(occ & ~rm) | qm] << 16) | ((15u - __popc(SM & rm)) << 8) | lo;
+                            }
+                            const uint32_t bs = __reduce_max_sync(FULL, sc);
+                            if (bs) {
+                                s = bs & 0xFFu;
+                                nd = 15u - ((bs >> 8) & 0xFFu);
+                                const uint32_t rm = overlap_extent(occ, SM, EM, s, s + nlen - 1u);
+                                if ((SM & rm) >> lane & 1u) ii = 0;  // destroy (all idle)
+                                occ &= ~rm;
+                                SM &= ~rm;
+                                EM &= ~rm;
+                                kd = K_RECONF;
+                            }
+                        }
+                        if (!kd) {  // sleep() until a running job finishes
+                            rec(o.hash, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                            o.K1 += 1u << 16;
+                            break;
+                        }
+                        // create the instance (try_new_mig_slice)
+                        created = true;
+                        occ |= ((pn >> 8) & 0xFFu) << s;
+                        if (KIND == MIG_FUSION_FISSION) {
+                            SM |= 1u << s;
+                            EM |= 1u << (s + nlen - 1u);
+                        }
+                        si = kValid | pn;
+                        if (lane == s) ii = si;
+                    }
+                }
+                // the decision record, then start the run
+                const uint32_t prof = (si >> 20) & 0xFu;
+                rec(o.hash, t, jsh | (kd << 12) | (s << 8) | (prof << 4) | nd);
+                o.K0 += created ? 0x10001u : 1u;
+                o.K1 += nd;
+                const uint4 A = jobA[j];
+                const uint4 Bv = jobB[j];
+                const uint32_t lev = si & 0xFu;
+                const uint32_t T = A.x & 0xFFFFu, ticks = A.y;
+                const uint32_t fe = reinterpret_cast<const uint16_t*>(&jobB[j])[3 + lev];
+                const uint32_t rs = t + (created ? reconfig : 0u);
+                const uint32_t cap = G.level_mem[lev];
+                uint32_t i_pre = 0xFFFFFFFFu;
+                const uint32_t conv = Bv.y & 0xFFFFu;  // 0 unless a converged DYNAMIC forecast
+                if (KIND != MIG_BASELINE && er && conv > 0 && Bv.x > cap && cap < full_mem) i_pre = conv;
+                uint32_t end, ek;
+                if (fe <= min(T, i_pre)) {  // OOM > COMPLETE > PREEMPT in one iteration (R29); NEVER = 0xFFFF > T
+                    ek = 1;
+                    end = rs + fe * ticks;
+                } else if (i_pre < T) {
+                    ek = 2;
+                    end = rs + i_pre * ticks;
+                } else {
+                    ek = 0;
+                    end = rs + T * ticks;
+                }
+                if (lane == s) {
+                    ii |= kBusy;
+                    iend = end;
+                    ijk = j | (ek << 16);
+                }
+                BM |= ((si >> 8) & 0xFFu) << s;
+                o.busy += (uint64_t)((si >> 4) & 0xFu) * (end - rs);
+            }
+        pop:
+            if (qh < n) {
+                ++qh;
+            } else {
+                rh = rh + 1 == ring_cap ? 0 : rh + 1;
+                --rn;
+            }
+        }
+        // ---------------- next event: min end tick over running instances ----------------
+        const uint32_t mine = (ii & kBusy) ? iend : 0xFFFFFFFFu;
+        const uint32_t tn = __reduce_min_sync(FULL, mine);
+        if (tn == 0xFFFFFFFFu) break;
+        t = tn;
+        uint32_t evm = __ballot_sync(FULL, mine == t);
+        do {
+            uint32_t s;
+            if ((evm & (evm - 1u)) == 0u) {
+                s = (uint32_t)__ffs(evm) - 1u;
+            } else {  // several events at one tick: COMPLETE < OOM < PREEMPT, then job id (R28)
+                const uint32_t key = ((evm >> lane) & 1u) ? ijk : 0xFFFFFFFFu;  // kind << 16 | job
+                const uint32_t km = __reduce_min_sync(FULL, key);
+                s = (uint32_t)__ffs(__ballot_sync(FULL, key == km)) - 1u;
+            }
+            evm &= ~(1u << s);
+            const uint32_t si = __shfl_sync(FULL, ii, s);
+            const uint32_t sjk = __shfl_sync(FULL, ijk, s);
+            const uint32_t job = sjk & 0xFFFFu, ek = sjk >> 16;
+            const uint32_t lo = (job << 16) | (s << 8) | (((si >> 20) & 0xFu) << 4);
+            uint32_t req = 0;
+            if (ek == 0) {
+                rec(o.hash, t, lo | (K_COMPLETE << 12));
+                o.turn += t;
+            } else if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
+                rec(o.hash, t, lo | (K_OOM << 12));
+                const uint32_t nl = G.level_next[si & 0xFu];
+                o.K2 += 1u << 16;
+                if (nl == 0) {
+                    rec(o.hash, t, lo | (K_FAILED << 12));
+                    o.K3 += 1u << 16;
+                } else {
+                    req = nl;
+                }
+            } else {  // PREEMPT: restart on the slice meeting the forecast (R25)
+                rec(o.hash, t, lo | (K_PREEMPT << 12));
+                o.K3 += 1u;
+                req = min(jobB[job].x, full_mem);
+            }
+            if (req) {  // back to the queue tail (R13) with the new tight fit
+                const uint32_t need = tight_fit_warp(G, req, jobA[job].w, fold, lane);
+                __syncwarp();
+                if (lane == 0) {
+                    jobA[job].x = (jobA[job].x & 0x00FFFFFFu) | (need << 24);
+                    uint32_t pos = rh + rn;
+                    if (pos >= ring_cap) pos -= ring_cap;
+                    ring[pos] = (uint16_t)job;
+                }
+                __syncwarp();
+                ++rn;
+            }
+            const uint32_t ext = ((si >> 8) & 0xFFu) << s;
+            BM &= ~ext;
+            if (KIND == MIG_DYNAMIC) {  // free on completion (R10)
+                if (lane == s) ii = 0;
+                occ &= ~ext;
+                o.K1 += 1u;
+            } else if (lane == s) {
+                ii &= ~kBusy;
+            }
+        } while (evm);
+    }
+    o.makespan = t;
+    return o;
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     DevGeom& G = *reinterpret_cast<DevGeom*>(smem);
     mig_policy* s_pol = reinterpret_cast<mig_policy*>(smem + kGeomBytes);
     unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(smem + kGeomBytes + kPolBytes);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t per_warp = P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u) + 96u;
+    const uint32_t per_warp = P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u);
     uint8_t* wb = smem + kGeomBytes + kPolBytes + kTotBytes + warp * per_warp;
     uint4* jobA = reinterpret_cast<uint4*>(wb);                      // {T | cls<<16 | need<<24, ticks, req0, warps}
     uint4* jobB = jobA + P.max_jobs;                                 // {pred, conv | fe0<<16, fe1|fe2<<16, fe3|fe4<<16}
-    uint16_t* ring = reinterpret_cast<uint16_t*>(jobB + P.max_jobs);  // requeue FIFO (R13: tail)
-    uint32_t* sres = reinterpret_cast<uint32_t*>(wb + per_warp - 96u);  // 80 B result staging
+    uint16_t* ring = reinterpret_cast<uint16_t*>(jobB + P.max_jobs);  // requeue FIFO
 
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
@@ -121,8 +359,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_simulate(const DevGeom* __restr
         }
         // ---- a1/a2: stage the trace (128-bit coalesced loads) and the per-job estimates ----
         for (uint32_t j = lane; j < n; j += 32) {
-            uint4 r = __ldg(P.jobs + j0 + j);
-            uint4 e = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
+            const uint4 r = __ldg(P.jobs + j0 + j);
+            const uint4 e = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
             const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
             if (cls > 2 || T > 4096 || (r.z >> 24) != 0) err |= (uint32_t)MIG_ERR_BAD_RECORD;
             uint4 A, Bv;
@@ -131,12 +369,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_simulate(const DevGeom* __restr
             A.w = e.y;
             if (cls == kClassDynamic) {
                 const uint4* es = reinterpret_cast<const uint4*>(P.est + j0 + j);
-                uint4 e0 = __ldg(es), e1 = __ldg(es + 1);
-                A.z = e0.x;                                        // req0 (smallest slice, R16)
+                const uint4 e0 = __ldg(es), e1 = __ldg(es + 1);
+                A.z = e0.x;  // req0 (smallest slice, R16)
                 Bv = make_uint4(e0.y, (e0.z & 0xFFFFu) | (e0.w << 16), (e0.w >> 16) | (e1.x << 16),
                                 (e1.x >> 16) | (e1.y << 16));
             } else {
-                A.z = r.x + e.x + P.ctx;                           // est + ws + ctx
+                A.z = r.x + e.x + P.ctx;  // est + ws + ctx
                 const uint64_t phys = (uint64_t)r.y + e.x + P.ctx;
                 uint32_t fe[5];
 #pragma unroll
@@ -153,269 +391,67 @@ __global__ void __launch_bounds__(kWarps * 32) k_simulate(const DevGeom* __restr
             const mig_policy& pol = s_pol[p];
             const uint32_t kind = pol.kind;
             const bool fold = (pol.flags & MIG_WARP_FOLD) != 0;
-            const bool er = (pol.flags & MIG_EARLY_RESTART) != 0 && kind != MIG_BASELINE;
+            const bool er = (pol.flags & MIG_EARLY_RESTART) != 0;
             __syncwarp();
             for (uint32_t j = lane; j < n; j += 32) {
-                uint4 A = jobA[j];
-                A.x = (A.x & 0x00FFFFFFu) | (tight_fit_lane(G, A.z, A.w, fold) << 24);
-                jobA[j].x = A.x;
+                const uint4 A = jobA[j];
+                jobA[j].x = (A.x & 0x00FFFFFFu) | (tight_fit_lane(G, A.z, A.w, fold) << 24);
             }
             __syncwarp();
-            // ---- lane-resident instance table (lane s = instance starting at slot s) ----
-            int ip = -1;  // profile
-            uint32_t ibusy = 0, ijob = 0, iend = 0, ikind = 0;
-            uint32_t occ = 0;
-            if (kind == MIG_BASELINE) {
-                if (lane == 0) ip = (int)G.full_prof;
-                occ = G.lenmask[G.full_prof];
-            } else if (kind == MIG_STATIC) {
-                for (uint32_t i = 0; i < G.n_layout; ++i) {
-                    if (lane == G.layout_start[i]) ip = (int)G.layout_prof[i];
-                    occ |= G.lenmask[G.layout_prof[i]] << G.layout_start[i];
-                }
+            TraceOut o;
+            if (kind == MIG_FUSION_FISSION)
+                o = simulate_trace<MIG_FUSION_FISSION>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                                       pol.reconfig_ticks, full_mem);
+            else if (kind == MIG_DYNAMIC)
+                o = simulate_trace<MIG_DYNAMIC>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                                pol.reconfig_ticks, full_mem);
+            else if (kind == MIG_STATIC)
+                o = simulate_trace<MIG_STATIC>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                               pol.reconfig_ticks, full_mem);
+            else
+                o = simulate_trace<MIG_BASELINE>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                                 pol.reconfig_ticks, full_mem);
+            // ---- a11: per-trace result (80 B, five 128-bit stores from lanes 0-4) ----
+            const uint32_t placements = o.K0 & 0xFFFFu, creates = o.K0 >> 16, destroys = o.K1 & 0xFFFFu,
+                           waits = o.K1 >> 16, rejected = o.K2 & 0xFFFFu, ooms = o.K2 >> 16,
+                           preempts = o.K3 & 0xFFFFu, failed = o.K3 >> 16;
+            const uint32_t completed = n - rejected - failed, restarts = ooms - failed + preempts;
+            const uint64_t energy = (uint64_t)pol.idle_w * o.makespan + (uint64_t)pol.w_per_slice * o.busy;
+            if (P.out && lane < 5) {
+                uint4 v;
+                if (lane == 0) v = make_uint4(o.makespan, n, completed, rejected);
+                else if (lane == 1) v = make_uint4(failed, ooms, preempts, restarts);
+                else if (lane == 2) v = make_uint4(placements, waits, creates, destroys);
+                else if (lane == 3) v = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)o.turn,
+                                                   (uint32_t)(o.turn >> 32));
+                else v = make_uint4((uint32_t)o.busy, (uint32_t)(o.busy >> 32), (uint32_t)o.hash,
+                                    (uint32_t)(o.hash >> 32));
+                reinterpret_cast<uint4*>(P.out + tr * P.n_pol + p)[lane] = v;
             }
-            uint64_t cnt = 0;  // lane-distributed counters
-            uint64_t hash = kFnvOffset;
-            uint32_t t = 0, makespan = 0;
-            uint32_t qh = 0, rh = 0, rn = 0;  // queue = jobs[qh..n) ++ ring[rh .. rh+rn)
-
-            // ---- a8: scheduler pass (Alg. 4; head-of-line, wake on every event R9) ----
-            auto sched_pass = [&]() {
-                while (qh < n || rn != 0) {
-                    const uint32_t j = qh < n ? qh : (uint32_t)ring[rh];
-                    const uint4 A = jobA[j];
-                    const uint32_t need = A.x >> 24;
-                    uint32_t s = 0xFFu, prof = 0, kd = 0, nd = 0;
-                    bool created = false;
-                    if (need == 0xFFu) {  // no profile can ever hold the job
-                        hash_record(hash, t, j, K_REJECT, 0xF, 0xF, 0);
-                        bump(cnt, lane, CBIT(C_REJECTED), 1);
-                    } else {
-                        const uint32_t nmem = G.mem[need], ncomp = G.comp[need];
-                        if (kind == MIG_BASELINE || kind == MIG_STATIC) {
-                            // smallest idle fitting slice, tie -> highest start (R11); baseline = whole GPU
-                            const bool cand = ip >= 0 && G.mem[ip] >= nmem && G.comp[ip] >= ncomp;
-                            const uint32_t key = (cand && !ibusy) ? (((31u - G.level[ip]) << 5) | lane) + 1u : 0u;
-                            const uint32_t km = __reduce_max_sync(FULL, key);
-                            if (km) {
-                                s = (km - 1u) & 31u;
-                                prof = (uint32_t)__shfl_sync(FULL, ip, s);
-                                kd = kind == MIG_BASELINE ? K_PLACE_BASELINE : K_PLACE_STATIC;
-                            } else if (__ballot_sync(FULL, cand)) {
-                                kd = K_WAIT;
-                            } else {
-                                kd = K_REJECT;
-                            }
-                        } else {
-                            if (kind == MIG_FUSION_FISSION) {  // idle slice that tightly fits (R7)
-                                const bool cand = ip >= 0 && !ibusy && G.mem[ip] == nmem && G.comp[ip] >= ncomp;
-                                const uint32_t m = __ballot_sync(FULL, cand);
-                                if (m) {
-                                    s = 31u - __clz(m);
-                                    prof = (uint32_t)__shfl_sync(FULL, ip, s);
-                                    kd = K_REUSE;
-                                }
-                            }
-                            if (!kd) {  // Alg. 2: argmax fcr over legal placements, tie -> highest start (R5)
-                                const uint32_t np = G.n_place[need];
-                                uint32_t score = 0;
-                                if (lane < np) {
-                                    const uint32_t pl = G.place[need][lane], mask = pl >> 8;
-                                    if (!(occ & mask)) score = ((uint32_t)G.fcr[occ | mask] << 8) | (pl & 0xFFu);
-                                }
-                                const uint32_t best = __reduce_max_sync(FULL, score);
-                                if (best) {
-                                    s = best & 0xFFu;
-                                    prof = need;
-                                    kd = K_ALLOC;
-                                    created = true;
-                                    occ |= G.lenmask[need] << s;
-                                    if (lane == s) ip = (int)need;
-                                } else if (kind == MIG_FUSION_FISSION) {
-                                    // fusion/fission (R8): destroy the idle instances a
-                                    // placement overlaps, best (fcr(result), -#destroyed, start)
-                                    const uint32_t ext_l = ip >= 0 ? G.lenmask[ip] << lane : 0u;
-                                    const uint32_t busy_slots = __reduce_or_sync(FULL, ibusy ? ext_l : 0u);
-                                    uint32_t qm = 0, qs = 0;
-                                    bool cand = false;
-                                    if (lane < np) {
-                                        const uint32_t pl = G.place[need][lane];
-                                        qm = pl >> 8;
-                                        qs = pl & 0xFFu;
-                                        cand = !(qm & busy_slots) && (qm & occ);
-                                    }
-                                    uint32_t removed = 0, ndl = 0;
-                                    for (uint32_t k = 0; k < G.n_slots; ++k) {
-                                        const uint32_t ek = __shfl_sync(FULL, ext_l, k);
-                                        if (ek & qm) {
-                                            removed |= ek;
-                                            ++ndl;
-                                        }
-                                    }
-                                    const uint32_t sc =
-                                        cand ? (((uint32_t)G.fcr[(occ & ~removed) | qm] << 16) | ((15u - ndl) << 8) | qs)
-                                             : 0u;
-                                    const uint32_t bs = __reduce_max_sync(FULL, sc);
-                                    if (bs) {
-                                        s = bs & 0xFFu;
-                                        nd = 15u - ((bs >> 8) & 0xFFu);
-                                        const uint32_t qmask = G.lenmask[need] << s;
-                                        const bool kill = (ext_l & qmask) != 0;
-                                        const uint32_t rem = __reduce_or_sync(FULL, kill ? ext_l : 0u);
-                                        if (kill) ip = -1;
-                                        occ = (occ & ~rem) | qmask;
-                                        if (lane == s) ip = (int)need;
-                                        prof = need;
-                                        kd = K_RECONF;
-                                        created = true;
-                                    }
-                                }
-                                if (!kd) kd = K_WAIT;
-                            }
-                        }
-                        if (kd == K_WAIT) {
-                            hash_record(hash, t, j, K_WAIT, 0xF, need, 0);
-                            bump(cnt, lane, CBIT(C_WAITS), 1);
-                            return;  // head-of-line: the pass ends
-                        }
-                        if (kd == K_REJECT) {
-                            hash_record(hash, t, j, K_REJECT, 0xF, need, 0);
-                            bump(cnt, lane, CBIT(C_REJECTED), 1);
-                        } else {
-                            hash_record(hash, t, j, kd, s, prof, nd);
-                            bump(cnt, lane, CBIT(C_PLACEMENTS) | (created ? CBIT(C_CREATES) : 0u), 1);
-                            bump(cnt, lane, CBIT(C_DESTROYS), nd);
-                            // ---- start the run; OOM / early restart / completion ----
-                            const uint4 Bv = jobB[j];
-                            const uint32_t T = A.x & 0xFFFFu, cls = (A.x >> 16) & 0xFFu, ticks = A.y;
-                            const uint32_t cap = G.mem[prof];
-                            const uint32_t fe = reinterpret_cast<const uint16_t*>(&jobB[j])[3 + G.level[prof]];
-                            const uint32_t rs = t + (created ? pol.reconfig_ticks : 0u);
-                            uint32_t i_pre = 0xFFFFFFFFu;
-                            const uint32_t conv = Bv.y & 0xFFFFu;
-                            if (er && cls == kClassDynamic && conv > 0 && Bv.x > cap && cap < full_mem) i_pre = conv;
-                            uint32_t end, ek;
-                            if (fe != kNever && fe <= min(T, i_pre)) {  // OOM > COMPLETE > PREEMPT (R29)
-                                ek = 1;
-                                end = rs + fe * ticks;
-                            } else if (i_pre < T) {
-                                ek = 2;
-                                end = rs + i_pre * ticks;
-                            } else {
-                                ek = 0;
-                                end = rs + T * ticks;
-                            }
-                            if (lane == s) {
-                                ibusy = 1;
-                                ijob = j;
-                                iend = end;
-                                ikind = ek;
-                            }
-                            bump(cnt, lane, CBIT(C_BUSY), (uint64_t)G.comp[prof] * (end - rs));
-                        }
-                    }
-                    // pop the head
-                    if (qh < n) {
-                        ++qh;
-                    } else {
-                        rh = rh + 1 == P.ring_cap ? 0 : rh + 1;
-                        --rn;
-                    }
-                }
-            };
-
-            sched_pass();
-            // ---- a8-a10: event loop ----
-            for (;;) {
-                const uint32_t mine = (ip >= 0 && ibusy) ? iend : 0xFFFFFFFFu;
-                const uint32_t tn = __reduce_min_sync(FULL, mine);
-                if (tn == 0xFFFFFFFFu) break;
-                t = tn;
-                uint32_t evm = __ballot_sync(FULL, mine == t);
-                while (evm) {
-                    uint32_t s;
-                    if ((evm & (evm - 1u)) == 0u) {
-                        s = (uint32_t)__ffs(evm) - 1u;
-                    } else {  // several events at one tick: COMPLETE < OOM < PREEMPT, then job id (R28)
-                        const uint32_t key = ((evm >> lane) & 1u) ? ((ikind << 16) | ijob) : 0xFFFFFFFFu;
-                        const uint32_t km = __reduce_min_sync(FULL, key);
-                        s = (uint32_t)__ffs(__ballot_sync(FULL, key == km)) - 1u;
-                    }
-                    evm &= ~(1u << s);
-                    const uint32_t prof = (uint32_t)__shfl_sync(FULL, ip, s);
-                    const uint32_t job = __shfl_sync(FULL, ijob, s);
-                    const uint32_t ek = __shfl_sync(FULL, ikind, s);
-                    bool requeue = false;
-                    uint32_t req = 0;
-                    if (ek == 0) {
-                        hash_record(hash, t, job, K_COMPLETE, s, prof, 0);
-                        bump(cnt, lane, CBIT(C_COMPLETED), 1);
-                        bump(cnt, lane, CBIT(C_TURNAROUND), t);
-                    } else if (ek == 1) {  // OOM: next larger slice (R14) or FAILED at full GPU
-                        hash_record(hash, t, job, K_OOM, s, prof, 0);
-                        const uint32_t nl = G.level_next[G.level[prof]];
-                        if (nl == 0) {
-                            hash_record(hash, t, job, K_FAILED, s, prof, 0);
-                            bump(cnt, lane, CBIT(C_OOMS) | CBIT(C_FAILED), 1);
-                        } else {
-                            bump(cnt, lane, CBIT(C_OOMS) | CBIT(C_RESTARTS), 1);
-                            requeue = true;
-                            req = nl;
-                        }
-                    } else {  // PREEMPT: restart on the slice meeting the forecast (R25)
-                        hash_record(hash, t, job, K_PREEMPT, s, prof, 0);
-                        bump(cnt, lane, CBIT(C_PREEMPTS) | CBIT(C_RESTARTS), 1);
-                        requeue = true;
-                        req = min(jobB[job].x, full_mem);
-                    }
-                    if (requeue) {  // back to the queue tail (R13) with the new tight fit
-                        const uint32_t need = tight_fit_warp(G, req, jobA[job].w, fold, lane);
-                        __syncwarp();
-                        if (lane == 0) {
-                            jobA[job].x = (jobA[job].x & 0x00FFFFFFu) | (need << 24);
-                            uint32_t pos = rh + rn;
-                            if (pos >= P.ring_cap) pos -= P.ring_cap;
-                            ring[pos] = (uint16_t)job;
-                        }
-                        __syncwarp();
-                        ++rn;
-                    }
-                    if (lane == s) ibusy = 0;
-                    if (kind == MIG_DYNAMIC) {  // free on completion (R10)
-                        if (lane == s) ip = -1;
-                        occ &= ~(G.lenmask[prof] << s);
-                        bump(cnt, lane, CBIT(C_DESTROYS), 1);
-                    }
-                }
-                makespan = t;
-                sched_pass();
-            }
-            // ---- a11: per-trace result (80 B) ----
-            const uint64_t busy = __shfl_sync(FULL, cnt, C_BUSY);
-            __syncwarp();
-            if (lane < 10) sres[2 + lane] = (uint32_t)cnt;
-            if (lane == 0) {
-                sres[0] = makespan;
-                sres[1] = n;
-            }
-            uint64_t* sres64 = reinterpret_cast<uint64_t*>(sres);
-            if (lane == C_TURNAROUND) sres64[7] = cnt;
-            if (lane == C_BUSY) {
-                sres64[8] = cnt;
-                sres64[6] = (uint64_t)pol.idle_w * makespan + (uint64_t)pol.w_per_slice * busy;
-            }
-            if (lane == 12) sres64[9] = hash;
-            __syncwarp();
-            if (P.out && lane < 5)
-                reinterpret_cast<uint4*>(P.out + tr * P.n_pol + p)[lane] = reinterpret_cast<const uint4*>(sres)[lane];
             // ---- a12: per-policy totals (shared-memory atomics, flushed once per CTA) ----
             if (lane < 19) {
                 uint64_t v;
-                if (lane == 0) v = 1;
-                else if (lane < 12) v = sres[lane];
-                else if (lane == 12 || lane == 13) v = sres[0];
-                else if (lane == 18) v = err;
-                else v = sres64[lane - 8];  // 14 energy, 15 turnaround, 16 busy, 17 hash
+                switch (lane) {
+                    case 0: v = 1; break;
+                    case 1: v = n; break;
+                    case 2: v = completed; break;
+                    case 3: v = rejected; break;
+                    case 4: v = failed; break;
+                    case 5: v = ooms; break;
+                    case 6: v = preempts; break;
+                    case 7: v = restarts; break;
+                    case 8: v = placements; break;
+                    case 9: v = waits; break;
+                    case 10: v = creates; break;
+                    case 11: v = destroys; break;
+                    case 12:
+                    case 13: v = o.makespan; break;
+                    case 14: v = energy; break;
+                    case 15: v = o.turn; break;
+                    case 16: v = o.busy; break;
+                    case 17: v = o.hash; break;
+                    default: v = err; break;
+                }
                 if (lane == 13) atomicMax(&s_tot[p * 20 + 13], (unsigned long long)v);
                 else if (lane == 18) { if (v) atomicOr(&s_tot[p * 20 + 18], (unsigned long long)v); }
                 else atomicAdd(&s_tot[p * 20 + lane], (unsigned long long)v);
@@ -437,7 +473,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_simulate(const DevGeom* __restr
 }
 
 size_t simulate_smem_bytes(uint32_t max_jobs) {
-    const size_t per_warp = (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u) + 96u;
+    const size_t per_warp = (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u);
     return kGeomBytes + kPolBytes + kTotBytes + kWarps * per_warp;
 }
 
