@@ -20,6 +20,8 @@
 // in four warp-uniform registers; the decision stream is folded into an FNV-1a-64 hash. Per-trace results
 // (80 B) are written with 128-bit stores; per-policy totals are reduced in shared memory and added to global
 // memory once per CTA.
+#include <stdlib.h>
+
 #include "device_common.cuh"
 
 namespace mig {
@@ -45,17 +47,26 @@ constexpr size_t kTotBytes = kMaxPolicies * 20 * 8;
 constexpr int kWarps = 8;  // warps (traces in flight) per CTA
 constexpr uint32_t kValid = 1u << 31, kBusy = 1u << 30;
 
-// Tight fit (R6, R30), lanes over profiles.
-__device__ __forceinline__ uint32_t tight_fit_warp(const DevGeom& G, uint32_t req, uint32_t warps, bool fold,
-                                                   uint32_t lane) {
-    bool ok = lane < G.n_prof && G.mem[lane] >= req;
-    if (fold && warps > 0 && lane < G.n_prof) {
-        uint32_t cf = G.wave_cap[G.full_prof], cp = G.wave_cap[lane];
-        ok = ok && ((warps + cp - 1) / cp == (warps + cf - 1) / cf);
+// A lane group of GW lanes simulates one trace (GW = 32: one trace per warp; GW = 8: four traces per warp).
+// Group-scoped warp intrinsics: the member mask is the group's lanes, so groups of one warp may diverge.
+template <int GW>
+struct Grp {
+    uint32_t gl, gbase, gmask;
+    __device__ __forceinline__ explicit Grp(uint32_t lane) {
+        gl = lane & (GW - 1);
+        gbase = lane - gl;
+        gmask = GW == 32 ? FULL : (((1u << (GW & 31)) - 1u) << gbase);
     }
-    uint32_t m = __ballot_sync(FULL, ok);
-    return m ? (uint32_t)(__ffs(m) - 1) : 0xFFu;
-}
+    __device__ __forceinline__ uint32_t ballot(bool p) const { return __ballot_sync(gmask, p) >> gbase; }
+    __device__ __forceinline__ uint32_t max(uint32_t v) const { return __reduce_max_sync(gmask, v); }
+    __device__ __forceinline__ uint32_t min(uint32_t v) const { return __reduce_min_sync(gmask, v); }
+    __device__ __forceinline__ uint32_t bor(uint32_t v) const { return __reduce_or_sync(gmask, v); }
+    __device__ __forceinline__ uint32_t shfl(uint32_t v, uint32_t src) const { return __shfl_sync(gmask, v, src, GW); }
+    __device__ __forceinline__ unsigned long long shfl64(unsigned long long v, uint32_t src) const {
+        return __shfl_sync(gmask, v, src, GW);
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(gmask); }
+};
 
 // Same, one lane (staging: lanes over jobs).
 __device__ __forceinline__ uint32_t tight_fit_lane(const DevGeom& G, uint32_t req, uint32_t warps, bool fold) {
@@ -71,8 +82,12 @@ __device__ __forceinline__ uint32_t tight_fit_lane(const DevGeom& G, uint32_t re
     return 0xFFu;
 }
 
-__device__ __forceinline__ void rec(uint64_t& h, uint32_t tick, uint32_t lo) {
-    h = (h ^ (((uint64_t)tick << 32) | lo)) * kFnvPrime;
+// FNV-1a-64 step h = (h ^ (tick << 32 | lo)) * (2^40 + 0x1b3) mod 2^64, on the two 32-bit halves of h.
+__device__ __forceinline__ void rec(uint32_t& hl, uint32_t& hh, uint32_t tick, uint32_t lo) {
+    const uint32_t x = hl ^ lo, y = hh ^ tick;
+    const uint64_t p = (uint64_t)x * 0x1b3u;
+    hl = (uint32_t)p;
+    hh = (uint32_t)(p >> 32) + y * 0x1b3u + (x << 8);
 }
 
 // Occupied slots of the instances a placement [lo, hi] overlaps, expanded to their boundaries (FF only).
@@ -84,15 +99,17 @@ __device__ __forceinline__ uint32_t overlap_extent(uint32_t occ, uint32_t SM, ui
 
 struct TraceOut {
     uint32_t K0, K1, K2, K3;  // placements|creates<<16, destroys|waits<<16, rejected|ooms<<16, preempts|failed<<16
-    uint64_t turn, busy, hash;
+    uint64_t turn, busy;
+    uint32_t hl, hh;          // decision hash halves
     uint32_t makespan;
 };
 
 // One trace under one policy kind (Alg. 4 PAPER.md:601-617 + the partition manager).
-template <int KIND>
-__device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t lane, uint32_t n, uint4* jobA,
+template <int KIND, int GW>
+__device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<GW>& g, uint32_t n, uint4* jobA,
                                                    const uint4* jobB, uint16_t* ring, uint32_t ring_cap, bool er,
                                                    bool fold, uint32_t reconfig, uint32_t full_mem) {
+    const uint32_t lane = g.gl;
     uint32_t ii = 0, iend = 0, ijk = 0;  // lane-resident instance (slot = lane)
     uint32_t occ = 0, SM = 0, EM = 0, BM = 0;
     if (KIND == MIG_BASELINE) {
@@ -109,7 +126,8 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
     TraceOut o;
     o.K0 = o.K1 = o.K2 = o.K3 = 0;
     o.turn = o.busy = 0;
-    o.hash = kFnvOffset;
+    o.hl = (uint32_t)kFnvOffset;
+    o.hh = (uint32_t)(kFnvOffset >> 32);
     uint32_t t = 0, qh = 0, rh = 0, rn = 0;  // queue = jobs[qh..n) ++ ring[rh .. rh+rn) (requeues at the tail, R13)
 
     for (;;) {
@@ -119,7 +137,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
             const uint32_t need = jobA[j].x >> 24;
             const uint32_t jsh = j << 16;
             if (need == 0xFFu) {  // no profile can ever hold the job: REJECT
-                rec(o.hash, t, jsh | (K_REJECT << 12) | 0xFF0u);
+                rec(o.hl, o.hh, t, jsh | (K_REJECT << 12) | 0xFF0u);
                 o.K2 += 1u;
             } else {
                 const uint32_t pn = G.pinfo[need];
@@ -128,37 +146,37 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
                 bool created = false;
                 if (KIND == MIG_BASELINE) {  // one job at a time on the whole GPU
                     if (BM) {
-                        rec(o.hash, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                        rec(o.hl, o.hh, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
                         o.K1 += 1u << 16;
                         break;
                     }
-                    si = __shfl_sync(FULL, ii, 0);
+                    si = g.shfl(ii, 0);
                     kd = K_PLACE_BASELINE;
                 } else if (KIND == MIG_STATIC) {  // smallest idle fitting layout slice, tie -> highest start (R11)
                     const uint32_t ilev = ii & 0xFu;
                     const bool cand = (ii & kValid) && ilev >= nlev && ((ii >> 4) & 0xFu) >= ncomp;
                     const uint32_t key = (cand && !(ii & kBusy)) ? (((15u - ilev) << 5) | lane) + 1u : 0u;
-                    const uint32_t km = __reduce_max_sync(FULL, key);
+                    const uint32_t km = g.max(key);
                     if (!km) {
-                        if (__ballot_sync(FULL, cand)) {
-                            rec(o.hash, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                        if (g.ballot(cand)) {
+                            rec(o.hl, o.hh, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
                             o.K1 += 1u << 16;
                             break;
                         }
-                        rec(o.hash, t, jsh | (K_REJECT << 12) | 0xF00u | (need << 4));
+                        rec(o.hl, o.hh, t, jsh | (K_REJECT << 12) | 0xF00u | (need << 4));
                         o.K2 += 1u;
                         goto pop;
                     }
                     s = (km - 1u) & 31u;
-                    si = __shfl_sync(FULL, ii, s);
+                    si = g.shfl(ii, s);
                     kd = K_PLACE_STATIC;
                 } else {
                     if (KIND == MIG_FUSION_FISSION) {  // an idle slice that tightly fits (R7)
                         const bool cand = (ii >> 30) == 2u && (ii & 0xFu) == nlev && ((ii >> 4) & 0xFu) >= ncomp;
-                        const uint32_t m = __ballot_sync(FULL, cand);
+                        const uint32_t m = g.ballot(cand);
                         if (m) {
                             s = 31u - __clz(m);
-                            si = __shfl_sync(FULL, ii, s);
+                            si = g.shfl(ii, s);
                             kd = K_REUSE;
                         }
                     }
@@ -168,7 +186,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
                         const uint32_t qm = pl >> 8;
                         const uint32_t score =
                             (pl && !(occ & qm)) ? ((uint32_t)G.fcr[occ | qm] << 8) | (pl & 0xFFu) : 0u;
-                        const uint32_t best = __reduce_max_sync(FULL, score);
+                        const uint32_t best = g.max(score);
                         const uint32_t nlen = (pn >> 16) & 0xFu;
                         if (best) {
                             s = best & 0xFFu;
@@ -182,7 +200,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
                                 const uint32_t rm = overlap_extent(occ, SM, EM, lo, lo + nlen - 1u);
                                 sc = ((uint32_t)G.fcr[(occ & ~rm) | qm] << 16) | ((15u - __popc(SM & rm)) << 8) | lo;
                             }
-                            const uint32_t bs = __reduce_max_sync(FULL, sc);
+                            const uint32_t bs = g.max(sc);
                             if (bs) {
                                 s = bs & 0xFFu;
                                 nd = 15u - ((bs >> 8) & 0xFFu);
@@ -195,7 +213,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
                             }
                         }
                         if (!kd) {  // sleep() until a running job finishes
-                            rec(o.hash, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                            rec(o.hl, o.hh, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
                             o.K1 += 1u << 16;
                             break;
                         }
@@ -212,7 +230,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
                 }
                 // the decision record, then start the run
                 const uint32_t prof = (si >> 20) & 0xFu;
-                rec(o.hash, t, jsh | (kd << 12) | (s << 8) | (prof << 4) | nd);
+                rec(o.hl, o.hh, t, jsh | (kd << 12) | (s << 8) | (prof << 4) | nd);
                 o.K0 += created ? 0x10001u : 1u;
                 o.K1 += nd;
                 const uint4 A = jobA[j];
@@ -254,53 +272,53 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
         }
         // ---------------- next event: min end tick over running instances ----------------
         const uint32_t mine = (ii & kBusy) ? iend : 0xFFFFFFFFu;
-        const uint32_t tn = __reduce_min_sync(FULL, mine);
+        const uint32_t tn = g.min(mine);
         if (tn == 0xFFFFFFFFu) break;
         t = tn;
-        uint32_t evm = __ballot_sync(FULL, mine == t);
+        uint32_t evm = g.ballot(mine == t);
         do {
             uint32_t s;
             if ((evm & (evm - 1u)) == 0u) {
                 s = (uint32_t)__ffs(evm) - 1u;
             } else {  // several events at one tick: COMPLETE < OOM < PREEMPT, then job id (R28)
                 const uint32_t key = ((evm >> lane) & 1u) ? ijk : 0xFFFFFFFFu;  // kind << 16 | job
-                const uint32_t km = __reduce_min_sync(FULL, key);
-                s = (uint32_t)__ffs(__ballot_sync(FULL, key == km)) - 1u;
+                const uint32_t km = g.min(key);
+                s = (uint32_t)__ffs(g.ballot(key == km)) - 1u;
             }
             evm &= ~(1u << s);
-            const uint32_t si = __shfl_sync(FULL, ii, s);
-            const uint32_t sjk = __shfl_sync(FULL, ijk, s);
+            const uint32_t si = g.shfl(ii, s);
+            const uint32_t sjk = g.shfl(ijk, s);
             const uint32_t job = sjk & 0xFFFFu, ek = sjk >> 16;
             const uint32_t lo = (job << 16) | (s << 8) | (((si >> 20) & 0xFu) << 4);
             uint32_t req = 0;
             if (ek == 0) {
-                rec(o.hash, t, lo | (K_COMPLETE << 12));
+                rec(o.hl, o.hh, t, lo | (K_COMPLETE << 12));
                 o.turn += t;
             } else if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
-                rec(o.hash, t, lo | (K_OOM << 12));
+                rec(o.hl, o.hh, t, lo | (K_OOM << 12));
                 const uint32_t nl = G.level_next[si & 0xFu];
                 o.K2 += 1u << 16;
                 if (nl == 0) {
-                    rec(o.hash, t, lo | (K_FAILED << 12));
+                    rec(o.hl, o.hh, t, lo | (K_FAILED << 12));
                     o.K3 += 1u << 16;
                 } else {
                     req = nl;
                 }
             } else {  // PREEMPT: restart on the slice meeting the forecast (R25)
-                rec(o.hash, t, lo | (K_PREEMPT << 12));
+                rec(o.hl, o.hh, t, lo | (K_PREEMPT << 12));
                 o.K3 += 1u;
                 req = min(jobB[job].x, full_mem);
             }
             if (req) {  // back to the queue tail (R13) with the new tight fit
-                const uint32_t need = tight_fit_warp(G, req, jobA[job].w, fold, lane);
-                __syncwarp();
+                const uint32_t need = tight_fit_lane(G, req, jobA[job].w, fold);
+                g.sync();
                 if (lane == 0) {
                     jobA[job].x = (jobA[job].x & 0x00FFFFFFu) | (need << 24);
                     uint32_t pos = rh + rn;
                     if (pos >= ring_cap) pos -= ring_cap;
                     ring[pos] = (uint16_t)job;
                 }
-                __syncwarp();
+                g.sync();
                 ++rn;
             }
             const uint32_t ext = ((si >> 8) & 0xFFu) << s;
@@ -318,14 +336,16 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, uint32_t la
     return o;
 }
 
+template <int GW>
 __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     DevGeom& G = *reinterpret_cast<DevGeom*>(smem);
     mig_policy* s_pol = reinterpret_cast<mig_policy*>(smem + kGeomBytes);
     unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(smem + kGeomBytes + kPolBytes);
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t per_warp = P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u);
-    uint8_t* wb = smem + kGeomBytes + kPolBytes + kTotBytes + warp * per_warp;
+    const Grp<GW> g(threadIdx.x & 31u);
+    const uint32_t lane = g.gl, group = threadIdx.x / GW;
+    const uint32_t per_group = P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u);
+    uint8_t* wb = smem + kGeomBytes + kPolBytes + kTotBytes + group * per_group;
     uint4* jobA = reinterpret_cast<uint4*>(wb);                      // {T | cls<<16 | need<<24, ticks, req0, warps}
     uint4* jobB = jobA + P.max_jobs;                                 // {pred, conv | fe0<<16, fe1|fe2<<16, fe3|fe4<<16}
     uint16_t* ring = reinterpret_cast<uint16_t*>(jobB + P.max_jobs);  // requeue FIFO
@@ -347,7 +367,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
     for (;;) {
         unsigned long long tr = 0;
         if (lane == 0) tr = atomicAdd(P.counter, 1ull);
-        tr = __shfl_sync(FULL, tr, 0);
+        tr = g.shfl64(tr, 0);
         if (tr >= P.n_traces) break;
         const uint64_t j0 = P.off[tr] - j_base;
         const uint64_t n64 = P.off[tr + 1] - P.off[tr];
@@ -358,7 +378,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
             n = 0;
         }
         // ---- a1/a2: stage the trace (128-bit coalesced loads) and the per-job estimates ----
-        for (uint32_t j = lane; j < n; j += 32) {
+        for (uint32_t j = lane; j < n; j += GW) {
             const uint4 r = __ldg(P.jobs + j0 + j);
             const uint4 e = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
             const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
@@ -385,32 +405,32 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
             jobA[j] = A;
             jobB[j] = Bv;
         }
-        err = __reduce_or_sync(FULL, err);
+        err = g.bor(err);
 
         for (uint32_t p = 0; p < P.n_pol; ++p) {
             const mig_policy& pol = s_pol[p];
             const uint32_t kind = pol.kind;
             const bool fold = (pol.flags & MIG_WARP_FOLD) != 0;
             const bool er = (pol.flags & MIG_EARLY_RESTART) != 0;
-            __syncwarp();
-            for (uint32_t j = lane; j < n; j += 32) {
+            g.sync();
+            for (uint32_t j = lane; j < n; j += GW) {
                 const uint4 A = jobA[j];
                 jobA[j].x = (A.x & 0x00FFFFFFu) | (tight_fit_lane(G, A.z, A.w, fold) << 24);
             }
-            __syncwarp();
+            g.sync();
             TraceOut o;
             if (kind == MIG_FUSION_FISSION)
-                o = simulate_trace<MIG_FUSION_FISSION>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
-                                                       pol.reconfig_ticks, full_mem);
+                o = simulate_trace<MIG_FUSION_FISSION, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                                           pol.reconfig_ticks, full_mem);
             else if (kind == MIG_DYNAMIC)
-                o = simulate_trace<MIG_DYNAMIC>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
-                                                pol.reconfig_ticks, full_mem);
+                o = simulate_trace<MIG_DYNAMIC, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                                    pol.reconfig_ticks, full_mem);
             else if (kind == MIG_STATIC)
-                o = simulate_trace<MIG_STATIC>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
-                                               pol.reconfig_ticks, full_mem);
+                o = simulate_trace<MIG_STATIC, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                                   pol.reconfig_ticks, full_mem);
             else
-                o = simulate_trace<MIG_BASELINE>(G, lane, n, jobA, jobB, ring, P.ring_cap, er, fold,
-                                                 pol.reconfig_ticks, full_mem);
+                o = simulate_trace<MIG_BASELINE, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                                                     pol.reconfig_ticks, full_mem);
             // ---- a11: per-trace result (80 B, five 128-bit stores from lanes 0-4) ----
             const uint32_t placements = o.K0 & 0xFFFFu, creates = o.K0 >> 16, destroys = o.K1 & 0xFFFFu,
                            waits = o.K1 >> 16, rejected = o.K2 & 0xFFFFu, ooms = o.K2 >> 16,
@@ -424,14 +444,13 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
                 else if (lane == 2) v = make_uint4(placements, waits, creates, destroys);
                 else if (lane == 3) v = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)o.turn,
                                                    (uint32_t)(o.turn >> 32));
-                else v = make_uint4((uint32_t)o.busy, (uint32_t)(o.busy >> 32), (uint32_t)o.hash,
-                                    (uint32_t)(o.hash >> 32));
+                else v = make_uint4((uint32_t)o.busy, (uint32_t)(o.busy >> 32), o.hl, o.hh);
                 reinterpret_cast<uint4*>(P.out + tr * P.n_pol + p)[lane] = v;
             }
             // ---- a12: per-policy totals (shared-memory atomics, flushed once per CTA) ----
-            if (lane < 19) {
+            for (uint32_t f = lane; f < 19; f += GW) {
                 uint64_t v;
-                switch (lane) {
+                switch (f) {
                     case 0: v = 1; break;
                     case 1: v = n; break;
                     case 2: v = completed; break;
@@ -449,12 +468,12 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
                     case 14: v = energy; break;
                     case 15: v = o.turn; break;
                     case 16: v = o.busy; break;
-                    case 17: v = o.hash; break;
+                    case 17: v = ((uint64_t)o.hh << 32) | o.hl; break;
                     default: v = err; break;
                 }
-                if (lane == 13) atomicMax(&s_tot[p * 20 + 13], (unsigned long long)v);
-                else if (lane == 18) { if (v) atomicOr(&s_tot[p * 20 + 18], (unsigned long long)v); }
-                else atomicAdd(&s_tot[p * 20 + lane], (unsigned long long)v);
+                if (f == 13) atomicMax(&s_tot[p * 20 + 13], (unsigned long long)v);
+                else if (f == 18) { if (v) atomicOr(&s_tot[p * 20 + 18], (unsigned long long)v); }
+                else atomicAdd(&s_tot[p * 20 + f], (unsigned long long)v);
             }
         }
     }
@@ -472,9 +491,40 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
     }
 }
 
-size_t simulate_smem_bytes(uint32_t max_jobs) {
-    const size_t per_warp = (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u);
-    return kGeomBytes + kPolBytes + kTotBytes + kWarps * per_warp;
+size_t simulate_smem_bytes(uint32_t max_jobs, int gw) {
+    const size_t per_group = (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u);
+    return kGeomBytes + kPolBytes + kTotBytes + (size_t)(kWarps * 32 / gw) * per_group;
+}
+
+template <int GW>
+static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n_traces, int sm_count,
+                             cudaStream_t stream) {
+    const size_t smem = simulate_smem_bytes(P.max_jobs, GW);
+    cudaError_t e = cudaFuncSetAttribute(k_simulate<GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate<GW>, kWarps * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t groups = (uint64_t)kWarps * 32 / GW;
+    uint64_t want = (n_traces + groups - 1) / groups;
+    uint64_t blocks = (uint64_t)per_sm * sm_count;
+    if (want < blocks) blocks = want;
+    if (blocks < 1) blocks = 1;
+    k_simulate<GW><<<(unsigned)blocks, kWarps * 32, smem, stream>>>(Gdev, P);
+    return cudaGetLastError();
+}
+
+// Lanes per trace: 8 (four traces per warp) unless MIG_LANES_PER_TRACE=32 (one trace per warp) or the staged
+// traces would not fit shared memory four to a warp.
+int simulate_group_width(uint32_t max_jobs) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* env = getenv("MIG_LANES_PER_TRACE");
+        forced = env ? atoi(env) : 0;
+    }
+    if (forced == 32 || forced == 8) return forced;
+    return simulate_smem_bytes(max_jobs, 8) <= 200 * 1024 ? 8 : 32;
 }
 
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
@@ -497,19 +547,8 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     P.n_pol = n_pol;
     P.ctx = pols[0].ctx_mib;
     for (uint32_t i = 0; i < n_pol; ++i) P.pol[i] = pols[i];
-    const size_t smem = simulate_smem_bytes(tr.max_jobs);
-    cudaError_t e = cudaFuncSetAttribute(k_simulate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate, kWarps * 32, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    uint64_t want = (tr.n_traces + kWarps - 1) / kWarps;
-    uint64_t blocks = (uint64_t)per_sm * sm_count;
-    if (want < blocks) blocks = want;
-    if (blocks < 1) blocks = 1;
-    k_simulate<<<(unsigned)blocks, kWarps * 32, smem, stream>>>(Gdev, P);
-    return cudaGetLastError();
+    if (simulate_group_width(tr.max_jobs) == 8) return launch_gw<8>(Gdev, P, tr.n_traces, sm_count, stream);
+    return launch_gw<32>(Gdev, P, tr.n_traces, sm_count, stream);
 }
 
 }  // namespace mig
