@@ -21,6 +21,7 @@
 // (80 B) are written with 128-bit stores; per-policy totals are reduced in shared memory and added to global
 // memory once per CTA.
 #include <stdlib.h>
+#include <string.h>
 
 #include "device_common.cuh"
 
@@ -44,7 +45,7 @@ struct SimParams {
 constexpr size_t kGeomBytes = (sizeof(DevGeom) + 15) & ~size_t(15);
 constexpr size_t kPolBytes = (kMaxPolicies * sizeof(mig_policy) + 15) & ~size_t(15);
 constexpr size_t kTotBytes = kMaxPolicies * 20 * 8;
-constexpr int kWarps = 8;  // warps (traces in flight) per CTA
+constexpr int kWarps = 4;  // warps per CTA
 constexpr uint32_t kValid = 1u << 31, kBusy = 1u << 30;
 
 // A lane group of GW lanes simulates one trace (GW = 32: one trace per warp; GW = 8: four traces per warp).
@@ -97,6 +98,52 @@ __device__ __forceinline__ uint32_t overlap_extent(uint32_t occ, uint32_t SM, ui
     return occ & ((2u << b) - 1u) & ~((1u << a) - 1u);
 }
 
+// Staged jobs of one trace in shared memory.
+//   WIDE (32 B/job, short traces): A = {T | cls<<16 | need<<24, ticks, req0, warps},
+//                                  B = {pred, conv | fe0<<16, fe1 | fe2<<16, fe3 | fe4<<16}
+//   NARROW (16 B/job, long traces): A = {T | cls<<16 | need<<24, ticks, phys (STATIC/MODEL) | pred (DYNAMIC),
+//                                  conv (DYNAMIC)}; the first-exceed iterations of a DYNAMIC job are read from
+//                                  the estimate buffer at run start, req0 and warps from the trace records.
+template <bool WIDE>
+struct JobStore {
+    uint4* A;
+    const uint4* B;
+    const uint4* gjobs;  // this trace's records (global)
+    const uint4* gext;
+    const mig_job_estimate* gest;
+    uint32_t ctx;
+
+    __device__ __forceinline__ uint32_t need(uint32_t j) const { return A[j].x >> 24; }
+    __device__ __forceinline__ void set_need(uint32_t j, uint32_t nd) const {
+        A[j].x = (A[j].x & 0x00FFFFFFu) | (nd << 24);
+    }
+    __device__ __forceinline__ uint32_t warps(uint32_t j) const {
+        return WIDE ? A[j].w : (gext ? __ldg(&gext[j].y) : 0u);
+    }
+    __device__ __forceinline__ uint32_t pred(uint32_t j) const { return WIDE ? B[j].x : A[j].z; }
+    // T, ticks, first-exceed iteration of memory level lev, converged forecast (pred, conv; conv = 0 if none)
+    __device__ __forceinline__ void run_info(const DevGeom& G, uint32_t j, uint32_t lev, uint32_t& T, uint32_t& ticks,
+                                             uint32_t& fe, uint32_t& pred, uint32_t& conv) const {
+        const uint4 a = A[j];
+        T = a.x & 0xFFFFu;
+        ticks = a.y;
+        if (WIDE) {
+            const uint4 b = B[j];
+            pred = b.x;
+            conv = b.y & 0xFFFFu;
+            fe = reinterpret_cast<const uint16_t*>(&B[j])[3 + lev];
+        } else if (((a.x >> 16) & 0xFFu) == kClassDynamic) {
+            pred = a.z;
+            conv = a.w & 0xFFFFu;
+            fe = __ldg(reinterpret_cast<const unsigned short*>(gest + j) + 6 + lev);
+        } else {
+            pred = 0;
+            conv = 0;
+            fe = (T >= 1 && a.z > G.level_mem[lev]) ? 1u : kNever;  // R12: static jobs OOM at iteration 1
+        }
+    }
+};
+
 struct TraceOut {
     uint32_t K0, K1, K2, K3;  // placements|creates<<16, destroys|waits<<16, rejected|ooms<<16, preempts|failed<<16
     uint64_t turn, busy;
@@ -105,10 +152,10 @@ struct TraceOut {
 };
 
 // One trace under one policy kind (Alg. 4 PAPER.md:601-617 + the partition manager).
-template <int KIND, int GW>
-__device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<GW>& g, uint32_t n, uint4* jobA,
-                                                   const uint4* jobB, uint16_t* ring, uint32_t ring_cap, bool er,
-                                                   bool fold, uint32_t reconfig, uint32_t full_mem) {
+template <int KIND, int GW, bool WIDE>
+__device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<GW>& g, uint32_t n,
+                                                   const JobStore<WIDE>& J, uint16_t* ring, uint32_t ring_cap,
+                                                   bool er, bool fold, uint32_t reconfig, uint32_t full_mem) {
     const uint32_t lane = g.gl;
     uint32_t ii = 0, iend = 0, ijk = 0;  // lane-resident instance (slot = lane)
     uint32_t occ = 0, SM = 0, EM = 0, BM = 0;
@@ -134,7 +181,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
         // ---------------- scheduler pass at tick t (head-of-line; wake on every event tick, R9) ----------------
         while (qh < n || rn != 0) {
             const uint32_t j = qh < n ? qh : (uint32_t)ring[rh];
-            const uint32_t need = jobA[j].x >> 24;
+            const uint32_t need = J.need(j);
             const uint32_t jsh = j << 16;
             if (need == 0xFFu) {  // no profile can ever hold the job: REJECT
                 rec(o.hl, o.hh, t, jsh | (K_REJECT << 12) | 0xFF0u);
@@ -233,16 +280,13 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
                 rec(o.hl, o.hh, t, jsh | (kd << 12) | (s << 8) | (prof << 4) | nd);
                 o.K0 += created ? 0x10001u : 1u;
                 o.K1 += nd;
-                const uint4 A = jobA[j];
-                const uint4 Bv = jobB[j];
                 const uint32_t lev = si & 0xFu;
-                const uint32_t T = A.x & 0xFFFFu, ticks = A.y;
-                const uint32_t fe = reinterpret_cast<const uint16_t*>(&jobB[j])[3 + lev];
+                uint32_t T, ticks, fe, pred, conv;  // conv = 0 unless a converged DYNAMIC forecast
+                J.run_info(G, j, lev, T, ticks, fe, pred, conv);
                 const uint32_t rs = t + (created ? reconfig : 0u);
                 const uint32_t cap = G.level_mem[lev];
                 uint32_t i_pre = 0xFFFFFFFFu;
-                const uint32_t conv = Bv.y & 0xFFFFu;  // 0 unless a converged DYNAMIC forecast
-                if (KIND != MIG_BASELINE && er && conv > 0 && Bv.x > cap && cap < full_mem) i_pre = conv;
+                if (KIND != MIG_BASELINE && er && conv > 0 && pred > cap && cap < full_mem) i_pre = conv;
                 uint32_t end, ek;
                 if (fe <= min(T, i_pre)) {  // OOM > COMPLETE > PREEMPT in one iteration (R29); NEVER = 0xFFFF > T
                     ek = 1;
@@ -307,13 +351,13 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
             } else {  // PREEMPT: restart on the slice meeting the forecast (R25)
                 rec(o.hl, o.hh, t, lo | (K_PREEMPT << 12));
                 o.K3 += 1u;
-                req = min(jobB[job].x, full_mem);
+                req = min(J.pred(job), full_mem);
             }
             if (req) {  // back to the queue tail (R13) with the new tight fit
-                const uint32_t need = tight_fit_lane(G, req, jobA[job].w, fold);
+                const uint32_t need = tight_fit_lane(G, req, J.warps(job), fold);
                 g.sync();
                 if (lane == 0) {
-                    jobA[job].x = (jobA[job].x & 0x00FFFFFFu) | (need << 24);
+                    J.set_need(job, need);
                     uint32_t pos = rh + rn;
                     if (pos >= ring_cap) pos -= ring_cap;
                     ring[pos] = (uint16_t)job;
@@ -336,19 +380,19 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
     return o;
 }
 
-template <int GW>
-__global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
+template <int GW, bool WIDE>
+__global__ void __launch_bounds__(kWarps * 32, 8) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     DevGeom& G = *reinterpret_cast<DevGeom*>(smem);
     mig_policy* s_pol = reinterpret_cast<mig_policy*>(smem + kGeomBytes);
     unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(smem + kGeomBytes + kPolBytes);
     const Grp<GW> g(threadIdx.x & 31u);
     const uint32_t lane = g.gl, group = threadIdx.x / GW;
-    const uint32_t per_group = P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u);
+    const uint32_t per_group = P.max_jobs * (WIDE ? 32u : 16u) + ((P.max_jobs * 2u + 15u) & ~15u);
     uint8_t* wb = smem + kGeomBytes + kPolBytes + kTotBytes + group * per_group;
-    uint4* jobA = reinterpret_cast<uint4*>(wb);                      // {T | cls<<16 | need<<24, ticks, req0, warps}
-    uint4* jobB = jobA + P.max_jobs;                                 // {pred, conv | fe0<<16, fe1|fe2<<16, fe3|fe4<<16}
-    uint16_t* ring = reinterpret_cast<uint16_t*>(jobB + P.max_jobs);  // requeue FIFO
+    uint4* jobA = reinterpret_cast<uint4*>(wb);
+    uint4* jobB = WIDE ? jobA + P.max_jobs : nullptr;
+    uint16_t* ring = reinterpret_cast<uint16_t*>(jobA + P.max_jobs * (WIDE ? 2u : 1u));  // requeue FIFO
 
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
@@ -386,24 +430,38 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
             uint4 A, Bv;
             A.x = T | (cls << 16);
             A.y = r.w;
-            A.w = e.y;
             if (cls == kClassDynamic) {
                 const uint4* es = reinterpret_cast<const uint4*>(P.est + j0 + j);
-                const uint4 e0 = __ldg(es), e1 = __ldg(es + 1);
-                A.z = e0.x;  // req0 (smallest slice, R16)
-                Bv = make_uint4(e0.y, (e0.z & 0xFFFFu) | (e0.w << 16), (e0.w >> 16) | (e1.x << 16),
-                                (e1.x >> 16) | (e1.y << 16));
+                const uint4 e0 = __ldg(es);
+                if (WIDE) {
+                    const uint4 e1 = __ldg(es + 1);
+                    A.z = e0.x;  // req0 (smallest slice, R16)
+                    A.w = e.y;
+                    Bv = make_uint4(e0.y, (e0.z & 0xFFFFu) | (e0.w << 16), (e0.w >> 16) | (e1.x << 16),
+                                    (e1.x >> 16) | (e1.y << 16));
+                } else {
+                    A.z = e0.y;             // pred
+                    A.w = e0.z & 0xFFFFu;   // conv
+                }
             } else {
-                A.z = r.x + e.x + P.ctx;  // est + ws + ctx
-                const uint64_t phys = (uint64_t)r.y + e.x + P.ctx;
-                uint32_t fe[5];
+                // physical footprint true + ws + ctx; exceeds level l at iteration 1 or never (R12)
+                const uint64_t phys64 = (uint64_t)r.y + e.x + P.ctx;
+                const uint32_t phys = phys64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)phys64;
+                if (WIDE) {
+                    A.z = r.x + e.x + P.ctx;  // req0 = est + ws + ctx
+                    A.w = e.y;
+                    uint32_t fe[5];
 #pragma unroll
-                for (int l = 0; l < kMaxLevels; ++l)
-                    fe[l] = (l < (int)G.n_levels && T >= 1 && phys > G.level_mem[l]) ? 1u : kNever;
-                Bv = make_uint4(0u, fe[0] << 16, fe[1] | (fe[2] << 16), fe[3] | (fe[4] << 16));
+                    for (int l = 0; l < kMaxLevels; ++l)
+                        fe[l] = (l < (int)G.n_levels && T >= 1 && phys > G.level_mem[l]) ? 1u : kNever;
+                    Bv = make_uint4(0u, fe[0] << 16, fe[1] | (fe[2] << 16), fe[3] | (fe[4] << 16));
+                } else {
+                    A.z = phys;
+                    A.w = 0;
+                }
             }
             jobA[j] = A;
-            jobB[j] = Bv;
+            if (WIDE) jobB[j] = Bv;
         }
         err = g.bor(err);
 
@@ -415,21 +473,32 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
             g.sync();
             for (uint32_t j = lane; j < n; j += GW) {
                 const uint4 A = jobA[j];
-                jobA[j].x = (A.x & 0x00FFFFFFu) | (tight_fit_lane(G, A.z, A.w, fold) << 24);
+                uint32_t req0, warps;
+                if (WIDE) {
+                    req0 = A.z;
+                    warps = A.w;
+                } else {  // re-read the record: req0 = est + ws + ctx, or the smallest slice (DYNAMIC, R16)
+                    const uint4 r = __ldg(P.jobs + j0 + j);
+                    const uint4 e = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
+                    req0 = ((r.z >> 16) & 0xFFu) == kClassDynamic ? G.mem[0] : r.x + e.x + P.ctx;
+                    warps = e.y;
+                }
+                jobA[j].x = (A.x & 0x00FFFFFFu) | (tight_fit_lane(G, req0, warps, fold) << 24);
             }
             g.sync();
+            const JobStore<WIDE> J{jobA, jobB, P.jobs + j0, P.ext ? P.ext + j0 : nullptr, P.est + j0, P.ctx};
             TraceOut o;
             if (kind == MIG_FUSION_FISSION)
-                o = simulate_trace<MIG_FUSION_FISSION, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_FUSION_FISSION, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
                                                            pol.reconfig_ticks, full_mem);
             else if (kind == MIG_DYNAMIC)
-                o = simulate_trace<MIG_DYNAMIC, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_DYNAMIC, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
                                                     pol.reconfig_ticks, full_mem);
             else if (kind == MIG_STATIC)
-                o = simulate_trace<MIG_STATIC, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_STATIC, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
                                                    pol.reconfig_ticks, full_mem);
             else
-                o = simulate_trace<MIG_BASELINE, GW>(G, g, n, jobA, jobB, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_BASELINE, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
                                                      pol.reconfig_ticks, full_mem);
             // ---- a11: per-trace result (80 B, five 128-bit stores from lanes 0-4) ----
             const uint32_t placements = o.K0 & 0xFFFFu, creates = o.K0 >> 16, destroys = o.K1 & 0xFFFFu,
@@ -491,19 +560,19 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_simulate(const DevGeom* __re
     }
 }
 
-size_t simulate_smem_bytes(uint32_t max_jobs, int gw) {
-    const size_t per_group = (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u);
+size_t simulate_smem_bytes(uint32_t max_jobs, int gw, bool wide) {
+    const size_t per_group = (size_t)max_jobs * (wide ? 32u : 16u) + ((max_jobs * 2u + 15u) & ~15u);
     return kGeomBytes + kPolBytes + kTotBytes + (size_t)(kWarps * 32 / gw) * per_group;
 }
 
-template <int GW>
+template <int GW, bool WIDE>
 static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n_traces, int sm_count,
                              cudaStream_t stream) {
-    const size_t smem = simulate_smem_bytes(P.max_jobs, GW);
-    cudaError_t e = cudaFuncSetAttribute(k_simulate<GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = simulate_smem_bytes(P.max_jobs, GW, WIDE);
+    cudaError_t e = cudaFuncSetAttribute(k_simulate<GW, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate<GW>, kWarps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate<GW, WIDE>, kWarps * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint64_t groups = (uint64_t)kWarps * 32 / GW;
@@ -511,7 +580,7 @@ static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n
     uint64_t blocks = (uint64_t)per_sm * sm_count;
     if (want < blocks) blocks = want;
     if (blocks < 1) blocks = 1;
-    k_simulate<GW><<<(unsigned)blocks, kWarps * 32, smem, stream>>>(Gdev, P);
+    k_simulate<GW, WIDE><<<(unsigned)blocks, kWarps * 32, smem, stream>>>(Gdev, P);
     return cudaGetLastError();
 }
 
@@ -524,7 +593,18 @@ int simulate_group_width(uint32_t max_jobs) {
         forced = env ? atoi(env) : 0;
     }
     if (forced == 32 || forced == 8) return forced;
-    return simulate_smem_bytes(max_jobs, 8) <= 200 * 1024 ? 8 : 32;
+    return simulate_smem_bytes(max_jobs, 8, false) <= 200 * 1024 ? 8 : 32;
+}
+
+// Staging layout: 32 B/job for short traces (everything on chip), 16 B/job for long ones (occupancy).
+bool simulate_wide_layout(uint32_t max_jobs) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* env = getenv("MIG_JOB_LAYOUT");
+        forced = env ? (strcmp(env, "wide") == 0 ? 1 : strcmp(env, "narrow") == 0 ? 2 : 0) : 0;
+    }
+    if (forced) return forced == 1;
+    return max_jobs <= 32;
 }
 
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
@@ -547,8 +627,12 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     P.n_pol = n_pol;
     P.ctx = pols[0].ctx_mib;
     for (uint32_t i = 0; i < n_pol; ++i) P.pol[i] = pols[i];
-    if (simulate_group_width(tr.max_jobs) == 8) return launch_gw<8>(Gdev, P, tr.n_traces, sm_count, stream);
-    return launch_gw<32>(Gdev, P, tr.n_traces, sm_count, stream);
+    const bool wide = simulate_wide_layout(tr.max_jobs);
+    if (simulate_group_width(tr.max_jobs) == 8)
+        return wide ? launch_gw<8, true>(Gdev, P, tr.n_traces, sm_count, stream)
+                    : launch_gw<8, false>(Gdev, P, tr.n_traces, sm_count, stream);
+    return wide ? launch_gw<32, true>(Gdev, P, tr.n_traces, sm_count, stream)
+                : launch_gw<32, false>(Gdev, P, tr.n_traces, sm_count, stream);
 }
 
 }  // namespace mig

@@ -1,0 +1,43 @@
+"""Every k_simulate variant (lanes per trace 8 | 32, job staging layout wide | narrow) is parity-checked against
+the oracle. The variant is chosen per process from MIG_LANES_PER_TRACE / MIG_JOB_LAYOUT, so each runs in a
+subprocess."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r'''
+import sys
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+import numpy as np
+from test_parity_gpu import run_pair, assert_same, check_totals, random_tiny_traces, SPECS
+from tracegen import tracegen as tg
+import json
+from conftest import geom_path
+for cfg, n in [(2, 300), (3, 400), (4, 1500), (5, 200)]:
+    jobs, ext, off = tg.generate_host(cfg, n)
+    got, want, tot = run_pair(tg.CONFIG_GEOMETRY[cfg], jobs, ext, off, SPECS, seed=tg.seed_of(cfg))
+    assert_same(got, want)
+    check_totals(got, tot)
+spec = json.load(open(geom_path("a100-40gb")))
+jobs, ext, off = random_tiny_traces(np.random.default_rng(3), spec, 300, 60)
+specs = SPECS + [dict(kind=3, flags=3)]
+got, want, tot = run_pair("a100-40gb", jobs, ext, off, specs, seed=7, common=dict(ctx_mib=256, reconfig_ticks=100))
+assert_same(got, want)
+print("variant OK")
+'''
+
+
+@pytest.mark.parametrize("lanes", ["8", "32"])
+@pytest.mark.parametrize("layout", ["wide", "narrow"])
+def test_variant_parity(lanes, layout):
+    env = dict(os.environ, MIG_LANES_PER_TRACE=lanes, MIG_JOB_LAYOUT=layout)
+    code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "variant OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
