@@ -81,18 +81,22 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     const uint32_t b = r.x, q0 = r.y, ws = e.x, slope = e.z, sigma_n = e.w & 0xFFFFu, qs = e.w >> 16;
     const uint64_t key = tg_key(P.seed, trace_id, jidx);
     const int64_t ws_ctx = (int64_t)ws + P.ctx;
-    int64_t thr[kMaxLevels];
     uint32_t fe[5] = {kNever, kNever, kNever, kNever, kNever};
+    auto lvl_thr = [&](uint32_t l) -> int64_t { return (int64_t)G.level_mem[l] - ws_ctx; };  // phys > L <=> floor > thr
+    auto fe_set = [&](uint32_t l, uint32_t v) {
 #pragma unroll
-    for (int l = 0; l < kMaxLevels; ++l) thr[l] = (int64_t)G.level_mem[l] - ws_ctx;  // phys > L <=> floor > thr
-    uint32_t fe_left = G.n_levels;
+        for (int k = 0; k < kMaxLevels; ++k)
+            if ((uint32_t)k == l) fe[k] = v;
+    };
+    const bool q_unit = q0 == 65536u && qs == 0;  // constant inverse reuse 1.0: phys = y + ws + ctx
+    uint32_t lnext = 0;                          // lowest level whose first exceed is not yet known
     int64_t Sy = 0, Sty = 0, Syy = 0, Sq = 0, Stq = 0, Plast = 0;
     uint32_t okprev = 0, conv = 0, pred = 0;
     double phi = 0.0, a = 0.0, sig = 0.0;
     bool done_pred = T < P.min_n;
     bool bad = false;
     for (uint32_t base = 0; base < T; base += 32) {
-        if (done_pred && fe_left == 0) break;
+        if (done_pred && lnext >= G.n_levels) break;
         const uint32_t n = base + lane + 1;
         const bool valid = n <= T;
         uint32_t y = 0, q = 0;
@@ -100,19 +104,17 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
             tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
             bad |= (q == 0) | (y >= (1u << 18));
         }
-        // first-exceed iteration of every memory level (R12): phys(i) = floor(y*65536/q) + ws + ctx > L
-        if (fe_left) {
-#pragma unroll
-            for (int l = 0; l < kMaxLevels; ++l) {
-                if (l < (int)G.n_levels && fe[l] == kNever) {
-                    bool over = valid && (thr[l] < 0 || (uint64_t)y * 65536ull >= (uint64_t)(thr[l] + 1) * q);
-                    uint32_t m = __ballot_sync(FULL, over);
-                    if (m) {
-                        fe[l] = base + __ffs(m);
-                        --fe_left;
-                    }
-                }
-            }
+        // first-exceed iteration of every memory level (R12): phys(i) = floor(y*65536/q) + ws + ctx > L.
+        // Levels ascend, so fe[l] <= fe[l+1]: only the lowest level not yet crossed needs a ballot per chunk
+        // (more when one chunk crosses several levels).
+        while (lnext < G.n_levels) {
+            const int64_t th = lvl_thr(lnext);
+            const bool over = valid && (th < 0 || (q_unit ? (int64_t)y > th
+                                                           : (uint64_t)y * 65536ull >= (uint64_t)(th + 1) * q));
+            const uint32_t m = __ballot_sync(FULL, over);
+            if (!m) break;
+            fe_set(lnext, base + __ffs(m));
+            ++lnext;
         }
         if (done_pred) continue;
         // exact integer moments at n = base + lane + 1 (inclusive warp scans + carried totals)
@@ -167,7 +169,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig);
 }
 
-__global__ void __launch_bounds__(256) k_estimate(const DevGeom G, const EstParams P) {
+__global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstParams P) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t j_base = P.off[0];
     for (;;) {

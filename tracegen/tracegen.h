@@ -67,12 +67,13 @@ TG_HD uint32_t tg_octave(uint64_t r, uint32_t a, uint32_t b) {
     return (1u << e) + (uint32_t)(((r & 0xFFFFFFFFull) * (uint64_t)(1u << e)) >> 32);
 }
 
-/* Irwin-Hall(4) noise with standard deviation ~sigma: (sum of four 16-bit uniforms - 131070) * sigma / 37838,
- * truncating division (C and CUDA agree). No log/cos, so host and device are bit-identical. */
+/* Irwin-Hall(4) noise with standard deviation ~sigma: (sum of four 16-bit uniforms - 131070) has standard
+ * deviation 37837.6 = 2^28 / 7094.3, so noise = floor((sum - 131070) * (sigma * 7094) / 2^28) (one 32x32->64
+ * multiply and an arithmetic shift; sigma < 2^16). No log/cos/division, so host and device are bit-identical. */
 TG_HD int32_t tg_irwin_hall(uint64_t r, uint32_t sigma) {
-    int64_t s = (int64_t)(r & 0xFFFF) + (int64_t)((r >> 16) & 0xFFFF) + (int64_t)((r >> 32) & 0xFFFF) +
-                (int64_t)((r >> 48) & 0xFFFF);
-    return (int32_t)(((s - 131070) * (int64_t)sigma) / 37838);
+    int32_t s = (int32_t)(r & 0xFFFF) + (int32_t)((r >> 16) & 0xFFFF) + (int32_t)((r >> 32) & 0xFFFF) +
+                (int32_t)((r >> 48) & 0xFFFF);
+    return (int32_t)(((int64_t)(s - 131070) * (int64_t)(int32_t)((sigma & 0xFFFFu) * 7094u)) >> 28);
 }
 
 /* Per-iteration sample i (1-based) of a DYNAMIC job: requested MiB y_i (allocator-rounded up to 2 MiB, >= 2) and
