@@ -218,6 +218,7 @@ def run_mine(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     import paper_2508_18556_b200 as mig
+    from paper_2508_18556_b200.sharding import reduce_totals, shard_range
     from tracegen import tracegen as tg
 
     stream = torch.cuda.current_stream(dev)
@@ -225,7 +226,7 @@ def run_mine(args):
     pols = [mig.policy(g, kind=k, flags=f) for k, f in wl["policies"]]
     n_pol = len(pols)
     seed = tg.seed_of(cfg)
-    t_id0 = rank * n_per
+    t_id0, _ = shard_range(rank, world, n_per_rank=n_per)
     jobs, ext, off = tg.generate_device(cfg, n_per, trace_id0=t_id0, seed=seed, device=dev)
     J = tg.jobs_per_trace(cfg)
     tr = mig.Traces(jobs, ext, off, n_per, seed=seed, trace_id0=t_id0, max_jobs=J)
@@ -250,11 +251,7 @@ def run_mine(args):
         if ev is not None:
             ev[2].record(stream)
         if world > 1:  # the per-policy metric reduce over NVLink (NCCL)
-            t64 = tot.view(torch.int64).view(n_pol, 20)
-            mx = t64[:, 13].clone()
-            dist.all_reduce(t64, op=dist.ReduceOp.SUM)
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            t64[:, 13] = mx
+            reduce_totals(tot.view(torch.int64).view(n_pol, 20), dist)
 
     for _ in range(args.warmup):
         step()
