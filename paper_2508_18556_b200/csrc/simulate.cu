@@ -45,7 +45,6 @@ struct SimParams {
 constexpr size_t kGeomBytes = (sizeof(DevGeom) + 15) & ~size_t(15);
 constexpr size_t kPolBytes = (kMaxPolicies * sizeof(mig_policy) + 15) & ~size_t(15);
 constexpr size_t kTotBytes = kMaxPolicies * 20 * 8;
-constexpr int kWarps = 4;  // warps per CTA
 constexpr uint32_t kValid = 1u << 31, kBusy = 1u << 30;
 
 // A lane group of GW lanes simulates one trace (GW = 32: one trace per warp; GW = 8: four traces per warp).
@@ -121,6 +120,9 @@ struct JobStore {
         return WIDE ? A[j].w : (gext ? __ldg(&gext[j].y) : 0u);
     }
     __device__ __forceinline__ uint32_t pred(uint32_t j) const { return WIDE ? B[j].x : A[j].z; }
+    // NARROW only: requeue FIFO as a linked list through the spare high half of A[j].w
+    __device__ __forceinline__ uint32_t next(uint32_t j) const { return A[j].w >> 16; }
+    __device__ __forceinline__ void set_next(uint32_t j, uint32_t nx) const { A[j].w = (A[j].w & 0xFFFFu) | (nx << 16); }
     // T, ticks, first-exceed iteration of memory level lev, converged forecast (pred, conv; conv = 0 if none)
     __device__ __forceinline__ void run_info(const DevGeom& G, uint32_t j, uint32_t lev, uint32_t& T, uint32_t& ticks,
                                              uint32_t& fe, uint32_t& pred, uint32_t& conv) const {
@@ -151,12 +153,73 @@ struct TraceOut {
     uint32_t makespan;
 };
 
+// BASELINE: the non-partitioned GPU runs one job at a time in queue order, so there is no
+// partition state and no requeue (an OOM on the whole GPU is FAILED). Straight-line code producing the same
+// decision/event record stream as the general loop: [REJECT]* PLACE [REJECT]* WAIT <event> PLACE ...
+template <bool WIDE>
+__device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n, const JobStore<WIDE>& J) {
+    TraceOut o;
+    o.K0 = o.K1 = o.K2 = o.K3 = 0;
+    o.turn = o.busy = 0;
+    o.hl = (uint32_t)kFnvOffset;
+    o.hh = (uint32_t)(kFnvOffset >> 32);
+    const uint32_t fp = G.full_prof, pi = G.pinfo[fp];
+    const uint32_t lev = pi & 0xFu, comp = (pi >> 4) & 0xFu;
+    const uint32_t place_lo = (K_PLACE_BASELINE << 12) | (fp << 4);  // slot 0
+    const uint32_t ev_lo = fp << 4;
+    uint32_t t = 0, qh = 0;
+    while (qh < n) {
+        uint32_t j = qh, need = J.need(j);
+        if (need == 0xFFu) {  // no profile can hold the job
+            rec(o.hl, o.hh, t, (j << 16) | (K_REJECT << 12) | 0xFF0u);
+            o.K2 += 1u;
+            ++qh;
+            continue;
+        }
+        rec(o.hl, o.hh, t, (j << 16) | place_lo);
+        o.K0 += 1u;
+        uint32_t T, ticks, fe, pred, conv;
+        J.run_info(G, j, lev, T, ticks, fe, pred, conv);
+        const bool oom = fe <= T;  // first exceed of the whole GPU (R12); no early restart on baseline
+        const uint32_t end = t + (oom ? fe : T) * ticks;
+        o.busy += (uint64_t)comp * (end - t);
+        ++qh;
+        while (qh < n) {  // the rest of the pass at t: rejections, then the head waits
+            const uint32_t need2 = J.need(qh);
+            if (need2 == 0xFFu) {
+                rec(o.hl, o.hh, t, (qh << 16) | (K_REJECT << 12) | 0xFF0u);
+                o.K2 += 1u;
+                ++qh;
+                continue;
+            }
+            rec(o.hl, o.hh, t, (qh << 16) | (K_WAIT << 12) | 0xF00u | (need2 << 4));
+            o.K1 += 1u << 16;
+            break;
+        }
+        t = end;  // the run's end event
+        if (oom) {
+            rec(o.hl, o.hh, t, (j << 16) | (K_OOM << 12) | ev_lo);
+            rec(o.hl, o.hh, t, (j << 16) | (K_FAILED << 12) | ev_lo);
+            o.K2 += 1u << 16;
+            o.K3 += 1u << 16;
+        } else {
+            rec(o.hl, o.hh, t, (j << 16) | (K_COMPLETE << 12) | ev_lo);
+            o.turn += t;
+        }
+    }
+    o.makespan = t;
+    return o;
+}
+
 // One trace under one policy kind (Alg. 4 PAPER.md:601-617 + the partition manager).
 template <int KIND, int GW, bool WIDE>
 __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<GW>& g, uint32_t n,
                                                    const JobStore<WIDE>& J, uint16_t* ring, uint32_t ring_cap,
                                                    bool er, bool fold, uint32_t reconfig, uint32_t full_mem) {
     const uint32_t lane = g.gl;
+    if constexpr (KIND == MIG_BASELINE) {
+        return baseline_trace<WIDE>(G, n, J);
+    }
     uint32_t ii = 0, iend = 0, ijk = 0;  // lane-resident instance (slot = lane)
     uint32_t occ = 0, SM = 0, EM = 0, BM = 0;
     if (KIND == MIG_BASELINE) {
@@ -175,12 +238,15 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
     o.turn = o.busy = 0;
     o.hl = (uint32_t)kFnvOffset;
     o.hh = (uint32_t)(kFnvOffset >> 32);
-    uint32_t t = 0, qh = 0, rh = 0, rn = 0;  // queue = jobs[qh..n) ++ ring[rh .. rh+rn) (requeues at the tail, R13)
+    // queue = jobs[qh..n) ++ requeued jobs (tail, R13): a u16 ring (WIDE) or a list linked through the staged
+    // records (NARROW; rh = head, rn = tail, 0xFFFF = empty)
+    constexpr uint32_t kNone = 0xFFFFu;
+    uint32_t t = 0, qh = 0, rh = WIDE ? 0u : kNone, rn = WIDE ? 0u : kNone;
 
     for (;;) {
         // ---------------- scheduler pass at tick t (head-of-line; wake on every event tick, R9) ----------------
-        while (qh < n || rn != 0) {
-            const uint32_t j = qh < n ? qh : (uint32_t)ring[rh];
+        while (qh < n || (WIDE ? rn != 0 : rh != kNone)) {
+            const uint32_t j = qh < n ? qh : (WIDE ? (uint32_t)ring[rh] : rh);
             const uint32_t need = J.need(j);
             const uint32_t jsh = j << 16;
             if (need == 0xFFu) {  // no profile can ever hold the job: REJECT
@@ -309,9 +375,12 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
         pop:
             if (qh < n) {
                 ++qh;
-            } else {
+            } else if (WIDE) {
                 rh = rh + 1 == ring_cap ? 0 : rh + 1;
                 --rn;
+            } else {
+                rh = J.next(rh);
+                if (rh == kNone) rn = kNone;
             }
         }
         // ---------------- next event: min end tick over running instances ----------------
@@ -358,12 +427,22 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
                 g.sync();
                 if (lane == 0) {
                     J.set_need(job, need);
-                    uint32_t pos = rh + rn;
-                    if (pos >= ring_cap) pos -= ring_cap;
-                    ring[pos] = (uint16_t)job;
+                    if (WIDE) {
+                        uint32_t pos = rh + rn;
+                        if (pos >= ring_cap) pos -= ring_cap;
+                        ring[pos] = (uint16_t)job;
+                    } else {
+                        J.set_next(job, kNone);
+                        if (rn != kNone) J.set_next(rn, job);
+                    }
                 }
                 g.sync();
-                ++rn;
+                if (WIDE) {
+                    ++rn;
+                } else {
+                    if (rn == kNone) rh = job;
+                    rn = job;
+                }
             }
             const uint32_t ext = ((si >> 8) & 0xFFu) << s;
             BM &= ~ext;
@@ -380,19 +459,19 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
     return o;
 }
 
-template <int GW, bool WIDE>
-__global__ void __launch_bounds__(kWarps * 32, 8) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
+template <int GW, bool WIDE, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     DevGeom& G = *reinterpret_cast<DevGeom*>(smem);
     mig_policy* s_pol = reinterpret_cast<mig_policy*>(smem + kGeomBytes);
     unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(smem + kGeomBytes + kPolBytes);
     const Grp<GW> g(threadIdx.x & 31u);
     const uint32_t lane = g.gl, group = threadIdx.x / GW;
-    const uint32_t per_group = P.max_jobs * (WIDE ? 32u : 16u) + ((P.max_jobs * 2u + 15u) & ~15u);
+    const uint32_t per_group = WIDE ? P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u) : P.max_jobs * 16u;
     uint8_t* wb = smem + kGeomBytes + kPolBytes + kTotBytes + group * per_group;
     uint4* jobA = reinterpret_cast<uint4*>(wb);
     uint4* jobB = WIDE ? jobA + P.max_jobs : nullptr;
-    uint16_t* ring = reinterpret_cast<uint16_t*>(jobA + P.max_jobs * (WIDE ? 2u : 1u));  // requeue FIFO
+    uint16_t* ring = WIDE ? reinterpret_cast<uint16_t*>(jobA + P.max_jobs * 2u) : nullptr;  // requeue FIFO (WIDE)
 
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
@@ -457,7 +536,7 @@ __global__ void __launch_bounds__(kWarps * 32, 8) k_simulate(const DevGeom* __re
                     Bv = make_uint4(0u, fe[0] << 16, fe[1] | (fe[2] << 16), fe[3] | (fe[4] << 16));
                 } else {
                     A.z = phys;
-                    A.w = 0;
+                    A.w = 0;  // conv = 0; high half: requeue link
                 }
             }
             jobA[j] = A;
@@ -560,27 +639,30 @@ __global__ void __launch_bounds__(kWarps * 32, 8) k_simulate(const DevGeom* __re
     }
 }
 
+constexpr int warps_per_cta(bool wide) { return wide ? 4 : 8; }
+
 size_t simulate_smem_bytes(uint32_t max_jobs, int gw, bool wide) {
-    const size_t per_group = (size_t)max_jobs * (wide ? 32u : 16u) + ((max_jobs * 2u + 15u) & ~15u);
-    return kGeomBytes + kPolBytes + kTotBytes + (size_t)(kWarps * 32 / gw) * per_group;
+    const size_t per_group = wide ? (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u) : (size_t)max_jobs * 16u;
+    return kGeomBytes + kPolBytes + kTotBytes + (size_t)(warps_per_cta(wide) * 32 / gw) * per_group;
 }
 
 template <int GW, bool WIDE>
 static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n_traces, int sm_count,
                              cudaStream_t stream) {
+    constexpr int kW = warps_per_cta(WIDE);
     const size_t smem = simulate_smem_bytes(P.max_jobs, GW, WIDE);
-    cudaError_t e = cudaFuncSetAttribute(k_simulate<GW, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_simulate<GW, WIDE, kW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate<GW, WIDE>, kWarps * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate<GW, WIDE, kW>, kW * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const uint64_t groups = (uint64_t)kWarps * 32 / GW;
+    const uint64_t groups = (uint64_t)kW * 32 / GW;
     uint64_t want = (n_traces + groups - 1) / groups;
     uint64_t blocks = (uint64_t)per_sm * sm_count;
     if (want < blocks) blocks = want;
     if (blocks < 1) blocks = 1;
-    k_simulate<GW, WIDE><<<(unsigned)blocks, kWarps * 32, smem, stream>>>(Gdev, P);
+    k_simulate<GW, WIDE, kW><<<(unsigned)blocks, kW * 32, smem, stream>>>(Gdev, P);
     return cudaGetLastError();
 }
 
