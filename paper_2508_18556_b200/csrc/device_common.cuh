@@ -34,6 +34,8 @@ __device__ __forceinline__ void hash_record(uint64_t& h, uint32_t tick, uint32_t
 // Canonical int128 -> double: sign-magnitude, hi*2^64 + lo, each u64
 // conversion and the addition rounded to nearest. Identical sequence to the oracle's.
 __device__ __forceinline__ double i128_to_double(__int128 x) {
+    const int64_t lo64 = (int64_t)x;
+    if ((__int128)lo64 == x) return __ll2double_rn(lo64);  // same single rounding as the canonical form
     bool neg = x < 0;
     unsigned __int128 m = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;
     uint64_t hi = (uint64_t)(m >> 64), lo = (uint64_t)m;

@@ -36,30 +36,40 @@ struct FitOut {
     double phi, a, sigma;
 };
 
-// One fit + forecast at n samples (oracle: fit_and_predict).
+// One fit + forecast at n samples (oracle: fit_and_predict). The slope
+// diagnostic a = 6K/D is computed once for the reported lane (estimate_dynamic). q_unit: the inverse reuse is
+// exactly 1.0 at every sample, so its forecast is exactly 65536 and V = 1 (the canonical sequence gives the same).
 __device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int64_t Syy, int64_t Sq, int64_t Stq,
-                                         int64_t T, double z, int64_t ws_ctx) {
+                                         int64_t T, double z, int64_t ws_ctx, bool q_unit) {
     const int64_t n2m1 = n * n - 1;
     const int64_t D = n * n2m1;
     const int64_t Ky = 2 * Sty - (n + 1) * Sy;
-    const int64_t Kq = 2 * Stq - (n + 1) * Sq;
     const int64_t h = 2 * T - n - 1;
-    __int128 numY = (__int128)Sy * n2m1 + (__int128)3 * Ky * h;
-    __int128 ssrN = (__int128)n2m1 * ((__int128)n * Syy - (__int128)Sy * Sy) - (__int128)3 * Ky * Ky;
-    __int128 numQ = (__int128)Sq * n2m1 + (__int128)3 * Kq * h;
+    const __int128 numY = (__int128)Sy * n2m1 + (__int128)3 * Ky * h;
+    const __int128 ssrN = (__int128)n2m1 * (__int128)(n * Syy - Sy * Sy) - (__int128)3 * Ky * Ky;  // n*Syy, Sy^2 < 2^62
     const double den = __ll2double_rn(D);
     FitOut f;
-    double yT = __ddiv_rn(i128_to_double(numY), den);
-    double var = __ddiv_rn(i128_to_double(ssrN), __ll2double_rn(D * (n - 2)));
+    const double yT = __ddiv_rn(i128_to_double(numY), den);
+    const double var = __ddiv_rn(i128_to_double(ssrN), __ll2double_rn(D * (n - 2)));
     f.sigma = __dsqrt_rn(var);
     double u = __dadd_rn(yT, __dmul_rn(z, f.sigma));
     if (u < 0.0) u = 0.0;
-    double V = __ddiv_rn(__ddiv_rn(i128_to_double(numQ), den), 65536.0);
-    if (V < 1.0) V = 1.0;
+    double V = 1.0;
+    if (!q_unit) {
+        const int64_t Kq = 2 * Stq - (n + 1) * Sq;
+        const __int128 numQ = (__int128)Sq * n2m1 + (__int128)3 * Kq * h;
+        V = __dmul_rn(__ddiv_rn(i128_to_double(numQ), den), 1.0 / 65536.0);  // exact power-of-two scaling
+        if (V < 1.0) V = 1.0;
+    }
     f.phi = __ddiv_rn(u, V);
-    f.a = __ddiv_rn(__ll2double_rn(6 * Ky), den);
+    f.a = 0.0;
     f.P = (int64_t)ceil(f.phi) + ws_ctx;
     return f;
+}
+
+__device__ __forceinline__ double slope_of(int64_t n, int64_t Sy, int64_t Sty) {
+    const int64_t Ky = 2 * Sty - (n + 1) * Sy;
+    return __ddiv_rn(__ll2double_rn(6 * Ky), __ll2double_rn(n * (n * n - 1)));
 }
 
 __device__ __forceinline__ void store_estimate(mig_job_estimate* dst, uint32_t req0, uint32_t pred, uint32_t conv,
@@ -126,7 +136,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         const int64_t stq = Stq + warp_scan_i64(valid ? ni * qi : 0, lane);
         const bool has = valid && n >= P.min_n;
         FitOut f = {0, 0.0, 0.0, 0.0};
-        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx);
+        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit);
         int64_t Pprev = __shfl_up_sync(FULL, f.P, 1);
         if (lane == 0) Pprev = Plast;
         const bool prev_has = n >= P.min_n + 1;
@@ -141,8 +151,9 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         const uint32_t last_lane = (T - 1 - base) < 32 ? (T - 1 - base) : 31;
         const uint32_t src = cm ? (uint32_t)(__ffs(cm) - 1) : last_lane;
         const int64_t Ps = __shfl_sync(FULL, f.P, src);
-        const double phs = __shfl_sync(FULL, f.phi, src), as = __shfl_sync(FULL, f.a, src),
-                     ss = __shfl_sync(FULL, f.sigma, src);
+        const double phs = __shfl_sync(FULL, f.phi, src), ss = __shfl_sync(FULL, f.sigma, src);
+        const int64_t nsrc = base + src + 1, sy_s = __shfl_sync(FULL, sy, src), sty_s = __shfl_sync(FULL, sty, src);
+        const double as = (cm || (base + 32 >= T && T >= P.min_n)) ? slope_of(nsrc, sy_s, sty_s) : 0.0;
         if (cm) {
             conv = base + src + 1;
             pred = (uint32_t)Ps;
