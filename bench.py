@@ -340,11 +340,12 @@ def run_mine(args):
     alu_peak = 148 * 4 * 32 * f_mhz * 1e6  # lane-ops/s: 4 SMSPs x 1 warp-instruction/cycle x 32 lanes per SM
     ops_sim = (OPS_PER_DECISION * dec_step + OPS_PER_EVENT * events_step + OPS_PER_JOB_STAGE * jobs_step * n_pol) / world
     achieved = ops_sim / (sim_ms * 1e-3)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", f"traffic_config{cfg}.json")
-    if os.path.exists(prof):
+    traffic, ncu = None, {}
+    prof = os.path.join(ROOT, "profiles", f"ncu_config{cfg}.json")
+    if os.path.exists(prof) and n_per == wl["traces"]:
         with open(prof) as f:
-            traffic = json.load(f).get("k_simulate_dram_bytes_per_launch")
+            ncu = json.load(f)
+        traffic = ncu.get("k_simulate_dram_bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": "decisions/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -361,7 +362,10 @@ def run_mine(args):
                      "unit": "int lane-ops/s", "frac": achieved / alu_peak, "traffic": traffic,
                      "peak_source": f"148 SMs x 4 SMSP x 32 lanes x {f_mhz:.0f} MHz ({peak_src} sm_max_mhz)",
                      "ops_model": f"{OPS_PER_DECISION}/decision + {OPS_PER_EVENT}/event + "
-                                  f"{OPS_PER_JOB_STAGE}/job/policy (DESIGN.md)"},
+                                  f"{OPS_PER_JOB_STAGE}/job/policy (DESIGN.md)",
+                     "ncu_issue_slot_util": ncu.get("k_simulate_issue_slot_util"),
+                     "ncu_active_lanes_per_instr": ncu.get("k_simulate_active_lanes_per_instr"),
+                     "ncu_source": ncu.get("source")},
         "hbm": {"algorithmic_bytes_per_launch": tr.n_jobs * 16 + n_per * n_pol * 80 + tr.n_jobs * 48 * 0,
                 "peak_gbs": peaks.get("hbm_gbs")},
         "cpu_baseline": cpu,

@@ -87,8 +87,6 @@ mig_status check_traces(const mig_traces* tr) {
 mig_status check_policy(const mig_policy& p) {
     if (p.kind > MIG_FUSION_FISSION) return mig_set_error(MIG_E_INVALID_ARG, "policy.kind out of range");
     if (p.flags & ~7u) return mig_set_error(MIG_E_INVALID_ARG, "unknown policy flag");
-    if (p.flags & MIG_EWMA_REUSE)
-        return mig_set_error(MIG_E_UNSUPPORTED, "MIG_EWMA_REUSE is not implemented on the device path");
     if (p.min_n < 3) return mig_set_error(MIG_E_INVALID_ARG, "policy.min_n must be >= 3");
     if (p.conv_k < 1 || p.conv_k > 32) return mig_set_error(MIG_E_INVALID_ARG, "policy.conv_k must be 1..32");
     if (p.eps_den == 0) return mig_set_error(MIG_E_INVALID_ARG, "policy.eps_den must be > 0");
@@ -107,9 +105,9 @@ mig_status check_policies(const mig_geometry* g, const mig_policy* pols, uint32_
         const mig_policy& a = pols[0];
         const mig_policy& b = pols[i];
         if (a.ctx_mib != b.ctx_mib || a.z != b.z || a.eps_num != b.eps_num || a.eps_den != b.eps_den ||
-            a.conv_k != b.conv_k || a.min_n != b.min_n)
-            return mig_set_error(MIG_E_INVALID_ARG,
-                                 "policies of one mig_simulate call must share ctx_mib, z, eps, conv_k, min_n");
+            a.conv_k != b.conv_k || a.min_n != b.min_n || ((a.flags ^ b.flags) & MIG_EWMA_REUSE))
+            return mig_set_error(MIG_E_INVALID_ARG, "policies of one mig_simulate call must share ctx_mib, z, eps, "
+                                                    "conv_k, min_n and the EWMA flag (one estimate per job)");
     }
     return MIG_OK;
 }

@@ -28,6 +28,7 @@ struct EstParams {
     unsigned long long* err;
     uint32_t ctx, eps_num, eps_den, conv_k, min_n;
     uint32_t dyn_only;  // skip writing STATIC/MODEL estimates (mig_simulate recomputes them while staging)
+    uint32_t ewma;      // MIG_EWMA_REUSE (R36): EWMA of the inverse reuse ratio instead of its linear trend
     double z;
 };
 
@@ -40,7 +41,7 @@ struct FitOut {
 // diagnostic a = 6K/D is computed once for the reported lane (estimate_dynamic). q_unit: the inverse reuse is
 // exactly 1.0 at every sample, so its forecast is exactly 65536 and V = 1 (the canonical sequence gives the same).
 __device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int64_t Syy, int64_t Sq, int64_t Stq,
-                                         int64_t T, double z, int64_t ws_ctx, bool q_unit) {
+                                         int64_t T, double z, int64_t ws_ctx, bool q_unit, bool ewma, int64_t L) {
     const int64_t n2m1 = n * n - 1;
     const int64_t D = n * n2m1;
     const int64_t Ky = 2 * Sty - (n + 1) * Sy;
@@ -55,7 +56,10 @@ __device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int
     double u = __dadd_rn(yT, __dmul_rn(z, f.sigma));
     if (u < 0.0) u = 0.0;
     double V = 1.0;
-    if (!q_unit) {
+    if (ewma) {  // R36: V = max(L_n / 65536, 1)
+        V = __dmul_rn(__ll2double_rn(L), 1.0 / 65536.0);
+        if (V < 1.0) V = 1.0;
+    } else if (!q_unit) {
         const int64_t Kq = 2 * Stq - (n + 1) * Sq;
         const __int128 numQ = (__int128)Sq * n2m1 + (__int128)3 * Kq * h;
         V = __dmul_rn(__ddiv_rn(i128_to_double(numQ), den), 1.0 / 65536.0);  // exact power-of-two scaling
@@ -100,7 +104,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     };
     const bool q_unit = q0 == 65536u && qs == 0;  // constant inverse reuse 1.0: phys = y + ws + ctx
     uint32_t lnext = 0;                          // lowest level whose first exceed is not yet known
-    int64_t Sy = 0, Sty = 0, Syy = 0, Sq = 0, Stq = 0, Plast = 0;
+    int64_t Sy = 0, Sty = 0, Syy = 0, Sq = 0, Stq = 0, Plast = 0, Lcarry = 0;
     uint32_t okprev = 0, conv = 0, pred = 0;
     double phi = 0.0, a = 0.0, sig = 0.0;
     bool done_pred = T < P.min_n;
@@ -134,9 +138,21 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         const int64_t syy = Syy + warp_scan_i64(yi * yi, lane);
         const int64_t sq = Sq + warp_scan_i64(qi, lane);
         const int64_t stq = Stq + warp_scan_i64(valid ? ni * qi : 0, lane);
+        // EWMA of the inverse reuse ratio (R36): L_1 = q_1, L_i = L_{i-1} + ((q_i - L_{i-1}) >> 3); a sequential
+        // recurrence, evaluated over the chunk's lanes in order (optional variant, never on the default path).
+        int64_t myL = 0;
+        if (P.ewma) {
+            int64_t L = Lcarry;
+            for (uint32_t k = 0; k < 32; ++k) {
+                const int64_t qk = (int64_t)__shfl_sync(FULL, q, k);
+                L = (base + k == 0) ? qk : L + ((qk - L) >> 3);
+                if (lane == k) myL = L;
+            }
+            Lcarry = L;
+        }
         const bool has = valid && n >= P.min_n;
         FitOut f = {0, 0.0, 0.0, 0.0};
-        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit);
+        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit, P.ewma != 0, myL);
         int64_t Pprev = __shfl_up_sync(FULL, f.P, 1);
         if (lane == 0) Pprev = Plast;
         const bool prev_has = n >= P.min_n + 1;
@@ -247,6 +263,7 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
     P.min_n = pol.min_n;
     P.z = pol.z;
     P.dyn_only = dyn_only ? 1u : 0u;
+    P.ewma = (pol.flags & MIG_EWMA_REUSE) ? 1u : 0u;
     const int threads = 256;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate, threads, 0);

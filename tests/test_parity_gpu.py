@@ -21,6 +21,7 @@ import paper_2508_18556_b200 as mig
 pytestmark = pytest.mark.gpu
 
 SPECS = [dict(kind=0), dict(kind=1), dict(kind=2), dict(kind=3), dict(kind=3, flags=1)]
+ESTIMATE_FIELDS = ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe", "phi", "a", "sigma"]
 
 
 def run_pair(geo, jobs, ext, off, specs, seed=0, common=None, max_jobs=None):
@@ -202,3 +203,20 @@ def test_full_size_sampled_parity(cfg, n_full, n_sample):
     # totals over the whole launch equal the sum of the per-trace results
     allres = mig.results_numpy(res, len(pols))
     check_totals(allres, mig.totals_numpy(tot))
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 300), (5, 200)])
+def test_ewma_variant_parity(cfg, n):
+    # MIG_EWMA_REUSE (R36, north_star only; parity unpinned by the paper): device == oracle bit for bit
+    jobs, ext, off = tg.generate_host(cfg, n)
+    specs = [dict(kind=3, flags=1 | 4), dict(kind=2, flags=1 | 4), dict(kind=0, flags=4)]
+    got, want, tot = run_pair(tg.CONFIG_GEOMETRY[cfg], jobs, ext, off, specs, seed=tg.seed_of(cfg))
+    assert_same(got, want)
+    geo = tg.CONFIG_GEOMETRY[cfg]
+    g = mig.mig_geometry_load(f"builtin:{geo}")
+    og = orc.Geometry(geom_path(geo))
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=tg.seed_of(cfg))
+    est = mig.estimates_numpy(mig.mig_estimate_memory(g, tr, mig.policy(g, flags=4)))
+    ref = orc.estimate(og, jobs, ext, off, orc.policy(flags=4), seed=tg.seed_of(cfg))
+    for f in ESTIMATE_FIELDS:
+        assert np.array_equal(est[f], ref[f]), f
