@@ -31,7 +31,7 @@ with open(os.path.join(ROOT, "BASELINE.json")) as _f:
     METRIC = json.load(_f)["metric"]
 
 POLICY_NAMES = {(0, 0): "BASELINE", (1, 0): "STATIC", (2, 0): "DYNAMIC", (3, 0): "FUSION_FISSION",
-                (3, 1): "FUSION_FISSION|EARLY_RESTART"}
+                (3, 1): "FUSION_FISSION|EARLY_RESTART", (4, 0): "SCHEME_A", (4, 1): "SCHEME_A|EARLY_RESTART"}
 WORKLOADS = {
     2: dict(desc="config2: 1M Monte-Carlo traces x 100 Rodinia-style jobs, A100-40GB, FUSION_FISSION (+BASELINE)",
             traces=1_000_000, policies=[(3, 0), (0, 0)]),
@@ -39,8 +39,8 @@ WORKLOADS = {
             traces=1_000_000, policies=[(3, 1), (3, 0), (0, 0)]),
     4: dict(desc="config4: 10M LLM KV-growth traces x 4 jobs, H100-80GB, FF+EARLY_RESTART (+FF, BASELINE)",
             traces=10_000_000, policies=[(3, 1), (3, 0), (0, 0)]),
-    5: dict(desc="config5 (per-GPU shard of 100M): 12.5M traces x 50 jobs, A100-40GB, 5-policy sweep",
-            traces=12_500_000, policies=[(0, 0), (1, 0), (2, 0), (3, 0), (3, 1)]),
+    5: dict(desc="config5 (per-GPU shard of 100M): 12.5M traces x 50 jobs, A100-40GB, 6-policy sweep",
+            traces=12_500_000, policies=[(0, 0), (1, 0), (2, 0), (3, 0), (3, 1), (4, 0)]),
 }
 
 # Algorithmic integer-op model of the hot path: lane-ops an ideal scalar implementation

@@ -73,6 +73,7 @@ typedef struct {
     uint32_t fcr_s0;       /* fcr(empty GPU) */
     uint32_t full_mem_mib; /* memory of the whole GPU */
     uint32_t n_layout;     /* instances of the static layout (policy MIG_STATIC) */
+    uint32_t scheme_a;     /* 1 if every memory level has a Scheme A layout (policy MIG_SCHEME_A usable) */
     uint32_t idle_w, w_per_slice; /* default power model (W idle; W per busy compute slice) */
 } mig_geometry_info;
 
@@ -131,7 +132,10 @@ enum {
     MIG_BASELINE = 0,      /* non-partitioned GPU, one job at a time, queue order       */
     MIG_STATIC = 1,        /* fixed slice layout, no reconfiguration                      */
     MIG_DYNAMIC = 2,       /* create a tight slice on demand (Alg. 2), destroy it at run end               */
-    MIG_FUSION_FISSION = 3 /* Scheme B: reuse idle tight slice, Alg. 2, merge/split idle slices, wait      */
+    MIG_FUSION_FISSION = 3, /* Scheme B: reuse idle tight slice, Alg. 2, merge/split idle slices, wait     */
+    MIG_SCHEME_A = 4        /* Scheme A schedule_by_group: size groups in ascending memory
+                               order, each on its homogeneous layout (geometry "scheme_a_layouts"), static
+                               round-robin division over the group's slices, reconfiguration when a group drains */
 };
 enum {
     MIG_EARLY_RESTART = 1, /* preempt when the converged forecast exceeds the slice   */

@@ -49,10 +49,12 @@ struct OrGeomDesc {
     uint32_t prof_compute[16], prof_len[16], prof_nstart[16], prof_start[16][8];
     uint32_t n_layout;
     uint32_t layout_prof[8], layout_start[8];
+    uint32_t n_alay[8];                      // Scheme A homogeneous layout per memory level (R38)
+    uint32_t alay_prof[8][8], alay_start[8][8];
 };
 
 struct OrPolicy {
-    uint32_t kind;   // 0 BASELINE, 1 STATIC, 2 DYNAMIC, 3 FUSION_FISSION
+    uint32_t kind;   // 0 BASELINE, 1 STATIC, 2 DYNAMIC, 3 FUSION_FISSION, 4 SCHEME_A
     uint32_t flags;  // 1 EARLY_RESTART, 2 WARP_FOLD, 4 EWMA_REUSE
     uint32_t ctx_mib, reconfig_ticks, idle_w, w_per_slice;
     double z;
@@ -74,10 +76,10 @@ struct OrResult {  // 80 B
 static_assert(sizeof(OrEstimate) == 48, "estimate layout");
 static_assert(sizeof(OrResult) == 80, "result layout");
 
-enum { BASELINE = 0, STATIC = 1, DYNAMIC = 2, FUSION_FISSION = 3 };
+enum { BASELINE = 0, STATIC = 1, DYNAMIC = 2, FUSION_FISSION = 3, SCHEME_A = 4 };
 enum { F_EARLY_RESTART = 1, F_WARP_FOLD = 2, F_EWMA = 4 };
 enum { K_REUSE = 1, K_ALLOC, K_RECONF, K_WAIT, K_REJECT, K_COMPLETE, K_OOM, K_PREEMPT, K_FAILED, K_PLACE_STATIC,
-       K_PLACE_BASELINE };
+       K_PLACE_BASELINE, K_LAYOUT, K_PLACE_GROUP };
 
 // ---------------------------------------------------------------------------------------------------------------
 // Geometry and Algorithm 1.
@@ -192,6 +194,19 @@ std::string build_geometry(Geometry& g) {
     g.fcr.assign(g.states.size(), 0);
     for (size_t s = 0; s < g.states.size(); ++s)
         for (uint32_t f = 0; f < g.n_finals; ++f) g.fcr[s] += reach[s][f];
+    // Scheme A layouts: valid states whose slices all have the level's memory
+    std::vector<uint32_t> mems;
+    for (uint32_t p = 0; p < d.n_prof; ++p)
+        if (std::find(mems.begin(), mems.end(), g.mem(p)) == mems.end()) mems.push_back(g.mem(p));
+    std::sort(mems.begin(), mems.end());
+    for (size_t l = 0; l < mems.size() && l < 8; ++l) {
+        std::vector<int> st;
+        for (uint32_t i = 0; i < d.n_alay[l]; ++i) {
+            int q = g.placement_id((int)d.alay_prof[l][i], (int)d.alay_start[l][i]);
+            if (q < 0 || !can_add(g, st, q) || g.mem((int)d.alay_prof[l][i]) != mems[l]) return "scheme A layout invalid";
+            st = with(st, q);
+        }
+    }
     // static layout must be a valid state
     std::vector<int> lay;
     for (uint32_t i = 0; i < d.n_layout; ++i) {
@@ -684,6 +699,13 @@ struct Sim {
         return false;
     }
 
+    void requeue(int jid) {
+        if (pol.kind == SCHEME_A)
+            a_enqueue(jid);  // the tail of its new (larger) group
+        else
+            queue.push_back(jid);
+    }
+
     void apply(const Event& ev) {
         int k = -1;
         for (size_t i = 0; i < inst.size(); ++i)
@@ -706,7 +728,7 @@ struct Sim {
             if (next_larger(cap, &nl)) {
                 j.req = nl;
                 r.restarts++;
-                queue.push_back((int)ev.job);  // return to the scheduling queue, at the tail (R13)
+                requeue((int)ev.job);  // return to the scheduling queue, at the tail (R13)
             } else {
                 record(t, ev.job, K_FAILED, in.start, in.prof, 0);
                 r.failed++;
@@ -716,7 +738,7 @@ struct Sim {
             r.preempts++;
             r.restarts++;
             j.req = std::min(j.e.pred_mib, g.full_mem());  // restart on the slice meeting the forecast (R25)
-            queue.push_back((int)ev.job);
+            requeue((int)ev.job);
         }
         in.busy = false;
         in.job = -1;
@@ -726,8 +748,116 @@ struct Sim {
         }
     }
 
+    // ---- Scheme A, schedule_by_group (Alg. PAPER.md:583-595; reading R38) ----
+    // Jobs are grouped by the memory of their tight-fit profile; groups run in ascending memory order on that
+    // group's homogeneous layout; job k of a group goes to slice (k mod #slices) (static round robin over slices
+    // in ascending start) and each slice runs its jobs in order. The GPU is reconfigured only when a
+    // group has drained. OOM'd / preempted jobs join the tail of their new (larger) group.
+    struct GroupState {
+        std::vector<std::vector<int>> lists;  // per level: job ids in group order
+        int cur = -1;
+        std::vector<size_t> next_idx;         // per slice of the current layout
+        std::vector<uint32_t> ready;          // per slice: earliest start (after creation)
+    };
+    GroupState gs;
+
+    int level_of_prof(int p) const {
+        std::vector<uint32_t> L = levels(g);
+        return (int)(std::find(L.begin(), L.end(), g.mem(p)) - L.begin());
+    }
+
+    void a_enqueue(int jid) {
+        Job& j = jobs[jid];
+        int need = tight_fit(g, j.req, j.warps, pol);
+        if (need < 0) {  // cannot happen after an OOM/preempt (the new requirement always fits the GPU)
+            record(t, jid, K_REJECT, 0xF, 0xF, 0);
+            r.rejected++;
+            return;
+        }
+        gs.lists[level_of_prof(need)].push_back(jid);
+    }
+
+    bool a_group_done() const {
+        for (const Instance& in : inst)
+            if (in.busy) return false;
+        for (size_t k = 0; k < gs.next_idx.size(); ++k)
+            if (gs.next_idx[k] < gs.lists[gs.cur].size()) return false;
+        return true;
+    }
+
+    void a_dispatch() {
+        for (size_t k = 0; k < inst.size(); ++k) {  // instances are kept in ascending start order
+            if (inst[k].busy || gs.next_idx[k] >= gs.lists[gs.cur].size()) continue;
+            int jid = gs.lists[gs.cur][gs.next_idx[k]];
+            gs.next_idx[k] += inst.size();
+            record(t, jid, K_PLACE_GROUP, inst[k].start, inst[k].prof, 0);
+            r.placements++;
+            uint32_t save = t;
+            bool created = t < gs.ready[k];  // first run on a freshly created slice waits for it
+            start_run(jid, (int)k, created);
+            t = save;
+        }
+    }
+
+    bool a_next_group() {
+        int nl = -1;
+        for (int l = gs.cur + 1; l < (int)gs.lists.size(); ++l)
+            if (!gs.lists[l].empty()) {
+                nl = l;
+                break;
+            }
+        if (nl < 0) return false;
+        uint32_t nd = (uint32_t)inst.size();
+        r.destroys += nd;
+        inst.clear();
+        gs.cur = nl;
+        std::vector<std::pair<int, int>> sl;
+        for (uint32_t i = 0; i < g.d.n_alay[nl]; ++i) sl.push_back({(int)g.d.alay_start[nl][i], (int)g.d.alay_prof[nl][i]});
+        std::sort(sl.begin(), sl.end());
+        for (auto& e : sl) inst.push_back({e.second, e.first, false, -1, 0});
+        r.creates += (uint32_t)inst.size();
+        check_invariants();
+        gs.next_idx.assign(inst.size(), 0);
+        for (size_t k = 0; k < inst.size(); ++k) gs.next_idx[k] = k;
+        gs.ready.assign(inst.size(), t + pol.reconfig_ticks);
+        record(t, 0xFFFF, K_LAYOUT, 0, (uint32_t)nl, nd);
+        return true;
+    }
+
+    void a_step() {  // after the events of tick t
+        if (gs.cur >= 0) a_dispatch();
+        while (gs.cur < 0 || a_group_done()) {
+            if (!a_next_group()) return;
+            a_dispatch();
+        }
+    }
+
+    void run_scheme_a() {
+        gs.lists.assign(levels(g).size(), {});
+        t = 0;
+        for (size_t i = 0; i < jobs.size(); ++i) a_enqueue((int)i);  // REJECTs at t = 0, in queue order
+        a_step();
+        while (!events.empty()) {
+            t = events.top().tick;
+            while (!events.empty() && events.top().tick == t) {
+                Event ev = events.top();
+                events.pop();
+                apply(ev);
+            }
+            r.makespan = t;
+            a_step();
+            check_invariants();
+            if (!err.empty()) return;
+        }
+        r.energy_wticks = (uint64_t)pol.idle_w * r.makespan + (uint64_t)pol.w_per_slice * r.busy_slice_ticks;
+    }
+
     void run() {
         r.n_jobs = (uint32_t)jobs.size();
+        if (pol.kind == SCHEME_A) {
+            run_scheme_a();
+            return;
+        }
         if (pol.kind == BASELINE) {
             inst.push_back({(int)g.d.n_prof - 1, 0, false, -1, 0});
         } else if (pol.kind == STATIC) {

@@ -15,11 +15,11 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
-BASELINE, STATIC, DYNAMIC, FUSION_FISSION = 0, 1, 2, 3
+BASELINE, STATIC, DYNAMIC, FUSION_FISSION, SCHEME_A = 0, 1, 2, 3, 4
 EARLY_RESTART, WARP_FOLD, EWMA_REUSE = 1, 2, 4
 
 KIND_NAMES = {1: "REUSE", 2: "ALLOC", 3: "RECONF", 4: "WAIT", 5: "REJECT", 6: "COMPLETE", 7: "OOM", 8: "PREEMPT",
-              9: "FAILED", 10: "PLACE_STATIC", 11: "PLACE_BASELINE"}
+              9: "FAILED", 10: "PLACE_STATIC", 11: "PLACE_BASELINE", 12: "LAYOUT", 13: "PLACE_GROUP"}
 
 RESULT_DTYPE = np.dtype([
     ("makespan", "<u4"), ("n_jobs", "<u4"), ("completed", "<u4"), ("rejected", "<u4"), ("failed", "<u4"),
@@ -37,7 +37,8 @@ class OrGeomDesc(C.Structure):
                 ("sms_per_slice", C.c_uint32), ("warps_per_sm", C.c_uint32), ("n_prof", C.c_uint32),
                 ("prof_compute", C.c_uint32 * 16), ("prof_len", C.c_uint32 * 16), ("prof_nstart", C.c_uint32 * 16),
                 ("prof_start", (C.c_uint32 * 8) * 16), ("n_layout", C.c_uint32), ("layout_prof", C.c_uint32 * 8),
-                ("layout_start", C.c_uint32 * 8)]
+                ("layout_start", C.c_uint32 * 8), ("n_alay", C.c_uint32 * 8), ("alay_prof", (C.c_uint32 * 8) * 8),
+                ("alay_start", (C.c_uint32 * 8) * 8)]
 
 
 class OrPolicy(C.Structure):
@@ -119,6 +120,13 @@ class Geometry:
         for i, (name, st) in enumerate(lay):
             d.layout_prof[i] = self.names.index(name)
             d.layout_start[i] = st
+        mems = sorted({p["memory_slots"] * spec["slot_mib"] for p in profs})
+        for entry in spec.get("scheme_a_layouts", []):
+            lvl = mems.index(entry["memory_mib"])
+            d.n_alay[lvl] = len(entry["slices"])
+            for i, (name, st) in enumerate(entry["slices"]):
+                d.alay_prof[lvl][i] = self.names.index(name)
+                d.alay_start[lvl][i] = st
         self.desc = d
         h = lib().or_geometry_new(C.byref(d))
         if not h:

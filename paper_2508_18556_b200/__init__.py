@@ -20,7 +20,7 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` (no CPU fallback exists)")
 _lib = C.CDLL(LIB_PATH)
 
-MIG_BASELINE, MIG_STATIC, MIG_DYNAMIC, MIG_FUSION_FISSION = 0, 1, 2, 3
+MIG_BASELINE, MIG_STATIC, MIG_DYNAMIC, MIG_FUSION_FISSION, MIG_SCHEME_A = 0, 1, 2, 3, 4
 MIG_EARLY_RESTART, MIG_WARP_FOLD, MIG_EWMA_REUSE = 1, 2, 4
 MIG_MAX_JOBS_PER_TRACE = 768
 MIG_NEVER = 0xFFFF
@@ -49,7 +49,7 @@ class MigError(RuntimeError):
 class mig_geometry_info(C.Structure):
     _fields_ = [("gpu_name", C.c_char * 64)] + [(n, C.c_uint32) for n in (
         "n_slots", "slot_mib", "n_compute", "n_profiles", "n_levels", "n_placements", "n_states", "n_finals",
-        "fcr_s0", "full_mem_mib", "n_layout", "idle_w", "w_per_slice")]
+        "fcr_s0", "full_mem_mib", "n_layout", "scheme_a", "idle_w", "w_per_slice")]
 
 
 class mig_traces(C.Structure):

@@ -85,7 +85,7 @@ mig_status check_traces(const mig_traces* tr) {
 }
 
 mig_status check_policy(const mig_policy& p) {
-    if (p.kind > MIG_FUSION_FISSION) return mig_set_error(MIG_E_INVALID_ARG, "policy.kind out of range");
+    if (p.kind > MIG_SCHEME_A) return mig_set_error(MIG_E_INVALID_ARG, "policy.kind out of range");
     if (p.flags & ~7u) return mig_set_error(MIG_E_INVALID_ARG, "unknown policy flag");
     if (p.min_n < 3) return mig_set_error(MIG_E_INVALID_ARG, "policy.min_n must be >= 3");
     if (p.conv_k < 1 || p.conv_k > 32) return mig_set_error(MIG_E_INVALID_ARG, "policy.conv_k must be 1..32");
@@ -102,6 +102,8 @@ mig_status check_policies(const mig_geometry* g, const mig_policy* pols, uint32_
         if (s != MIG_OK) return s;
         if (pols[i].kind == MIG_STATIC && g->dg.n_layout == 0)
             return mig_set_error(MIG_E_INVALID_ARG, "MIG_STATIC needs a geometry with a static_layout");
+        if (pols[i].kind == MIG_SCHEME_A && !g->info.scheme_a)
+            return mig_set_error(MIG_E_INVALID_ARG, "MIG_SCHEME_A needs scheme_a_layouts for every memory level");
         const mig_policy& a = pols[0];
         const mig_policy& b = pols[i];
         if (a.ctx_mib != b.ctx_mib || a.z != b.z || a.eps_num != b.eps_num || a.eps_den != b.eps_den ||

@@ -17,7 +17,7 @@ constexpr int kMaxPolicies = 8;
 // applied event in order, so oracle/GPU parity of the hash is parity of every placement and event time.
 enum : uint32_t {
     K_REUSE = 1, K_ALLOC = 2, K_RECONF = 3, K_WAIT = 4, K_REJECT = 5, K_COMPLETE = 6, K_OOM = 7, K_PREEMPT = 8,
-    K_FAILED = 9, K_PLACE_STATIC = 10, K_PLACE_BASELINE = 11
+    K_FAILED = 9, K_PLACE_STATIC = 10, K_PLACE_BASELINE = 11, K_LAYOUT = 12, K_PLACE_GROUP = 13
 };
 
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;

@@ -238,6 +238,46 @@ mig_status load_geometry(const std::string& text, mig_geometry* g) {
             d.n_layout++;
         }
     }
+    // Scheme A homogeneous layouts, one per memory level (R38; optional)
+    const mig::json::Value* al = root.get("scheme_a_layouts");
+    if (al && al->kind == mig::json::Value::Array) {
+        for (size_t i = 0; i < al->arr.size(); ++i) {
+            const mig::json::Value& e = al->arr[i];
+            std::string where = "scheme_a_layouts[" + std::to_string(i) + "]";
+            uint32_t mm;
+            if (!get_u32(e, "memory_mib", &mm, &err)) return mig_set_error(MIG_E_VALIDATION, where + ": " + err);
+            auto lit = std::find(L.begin(), L.end(), mm);
+            if (lit == L.end()) return mig_set_error(MIG_E_VALIDATION, where + ".memory_mib is not a profile memory");
+            const uint32_t lvl = (uint32_t)(lit - L.begin());
+            const mig::json::Value* sl = e.get("slices");
+            if (!sl || sl->kind != mig::json::Value::Array || sl->arr.empty() || sl->arr.size() > 8)
+                return mig_set_error(MIG_E_VALIDATION, where + ".slices must list 1..8 slices");
+            uint32_t occ = 0, comp = 0;
+            std::vector<std::pair<uint32_t, uint32_t>> v;
+            for (size_t k = 0; k < sl->arr.size(); ++k) {
+                const mig::json::Value& x = sl->arr[k];
+                std::string w2 = where + ".slices[" + std::to_string(k) + "]";
+                if (x.kind != mig::json::Value::Array || x.arr.size() != 2 || x.arr[0].kind != mig::json::Value::String ||
+                    x.arr[1].kind != mig::json::Value::Number)
+                    return mig_set_error(MIG_E_VALIDATION, w2 + " must be [profile_name, start]");
+                auto it = std::find(g->prof_names.begin(), g->prof_names.end(), x.arr[0].str);
+                if (it == g->prof_names.end()) return mig_set_error(MIG_E_VALIDATION, w2 + ": unknown profile");
+                const uint32_t p = (uint32_t)(it - g->prof_names.begin()), st = (uint32_t)x.arr[1].num;
+                bool legal = false;
+                for (uint32_t q = 0; q < d.n_place[p]; ++q) legal |= (d.place[p][q] & 0xFF) == st;
+                const uint32_t mask = d.lenmask[p] << st;
+                if (!legal || (mask & occ) || d.mem[p] != mm)
+                    return mig_set_error(MIG_E_VALIDATION, w2 + ": illegal or wrong-size slice");
+                occ |= mask;
+                comp += d.comp[p];
+                v.push_back({st, p});
+            }
+            if (comp > d.n_compute) return mig_set_error(MIG_E_VALIDATION, where + ": compute over-committed");
+            std::sort(v.begin(), v.end());
+            d.n_alay[lvl] = (uint32_t)v.size();
+            for (size_t k = 0; k < v.size(); ++k) d.alay[lvl][k] = v[k].first | (v[k].second << 8);
+        }
+    }
     mig_geometry_info& in = g->info;
     snprintf(in.gpu_name, sizeof(in.gpu_name), "%s", g->name.c_str());
     in.n_slots = d.n_slots;
@@ -251,6 +291,9 @@ mig_status load_geometry(const std::string& text, mig_geometry* g) {
     in.fcr_s0 = d.fcr[0];
     in.full_mem_mib = d.full_mem;
     in.n_layout = d.n_layout;
+    in.scheme_a = 1;
+    for (uint32_t l = 0; l < d.n_levels; ++l)
+        if (d.n_alay[l] == 0) in.scheme_a = 0;
     in.idle_w = idle_w;
     in.w_per_slice = wps;
     return MIG_OK;

@@ -32,6 +32,8 @@ struct DevGeom {
     uint32_t level_next[8];  // next larger memory after level l (0 = none, R14)
     uint32_t layout_prof[8], layout_start[8];
     uint32_t pinfo[16];      // packed: level | comp << 4 | lenmask << 8 | len << 16 | prof << 20
+    uint32_t n_alay[8];      // Scheme A: slices of the homogeneous layout of memory level l (0 = none)
+    uint32_t alay[8][8];     // start | prof << 8, ascending start
     uint16_t fcr[256];       // fcr by occupancy mask (0 = not a valid occupancy)
 };
 

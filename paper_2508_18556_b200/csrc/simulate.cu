@@ -39,6 +39,7 @@ struct SimParams {
     const unsigned long long* est_err;  // error word of k_estimate (merged into the totals)
     uint32_t max_jobs, n_pol, ctx;
     uint32_t ring_cap;  // = max_jobs
+    uint32_t scheme_a;  // some policy is MIG_SCHEME_A: per-trace group lists are staged
     mig_policy pol[kMaxPolicies];
 };
 
@@ -206,6 +207,185 @@ __device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n,
             rec(o.hl, o.hh, t, (j << 16) | (K_COMPLETE << 12) | ev_lo);
             o.turn += t;
         }
+    }
+    o.makespan = t;
+    return o;
+}
+
+// Scheme A, schedule_by_group (reading R38): jobs are grouped by the memory level of their tight
+// fit, groups run in ascending order on the level's homogeneous layout (geometry scheme_a_layouts), job k of a
+// group goes to slice k mod #slices (static round robin in ascending start) and each slice runs its jobs in order;
+// the GPU is reconfigured (LAYOUT record) only when a group has drained; OOM'd / preempted jobs join the tail of
+// their new group. GL[l * cap + i] = i-th job of group l; lane l holds that group's length.
+template <int GW, bool WIDE>
+__device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<GW>& g, uint32_t n,
+                                                   const JobStore<WIDE>& J, uint16_t* GL, uint32_t cap, bool er,
+                                                   bool fold, uint32_t reconfig, uint32_t full_mem) {
+    const uint32_t lane = g.gl;
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    TraceOut o;
+    o.K0 = o.K1 = o.K2 = o.K3 = 0;
+    o.turn = o.busy = 0;
+    o.hl = (uint32_t)kFnvOffset;
+    o.hh = (uint32_t)(kFnvOffset >> 32);
+    uint32_t t = 0, glen = 0;
+    // ---- t = 0: sorted_by_mig_group (REJECT records in queue order for jobs no profile holds) ----
+    for (uint32_t c = 0; c < n; c += GW) {
+        const uint32_t j = c + lane;
+        const uint32_t need = j < n ? J.need(j) : 0xFEu;
+        uint32_t rm = g.ballot(need == 0xFFu);
+        while (rm) {
+            const uint32_t k = (uint32_t)__ffs(rm) - 1u;
+            rm &= rm - 1u;
+            rec(o.hl, o.hh, t, ((c + k) << 16) | (K_REJECT << 12) | 0xFF0u);
+            o.K2 += 1u;
+        }
+        const uint32_t lv = need < 0xFEu ? G.level[need] : 0xFFu;
+        for (uint32_t l = 0; l < G.n_levels; ++l) {
+            const uint32_t m = g.ballot(lv == l);
+            if (!m) continue;
+            const uint32_t b = g.shfl(glen, l);
+            if (lv == l) GL[l * cap + b + __popc(m & ((1u << lane) - 1u))] = (uint16_t)j;
+            if (lane == l) glen += __popc(m);
+        }
+    }
+    g.sync();
+    uint32_t cur = kNone, ii = 0, iend = 0, ijk = 0, nxt = 0, SM = 0, BM = 0, ns = 0, ready = 0;
+
+    auto dispatch = [&]() {  // idle slices take their next job, ascending start
+        const uint32_t len = g.shfl(glen, cur);
+        uint32_t m = g.ballot((ii & kValid) && !(ii & kBusy) && nxt < len);
+        while (m) {
+            const uint32_t s = (uint32_t)__ffs(m) - 1u;
+            m &= m - 1u;
+            const uint32_t j = GL[cur * cap + g.shfl(nxt, s)];
+            const uint32_t si = g.shfl(ii, s);
+            rec(o.hl, o.hh, t, (j << 16) | (K_PLACE_GROUP << 12) | (s << 8) | (((si >> 20) & 0xFu) << 4));
+            o.K0 += 1u;
+            const uint32_t lev = si & 0xFu;
+            uint32_t T, ticks, fe, pred, conv;
+            J.run_info(G, j, lev, T, ticks, fe, pred, conv);
+            const uint32_t rs = t < ready ? t + reconfig : t;  // first run on a freshly created slice
+            const uint32_t cap_m = G.level_mem[lev];
+            uint32_t i_pre = 0xFFFFFFFFu;
+            if (er && conv > 0 && pred > cap_m && cap_m < full_mem) i_pre = conv;
+            uint32_t end, ek;
+            if (fe <= min(T, i_pre)) {
+                ek = 1;
+                end = rs + fe * ticks;
+            } else if (i_pre < T) {
+                ek = 2;
+                end = rs + i_pre * ticks;
+            } else {
+                ek = 0;
+                end = rs + T * ticks;
+            }
+            if (lane == s) {
+                ii |= kBusy;
+                iend = end;
+                ijk = j | (ek << 16);
+                nxt += ns;
+            }
+            BM |= ((si >> 8) & 0xFFu) << s;
+            o.busy += (uint64_t)((si >> 4) & 0xFu) * (end - rs);
+        }
+    };
+    auto next_group = [&]() -> bool {  // set_homogeneous_slices(next non-empty group)
+        const uint32_t m = g.ballot(lane < G.n_levels && (cur == kNone || lane > cur) && glen > 0);
+        if (!m) return false;
+        const uint32_t l = (uint32_t)__ffs(m) - 1u;
+        const uint32_t nd = __popc(SM);
+        rec(o.hl, o.hh, t, (0xFFFFu << 16) | (K_LAYOUT << 12) | (l << 4) | nd);
+        o.K1 += nd;
+        ii = 0;
+        SM = 0;
+        ns = G.n_alay[l];
+        for (uint32_t k = 0; k < ns; ++k) {
+            const uint32_t e = G.alay[l][k], st = e & 0xFFu;
+            if (lane == st) {
+                ii = kValid | G.pinfo[e >> 8];
+                nxt = k;
+            }
+            SM |= 1u << st;
+        }
+        o.K0 += ns << 16;
+        ready = t + reconfig;
+        cur = l;
+        return true;
+    };
+    auto step = [&]() {
+        if (cur != kNone) dispatch();
+        for (;;) {
+            if (cur != kNone) {
+                const uint32_t len = g.shfl(glen, cur);
+                if (BM || g.ballot((ii & kValid) && nxt < len)) break;  // the group has not drained
+            }
+            if (!next_group()) break;
+            dispatch();
+        }
+    };
+
+    step();
+    for (;;) {
+        const uint32_t mine = (ii & kBusy) ? iend : 0xFFFFFFFFu;
+        const uint32_t tn = g.min(mine);
+        if (tn == 0xFFFFFFFFu) break;
+        t = tn;
+        uint32_t evm = g.ballot(mine == t);
+        do {
+            uint32_t s;
+            if ((evm & (evm - 1u)) == 0u) {
+                s = (uint32_t)__ffs(evm) - 1u;
+            } else {  // COMPLETE < OOM < PREEMPT, then job id (R28)
+                const uint32_t key = ((evm >> lane) & 1u) ? ijk : 0xFFFFFFFFu;
+                const uint32_t km = g.min(key);
+                s = (uint32_t)__ffs(g.ballot(key == km)) - 1u;
+            }
+            evm &= ~(1u << s);
+            const uint32_t si = g.shfl(ii, s);
+            const uint32_t sjk = g.shfl(ijk, s);
+            const uint32_t job = sjk & 0xFFFFu, ek = sjk >> 16;
+            const uint32_t lo = (job << 16) | (s << 8) | (((si >> 20) & 0xFu) << 4);
+            uint32_t req = 0;
+            if (ek == 0) {
+                rec(o.hl, o.hh, t, lo | (K_COMPLETE << 12));
+                o.turn += t;
+            } else if (ek == 1) {
+                rec(o.hl, o.hh, t, lo | (K_OOM << 12));
+                const uint32_t nl = G.level_next[si & 0xFu];
+                o.K2 += 1u << 16;
+                if (nl == 0) {
+                    rec(o.hl, o.hh, t, lo | (K_FAILED << 12));
+                    o.K3 += 1u << 16;
+                } else {
+                    req = nl;
+                }
+            } else {
+                rec(o.hl, o.hh, t, lo | (K_PREEMPT << 12));
+                o.K3 += 1u;
+                req = min(J.pred(job), full_mem);
+            }
+            if (req) {  // the tail of the job's new (larger) group
+                const uint32_t need = tight_fit_lane(G, req, J.warps(job), fold);
+                if (need == 0xFFu) {
+                    rec(o.hl, o.hh, t, (job << 16) | (K_REJECT << 12) | 0xFF0u);
+                    o.K2 += 1u;
+                } else {
+                    const uint32_t lv = G.level[need];
+                    const uint32_t b = g.shfl(glen, lv);
+                    g.sync();
+                    if (lane == 0) {
+                        J.set_need(job, need);
+                        GL[lv * cap + b] = (uint16_t)job;
+                    }
+                    g.sync();
+                    if (lane == lv) ++glen;
+                }
+            }
+            BM &= ~(((si >> 8) & 0xFFu) << s);
+            if (lane == s) ii &= ~kBusy;
+        } while (evm);
+        step();
     }
     o.makespan = t;
     return o;
@@ -467,8 +647,11 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
     unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(smem + kGeomBytes + kPolBytes);
     const Grp<GW> g(threadIdx.x & 31u);
     const uint32_t lane = g.gl, group = threadIdx.x / GW;
-    const uint32_t per_group = WIDE ? P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u) : P.max_jobs * 16u;
+    const uint32_t gl_bytes = P.scheme_a ? ((kMaxLevels * P.max_jobs * 2u + 15u) & ~15u) : 0u;
+    const uint32_t per_group =
+        (WIDE ? P.max_jobs * 32u + ((P.max_jobs * 2u + 15u) & ~15u) : P.max_jobs * 16u) + gl_bytes;
     uint8_t* wb = smem + kGeomBytes + kPolBytes + kTotBytes + group * per_group;
+    uint16_t* GL = reinterpret_cast<uint16_t*>(wb + per_group - gl_bytes);  // Scheme A group lists
     uint4* jobA = reinterpret_cast<uint4*>(wb);
     uint4* jobB = WIDE ? jobA + P.max_jobs : nullptr;
     uint16_t* ring = WIDE ? reinterpret_cast<uint16_t*>(jobA + P.max_jobs * 2u) : nullptr;  // requeue FIFO (WIDE)
@@ -567,7 +750,9 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
             g.sync();
             const JobStore<WIDE> J{jobA, jobB, P.jobs + j0, P.ext ? P.ext + j0 : nullptr, P.est + j0, P.ctx};
             TraceOut o;
-            if (kind == MIG_FUSION_FISSION)
+            if (kind == MIG_SCHEME_A)
+                o = scheme_a_trace<GW, WIDE>(G, g, n, J, GL, P.max_jobs, er, fold, pol.reconfig_ticks, full_mem);
+            else if (kind == MIG_FUSION_FISSION)
                 o = simulate_trace<MIG_FUSION_FISSION, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
                                                            pol.reconfig_ticks, full_mem);
             else if (kind == MIG_DYNAMIC)
@@ -641,8 +826,9 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
 
 constexpr int warps_per_cta(bool wide) { return wide ? 4 : 8; }
 
-size_t simulate_smem_bytes(uint32_t max_jobs, int gw, bool wide) {
-    const size_t per_group = wide ? (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u) : (size_t)max_jobs * 16u;
+size_t simulate_smem_bytes(uint32_t max_jobs, int gw, bool wide, bool scheme_a) {
+    const size_t per_group = (wide ? (size_t)max_jobs * 32u + ((max_jobs * 2u + 15u) & ~15u) : (size_t)max_jobs * 16u) +
+                             (scheme_a ? ((kMaxLevels * max_jobs * 2u + 15u) & ~15u) : 0u);
     return kGeomBytes + kPolBytes + kTotBytes + (size_t)(warps_per_cta(wide) * 32 / gw) * per_group;
 }
 
@@ -650,7 +836,7 @@ template <int GW, bool WIDE>
 static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n_traces, int sm_count,
                              cudaStream_t stream) {
     constexpr int kW = warps_per_cta(WIDE);
-    const size_t smem = simulate_smem_bytes(P.max_jobs, GW, WIDE);
+    const size_t smem = simulate_smem_bytes(P.max_jobs, GW, WIDE, P.scheme_a != 0);
     cudaError_t e = cudaFuncSetAttribute(k_simulate<GW, WIDE, kW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -668,14 +854,14 @@ static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n
 
 // Lanes per trace: 8 (four traces per warp) unless MIG_LANES_PER_TRACE=32 (one trace per warp) or the staged
 // traces would not fit shared memory four to a warp.
-int simulate_group_width(uint32_t max_jobs) {
+int simulate_group_width(uint32_t max_jobs, bool scheme_a) {
     static int forced = -1;
     if (forced < 0) {
         const char* env = getenv("MIG_LANES_PER_TRACE");
         forced = env ? atoi(env) : 0;
     }
     if (forced == 32 || forced == 8) return forced;
-    return simulate_smem_bytes(max_jobs, 8, false) <= 200 * 1024 ? 8 : 32;
+    return simulate_smem_bytes(max_jobs, 8, false, scheme_a) <= 200 * 1024 ? 8 : 32;
 }
 
 // Staging layout: 32 B/job for short traces (everything on chip), 16 B/job for long ones (occupancy).
@@ -708,9 +894,12 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     P.ring_cap = tr.max_jobs;
     P.n_pol = n_pol;
     P.ctx = pols[0].ctx_mib;
-    for (uint32_t i = 0; i < n_pol; ++i) P.pol[i] = pols[i];
+    for (uint32_t i = 0; i < n_pol; ++i) {
+        P.pol[i] = pols[i];
+        if (pols[i].kind == MIG_SCHEME_A) P.scheme_a = 1;
+    }
     const bool wide = simulate_wide_layout(tr.max_jobs);
-    if (simulate_group_width(tr.max_jobs) == 8)
+    if (simulate_group_width(tr.max_jobs, P.scheme_a != 0) == 8)
         return wide ? launch_gw<8, true>(Gdev, P, tr.n_traces, sm_count, stream)
                     : launch_gw<8, false>(Gdev, P, tr.n_traces, sm_count, stream);
     return wide ? launch_gw<32, true>(Gdev, P, tr.n_traces, sm_count, stream)

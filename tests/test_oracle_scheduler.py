@@ -17,7 +17,7 @@ from conftest import GOLDEN_DIR, geom_path
 from oracle import oracle as orc
 from tracegen import tracegen as tg
 
-POLICY = {"BASELINE": 0, "STATIC": 1, "DYNAMIC": 2, "FUSION_FISSION": 3}
+POLICY = {"BASELINE": 0, "STATIC": 1, "DYNAMIC": 2, "FUSION_FISSION": 3, "SCHEME_A": 4}
 
 
 def spec_of(name):
@@ -42,7 +42,9 @@ def test_example_w(pname):
         if isinstance(v, int):
             assert int(r[k]) == v, (pname, k)
     dec = int(r["placements"]) + int(r["waits"]) + int(r["rejected"])
-    assert dec == 15  # 15 decisions under every policy
+    assert dec == (9 if pname == "SCHEME_A" else 15)  # 15 head evaluations under Scheme B policies
+    if pname == "SCHEME_A":
+        assert [d["tick"] for d in recs if d["kind"] == "LAYOUT"] == [0, 80, 220]  # 3 layouts
     if pname == "FUSION_FISSION":
         got = [(d["tick"], d["job"], d["kind"], d["start"]) for d in recs if d["kind"] not in ("COMPLETE",)]
         assert got[:4] == [(0, 0, "ALLOC", 2), (0, 1, "ALLOC", 1), (0, 2, "ALLOC", 0), (0, 3, "WAIT", 15)]
@@ -59,9 +61,11 @@ def test_throughput_ceilings():
         kw = dict(ctx_mib=512, reconfig_ticks=0)
         ff = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, **kw))[0, 0]
         dyn = orc.simulate(g, jobs, ext, off, orc.policy(kind=2, **kw))[0, 0]
+        sa = orc.simulate(g, jobs, ext, off, orc.policy(kind=4, **kw))[0, 0]
         base = orc.simulate(g, jobs, ext, off, orc.policy(kind=0, **kw))[0, 0]
         assert base["makespan"] / ff["makespan"] == pytest.approx(float(n), abs=0.01)
         assert base["makespan"] / dyn["makespan"] == pytest.approx(float(n), abs=0.01)
+        assert base["makespan"] / sa["makespan"] == pytest.approx(float(n), abs=0.01)  # SPEC.md:481 (Scheme A)
 
 
 def test_energy_closed_form():
@@ -207,3 +211,43 @@ def test_bruteforce_replay_tiny_queues(geo, cfg):
                     rp.step(d)
                 visited |= set(rp.visited)
     assert visited <= set(S)
+
+
+def test_scheme_a_reconfigurations_equal_groups():
+    # on an OOM-free mix Scheme A reconfigures once per size group present
+    g = orc.Geometry(geom_path("a100-40gb"))
+    rng = np.random.default_rng(4)
+    for _ in range(30):
+        sizes = rng.choice([3000, 8000, 15000, 30000], size=int(rng.integers(1, 25)))
+        tr = [tg.pack_job(int(m), int(m), 1, 0, int(rng.integers(10, 500))) for m in sizes]
+        jobs, ext, off = tg.pack_traces([tr])
+        r, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=4), records=True)
+        groups = len({int(g.tight_fit(int(m) + 512)) if g.mem[g.tight_fit(int(m) + 512)] != 20480 else 2
+                      for m in sizes})
+        assert sum(d["kind"] == "LAYOUT" for d in recs) == groups
+        assert r[0, 0]["ooms"] == 0 and r[0, 0]["completed"] == len(sizes)
+
+
+def test_scheme_a_vs_b_directions():
+    # Scheme A >= Scheme B on heterogeneous Ht1-style mixes (B waits head-of-line);
+    # the Ml3 corner case (only large jobs, two 20 GB halves, static division) favours Scheme B.
+    g = orc.Geometry(geom_path("a100-40gb"))
+    rng = np.random.default_rng(9)
+    wins = 0
+    for _ in range(40):
+        kinds = ["s"] * 11 + ["m"] * 2 + ["f"] * 2  # Ht1: 11 small, 2 medium, 2 full-GPU jobs
+        rng.shuffle(kinds)
+        mem = {"s": 3000, "m": 8000, "f": 30000}
+        dur = {"s": 700, "m": 1100, "f": 2000}  # equal total time per group
+        tr = [tg.pack_job(mem[k], mem[k], 1, 0, dur[k]) for k in kinds]
+        jobs, ext, off = tg.pack_traces([tr])
+        a, b = orc.simulate(g, jobs, ext, off, [orc.policy(kind=4), orc.policy(kind=3)])[0]
+        wins += a["makespan"] <= b["makespan"]
+    assert wins >= 36
+    worse = 0
+    for _ in range(40):  # Ml3: 18 large jobs with unequal durations
+        tr = [tg.pack_job(15000, 15000, 1, 0, int(d)) for d in rng.integers(100, 2000, 18)]
+        jobs, ext, off = tg.pack_traces([tr])
+        a, b = orc.simulate(g, jobs, ext, off, [orc.policy(kind=4), orc.policy(kind=3)])[0]
+        worse += b["makespan"] <= a["makespan"]
+    assert worse >= 36

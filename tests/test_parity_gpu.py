@@ -20,7 +20,8 @@ import paper_2508_18556_b200 as mig
 
 pytestmark = pytest.mark.gpu
 
-SPECS = [dict(kind=0), dict(kind=1), dict(kind=2), dict(kind=3), dict(kind=3, flags=1)]
+SPECS = [dict(kind=0), dict(kind=1), dict(kind=2), dict(kind=3), dict(kind=3, flags=1), dict(kind=4),
+         dict(kind=4, flags=1)]
 ESTIMATE_FIELDS = ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe", "phi", "a", "sigma"]
 
 
@@ -64,8 +65,9 @@ def test_config1_example_w_all_policies():
         fx = json.load(f)
     tr = [tg.pack_job(j["est_gb"] * 1024, j["true_gb"] * 1024, j["iters"], 0, j["iter_ticks"]) for j in fx["jobs_gb"]]
     jobs, ext, off = tg.pack_traces([tr])
-    specs = [dict(kind=k) for k in range(4)]
+    specs = [dict(kind=k) for k in range(5)]
     got, want, tot = run_pair("a30-24gb", jobs, ext, off, specs, common=fx["policy_common"])
+    assert got[0, 4]["makespan"] == 270 and got[0, 4]["energy_wticks"] == 28600  # Scheme A
     assert_same(got, want)
     assert got[0, 3]["makespan"] == 220 and got[0, 3]["energy_wticks"] == 27100
     check_totals(got, tot)
@@ -126,7 +128,7 @@ def test_random_ragged_traces_edge_cases(geo):
     spec = json.load(open(geom_path(geo)))
     rng = np.random.default_rng(5)
     jobs, ext, off = random_tiny_traces(rng, spec, 500, 40)
-    specs = SPECS + [dict(kind=3, flags=2), dict(kind=3, flags=3), dict(kind=1, flags=3)]
+    specs = SPECS + [dict(kind=3, flags=3)]
     for common in [dict(ctx_mib=0, reconfig_ticks=0), dict(ctx_mib=512, reconfig_ticks=500, z=1.0)]:
         got, want, tot = run_pair(geo, jobs, ext, off, specs, seed=99, common=common)
         assert_same(got, want)
