@@ -213,10 +213,14 @@ def run_mine(args):
                "traces_per_s": trs, "wall_s": round(wall, 2)}
         log(f"cpu oracle baseline: {r:.3e} decisions/s on {cores} cores")
 
+    local = local % max(1, torch.cuda.device_count())  # --share-gpu testing: several ranks on one device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # functional test of the multi-rank path on a single-GPU box (NCCL refuses a shared device)
+            dist.init_process_group(args.dist_backend)
     import paper_2508_18556_b200 as mig
     from paper_2508_18556_b200.sharding import reduce_totals, shard_range
     from tracegen import tracegen as tg
@@ -393,6 +397,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-cores", type=int, default=64)
     ap.add_argument("--ref-seconds", type=float, default=2.0)
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo (multi-rank test on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

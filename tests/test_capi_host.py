@@ -14,7 +14,7 @@ from oracle import oracle as orc
 
 import paper_2508_18556_b200 as mig
 
-GEOMS = ["a30-24gb", "a100-40gb", "a100-40gb-1g10", "a100-80gb", "h100-80gb"]
+GEOMS = ["a30-24gb", "a100-40gb", "a100-40gb-1g10", "a100-80gb", "h100-80gb", "b200-180gb"]
 
 
 def test_exports_every_declared_symbol():

@@ -74,7 +74,8 @@ def brute_tables(spec):
 
 
 @pytest.mark.parametrize("name,nS,nF", [("a30-24gb", 26, 5), ("a100-40gb", 298, 19), ("a100-80gb", 298, 19),
-                                         ("h100-80gb", 298, 19), ("a100-40gb-1g10", 723, 78)])
+                                         ("h100-80gb", 298, 19), ("a100-40gb-1g10", 723, 78),
+                                         ("b200-180gb", 723, 78)])
 def test_state_counts_match_bruteforce(name, nS, nF):
     spec = load(name)
     g = orc.Geometry(spec)

@@ -122,7 +122,7 @@ def random_tiny_traces(rng, geo_spec, n_traces, max_len, dyn_frac=0.3):
     return tg.pack_traces(traces)
 
 
-@pytest.mark.parametrize("geo", ["a30-24gb", "a100-40gb", "a100-40gb-1g10", "h100-80gb"])
+@pytest.mark.parametrize("geo", ["a30-24gb", "a100-40gb", "a100-40gb-1g10", "h100-80gb", "b200-180gb"])
 def test_random_ragged_traces_edge_cases(geo):
     # empty traces, ragged lengths, zero-iteration jobs, rejections, failures at the full GPU, warp folding
     spec = json.load(open(geom_path(geo)))
