@@ -306,7 +306,9 @@ def run_mine(args):
         if ext is not None:
             he = torch.empty((tr.n_jobs, 4), dtype=torch.int32, pin_memory=True)
             he.copy_(ext)
-        ho = off.cpu().numpy().view("u8")
+        hoff = torch.empty(off.shape, dtype=torch.int64, pin_memory=True)
+        hoff.copy_(off)
+        ho = hoff.numpy().view("u8")
         hres = torch.empty((n_per * n_pol, 80), dtype=torch.uint8, pin_memory=True)
         hjn = hj.numpy().view("u4")
         hen = None if he is None else he.numpy().view("u4")

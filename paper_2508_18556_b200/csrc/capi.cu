@@ -242,13 +242,16 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };  // every sub-buffer 256 B aligned
     const size_t jb = al(chunk_jobs_cap * 16), eb = T.jobs_ext ? al(chunk_jobs_cap * 16) : 0,
                  ob = al((chunk_traces + 1) * 8), esb = al(chunk_jobs_cap * sizeof(mig_job_estimate)),
-                 rb = al(chunk_traces * n_policies * sizeof(mig_trace_result)),
-                 tb = al(n_policies * sizeof(mig_policy_totals));
-    const size_t per = jb + eb + ob + esb + rb + tb + 64;
+                 rb = al(chunk_traces * n_policies * sizeof(mig_trace_result));
+    const size_t per = jb + eb + ob + esb + rb + 64;
     cudaStream_t ss[2];
     uint8_t* buf[2] = {nullptr, nullptr};
     std::vector<mig_policy_totals> host_tot(n_chunks * n_policies);
-    cudaError_t e = cudaSuccess;
+    // per-chunk totals stay on the device until the end (a D2H into pageable memory per chunk would block the
+    // host thread and serialise the copy/compute pipeline)
+    mig_policy_totals* d_tot_all = nullptr;
+    cudaError_t e = cudaMalloc(&d_tot_all, n_chunks * n_policies * sizeof(mig_policy_totals));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(totals)");
     for (int k = 0; k < 2; ++k) {
         if ((e = cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(e, "cudaStreamCreate");
@@ -270,8 +273,8 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         uint64_t* d_off = reinterpret_cast<uint64_t*>(b + jb + eb);
         mig_job_estimate* d_est = reinterpret_cast<mig_job_estimate*>(b + jb + eb + ob);
         mig_trace_result* d_out = reinterpret_cast<mig_trace_result*>(b + jb + eb + ob + esb);
-        mig_policy_totals* d_tot = reinterpret_cast<mig_policy_totals*>(b + jb + eb + ob + esb + rb);
-        unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(b + jb + eb + ob + esb + rb + tb);
+        mig_policy_totals* d_tot = d_tot_all + c * n_policies;
+        unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(b + jb + eb + ob + esb + rb);
         e = cudaMemcpyAsync(d_jobs, (const uint8_t*)T.jobs + jlo * 16, nj * 16, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess && T.jobs_ext)
             e = cudaMemcpyAsync(d_ext, (const uint8_t*)T.jobs_ext + jlo * 16, nj * 16, cudaMemcpyHostToDevice, s);
@@ -295,9 +298,6 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         if (out)
             e = cudaMemcpyAsync(out + t0 * n_policies, d_out, nt * n_policies * sizeof(mig_trace_result),
                                 cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(host_tot.data() + c * n_policies, d_tot, n_policies * sizeof(mig_policy_totals),
-                                cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) st = cuda_fail(e, "host pipeline D2H");
     }
     for (int k = 0; k < 2; ++k) {
@@ -306,6 +306,12 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         if (e != cudaSuccess && st == MIG_OK) st = cuda_fail(e, "host pipeline");
         cudaStreamDestroy(ss[k]);
     }
+    if (st == MIG_OK) {
+        e = cudaMemcpy(host_tot.data(), d_tot_all, n_chunks * n_policies * sizeof(mig_policy_totals),
+                       cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) st = cuda_fail(e, "host pipeline totals D2H");
+    }
+    cudaFree(d_tot_all);
     if (st != MIG_OK) return st;
     if (totals) {
         for (uint64_t c = 0; c < n_chunks; ++c)
