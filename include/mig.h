@@ -140,7 +140,9 @@ enum {
 enum {
     MIG_EARLY_RESTART = 1, /* preempt when the converged forecast exceeds the slice   */
     MIG_WARP_FOLD = 2,     /* tight fit keeps the full-GPU wave count                        */
-    MIG_EWMA_REUSE = 4     /* EWMA of the inverse reuse ratio instead of its trend (north_star; not in paper) */
+    MIG_EWMA_REUSE = 4,    /* EWMA of the inverse reuse ratio instead of its trend (north_star; not in paper) */
+    MIG_WAVE_TIME = 8      /* iter_ticks are full-GPU times; on profile p an iteration of a job with W warps takes
+                              ceil(ticks * waves(W,p) / waves(W,full)) ticks (R31 variant)  */
 };
 
 typedef struct {

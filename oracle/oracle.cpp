@@ -55,7 +55,7 @@ struct OrGeomDesc {
 
 struct OrPolicy {
     uint32_t kind;   // 0 BASELINE, 1 STATIC, 2 DYNAMIC, 3 FUSION_FISSION, 4 SCHEME_A
-    uint32_t flags;  // 1 EARLY_RESTART, 2 WARP_FOLD, 4 EWMA_REUSE
+    uint32_t flags;  // 1 EARLY_RESTART, 2 WARP_FOLD, 4 EWMA_REUSE, 8 WAVE_TIME
     uint32_t ctx_mib, reconfig_ticks, idle_w, w_per_slice;
     double z;
     uint32_t eps_num, eps_den, conv_k, min_n;
@@ -77,7 +77,7 @@ static_assert(sizeof(OrEstimate) == 48, "estimate layout");
 static_assert(sizeof(OrResult) == 80, "result layout");
 
 enum { BASELINE = 0, STATIC = 1, DYNAMIC = 2, FUSION_FISSION = 3, SCHEME_A = 4 };
-enum { F_EARLY_RESTART = 1, F_WARP_FOLD = 2, F_EWMA = 4 };
+enum { F_EARLY_RESTART = 1, F_WARP_FOLD = 2, F_EWMA = 4, F_WAVE_TIME = 8 };
 enum { K_REUSE = 1, K_ALLOC, K_RECONF, K_WAIT, K_REJECT, K_COMPLETE, K_OOM, K_PREEMPT, K_FAILED, K_PLACE_STATIC,
        K_PLACE_BASELINE, K_LAYOUT, K_PLACE_GROUP };
 
@@ -523,6 +523,16 @@ struct Sim {
         in.run_start = s;
         uint32_t cap = pol.kind == BASELINE ? g.full_mem() : g.mem(in.prof);
         uint32_t T = j.iters;
+        // Iteration time on the slice (R31 variant, flag WAVE_TIME): iter_ticks are full-GPU times; a job of W warps
+        // needs waves(W, p) = ceil(W / (sms_per_slice * compute(p) * warps_per_sm)) waves, so an
+        // iteration takes ceil(ticks * waves(W, p) / waves(W, full)) ticks on profile p.
+        uint32_t ticks = j.ticks;
+        if ((pol.flags & F_WAVE_TIME) && j.warps > 0) {
+            uint64_t cp = (uint64_t)g.d.sms_per_slice * g.d.prof_compute[in.prof] * g.d.warps_per_sm;
+            uint64_t cf = (uint64_t)g.d.sms_per_slice * g.d.prof_compute[g.d.n_prof - 1] * g.d.warps_per_sm;
+            uint64_t wp = (j.warps + cp - 1) / cp, wf = (j.warps + cf - 1) / cf;
+            ticks = (uint32_t)(((uint64_t)j.ticks * wp + wf - 1) / wf);
+        }
         // OOM at the end of the first iteration whose physical memory exceeds the slice (R12).
         uint32_t i_oom = first_exceed(j, cap, pol);
         // Early restart (R25): converged forecast above the slice, and a larger slice exists.
@@ -536,13 +546,13 @@ struct Sim {
         // Same-iteration precedence OOM > COMPLETE > PREEMPT (R29).
         if (i_oom != NEVER && i_oom <= std::min(T, i_pre)) {
             ev.kind_order = 1;
-            end = s + i_oom * j.ticks;
+            end = s + i_oom * ticks;
         } else if (i_pre < T) {
             ev.kind_order = 2;
-            end = s + i_pre * j.ticks;
+            end = s + i_pre * ticks;
         } else {
             ev.kind_order = 0;
-            end = s + T * j.ticks;
+            end = s + T * ticks;
         }
         ev.tick = end;
         uint32_t comp = pol.kind == BASELINE ? g.d.n_compute : g.d.prof_compute[in.prof];

@@ -83,6 +83,15 @@ __device__ __forceinline__ uint32_t tight_fit_lane(const DevGeom& G, uint32_t re
     return 0xFFu;
 }
 
+// Iteration time on profile p (flag MIG_WAVE_TIME, R31 variant): ticks are full-GPU times; a job of W warps runs
+// waves(W, p) = ceil(W / wave_cap[p]) waves, so one iteration takes ceil(ticks * wp / wf) ticks.
+__device__ __forceinline__ uint32_t wave_ticks(const DevGeom& G, uint32_t ticks, uint32_t warps, uint32_t prof) {
+    if (warps == 0) return ticks;
+    const uint32_t cp = G.wave_cap[prof], cf = G.wave_cap[G.full_prof];
+    const uint32_t wp = (warps + cp - 1) / cp, wf = (warps + cf - 1) / cf;
+    return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
+}
+
 // FNV-1a-64 step h = (h ^ (tick << 32 | lo)) * (2^40 + 0x1b3) mod 2^64, on the two 32-bit halves of h.
 __device__ __forceinline__ void rec(uint32_t& hl, uint32_t& hh, uint32_t tick, uint32_t lo) {
     const uint32_t x = hl ^ lo, y = hh ^ tick;
@@ -220,7 +229,7 @@ __device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n,
 template <int GW, bool WIDE>
 __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<GW>& g, uint32_t n,
                                                    const JobStore<WIDE>& J, uint16_t* GL, uint32_t cap, bool er,
-                                                   bool fold, uint32_t reconfig, uint32_t full_mem) {
+                                                   bool fold, bool wave, uint32_t reconfig, uint32_t full_mem) {
     const uint32_t lane = g.gl;
     constexpr uint32_t kNone = 0xFFFFFFFFu;
     TraceOut o;
@@ -265,6 +274,7 @@ __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<G
             const uint32_t lev = si & 0xFu;
             uint32_t T, ticks, fe, pred, conv;
             J.run_info(G, j, lev, T, ticks, fe, pred, conv);
+            if (wave) ticks = wave_ticks(G, ticks, J.warps(j), (si >> 20) & 0xFu);
             const uint32_t rs = t < ready ? t + reconfig : t;  // first run on a freshly created slice
             const uint32_t cap_m = G.level_mem[lev];
             uint32_t i_pre = 0xFFFFFFFFu;
@@ -395,7 +405,8 @@ __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<G
 template <int KIND, int GW, bool WIDE>
 __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<GW>& g, uint32_t n,
                                                    const JobStore<WIDE>& J, uint16_t* ring, uint32_t ring_cap,
-                                                   bool er, bool fold, uint32_t reconfig, uint32_t full_mem) {
+                                                   bool er, bool fold, bool wave, uint32_t reconfig,
+                                                   uint32_t full_mem) {
     const uint32_t lane = g.gl;
     if constexpr (KIND == MIG_BASELINE) {
         return baseline_trace<WIDE>(G, n, J);
@@ -529,6 +540,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
                 const uint32_t lev = si & 0xFu;
                 uint32_t T, ticks, fe, pred, conv;  // conv = 0 unless a converged DYNAMIC forecast
                 J.run_info(G, j, lev, T, ticks, fe, pred, conv);
+                if (wave) ticks = wave_ticks(G, ticks, J.warps(j), (si >> 20) & 0xFu);
                 const uint32_t rs = t + (created ? reconfig : 0u);
                 const uint32_t cap = G.level_mem[lev];
                 uint32_t i_pre = 0xFFFFFFFFu;
@@ -732,6 +744,7 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
             const uint32_t kind = pol.kind;
             const bool fold = (pol.flags & MIG_WARP_FOLD) != 0;
             const bool er = (pol.flags & MIG_EARLY_RESTART) != 0;
+            const bool wave = (pol.flags & MIG_WAVE_TIME) != 0;
             g.sync();
             for (uint32_t j = lane; j < n; j += GW) {
                 const uint4 A = jobA[j];
@@ -751,18 +764,18 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
             const JobStore<WIDE> J{jobA, jobB, P.jobs + j0, P.ext ? P.ext + j0 : nullptr, P.est + j0, P.ctx};
             TraceOut o;
             if (kind == MIG_SCHEME_A)
-                o = scheme_a_trace<GW, WIDE>(G, g, n, J, GL, P.max_jobs, er, fold, pol.reconfig_ticks, full_mem);
+                o = scheme_a_trace<GW, WIDE>(G, g, n, J, GL, P.max_jobs, er, fold, wave, pol.reconfig_ticks, full_mem);
             else if (kind == MIG_FUSION_FISSION)
-                o = simulate_trace<MIG_FUSION_FISSION, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_FUSION_FISSION, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold, wave,
                                                            pol.reconfig_ticks, full_mem);
             else if (kind == MIG_DYNAMIC)
-                o = simulate_trace<MIG_DYNAMIC, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_DYNAMIC, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold, wave,
                                                     pol.reconfig_ticks, full_mem);
             else if (kind == MIG_STATIC)
-                o = simulate_trace<MIG_STATIC, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_STATIC, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold, wave,
                                                    pol.reconfig_ticks, full_mem);
             else
-                o = simulate_trace<MIG_BASELINE, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold,
+                o = simulate_trace<MIG_BASELINE, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold, wave,
                                                      pol.reconfig_ticks, full_mem);
             // ---- a11: per-trace result (80 B, five 128-bit stores from lanes 0-4) ----
             const uint32_t placements = o.K0 & 0xFFFFu, creates = o.K0 >> 16, destroys = o.K1 & 0xFFFFu,

@@ -251,3 +251,21 @@ def test_scheme_a_vs_b_directions():
         a, b = orc.simulate(g, jobs, ext, off, [orc.policy(kind=4), orc.policy(kind=3)])[0]
         worse += b["makespan"] <= a["makespan"]
     assert worse >= 36
+
+
+def test_wave_time_closed_form():
+    # MIG_WAVE_TIME (R31 variant): A100 1g = 14 SMs x 64 warps = 896 resident warps, full = 6272.
+    # A job of W = 6272 warps is one wave on the full GPU and seven on a 1g slice: its 100-tick iteration takes
+    # 700 ticks there. With warp folding the tight fit keeps the wave count (7g) and the iteration stays 100.
+    g = orc.Geometry(geom_path("a100-40gb"))
+    jobs, ext, off = tg.pack_traces([[tg.pack_job(1000, 1000, 1, 0, 100, warps=6272)]])
+    kw = dict(ctx_mib=0, reconfig_ticks=0)
+    r = orc.simulate(g, jobs, ext, off, [orc.policy(kind=3, flags=orc.WAVE_TIME, **kw),
+                                         orc.policy(kind=3, flags=orc.WAVE_TIME | orc.WARP_FOLD, **kw),
+                                         orc.policy(kind=3, **kw), orc.policy(kind=0, flags=orc.WAVE_TIME, **kw)])[0]
+    assert [int(x["makespan"]) for x in r] == [700, 100, 100, 100]
+    assert int(r[0]["busy_slice_ticks"]) == 700 * 1 and int(r[1]["busy_slice_ticks"]) == 100 * 7
+    # 3g (2688) vs 4g (3584): W = 3000 is 2 waves on 3g, 1 on 4g and on the full GPU
+    jobs, ext, off = tg.pack_traces([[tg.pack_job(15000, 15000, 1, 0, 100, warps=3000)]])
+    r = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, flags=orc.WAVE_TIME, **kw))[0, 0]
+    assert int(r["makespan"]) == 200  # tight fit = 3g (fewer compute), two waves

@@ -222,3 +222,15 @@ def test_ewma_variant_parity(cfg, n):
     ref = orc.estimate(og, jobs, ext, off, orc.policy(flags=4), seed=tg.seed_of(cfg))
     for f in ESTIMATE_FIELDS:
         assert np.array_equal(est[f], ref[f]), f
+
+
+@pytest.mark.parametrize("geo", ["a100-40gb", "a30-24gb"])
+def test_wave_time_and_fold_variants(geo):
+    # MIG_WAVE_TIME (R31 variant) x MIG_WARP_FOLD x early restart, all policy kinds, random ragged traces with warps
+    spec = json.load(open(geom_path(geo)))
+    jobs, ext, off = random_tiny_traces(np.random.default_rng(21), spec, 400, 30)
+    specs = [dict(kind=0, flags=8), dict(kind=1, flags=8), dict(kind=2, flags=8 | 2), dict(kind=3, flags=8),
+             dict(kind=3, flags=8 | 2 | 1), dict(kind=4, flags=8), dict(kind=4, flags=8 | 2 | 1), dict(kind=1, flags=3)]
+    got, want, tot = run_pair(geo, jobs, ext, off, specs, seed=5, common=dict(ctx_mib=128, reconfig_ticks=20))
+    assert_same(got, want)
+    check_totals(got, tot)
