@@ -121,6 +121,13 @@ typedef struct {
     uint64_t n_jobs;            /* trace_off[n_traces] - trace_off[0] (sizes internal estimate scratch)  */
     uint32_t max_jobs;          /* upper bound on jobs per trace, 1..MIG_MAX_JOBS_PER_TRACE               */
     uint32_t reserved;          /* must be 0                                                             */
+    /* Recorded per-iteration samples (requested MiB and inverse reuse ratio per iteration), or NULL
+     * to draw them from the generator. samples points at the sample of index sample_off[0]; DYNAMIC job j's
+     * iteration i (1-based) is samples[sample_off[j] - sample_off[0] + i - 1] = {req_mib, inv_reuse_q16}, and
+     * sample_off[j+1] - sample_off[j] must be >= its iteration count. sample_off has n_jobs + 1 entries aligned
+     * with the job records (jobs[k] <-> sample_off[k]). */
+    const void* samples;        /* 8 B per sample (uint2)                                                */
+    const uint64_t* sample_off; /* n_jobs + 1, or NULL when samples is NULL                              */
 } mig_traces;
 
 #define MIG_MAX_JOBS_PER_TRACE 768 /* on-chip (shared-memory) staging limit of one trace */
@@ -203,6 +210,11 @@ mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const m
  * current device; returns after the results are in host memory. */
 mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, const mig_policy* policies,
                              uint32_t n_policies, mig_trace_result* out, mig_policy_totals* totals);
+
+/* Workspace of third-party libraries: parse a CUBLAS_WORKSPACE_CONFIG string
+ * ":SIZE_KiB:COUNT[,:SIZE_KiB:COUNT...]" (empty = 0) and return sum(SIZE*1024*COUNT) * n_layers bytes in *bytes
+ * (SPEC.md:228-236). Host only. MIG_E_PARSE on a malformed string. */
+mig_status mig_workspace_bytes(const char* cublas_workspace_config, uint32_t n_layers, uint64_t* bytes);
 
 /* Number of kernel launches issued by the last device call on this thread (bench accounting). */
 uint32_t mig_last_launch_count(void);

@@ -394,8 +394,13 @@ uint16_t first_exceed(const Job& j, uint64_t cap, const OrPolicy& pol) {
     return NEVER;
 }
 
+struct Recorded {  // recorded per-iteration samples of one job, or none
+    const uint32_t* pairs = nullptr;  // (req_mib, inv_reuse_q16) per iteration
+    uint64_t count = 0;
+};
+
 Job load_job(const Geometry& g, const uint32_t* rec, const uint32_t* ext, uint64_t seed, uint64_t trace,
-             uint32_t jidx, const OrPolicy& pol) {
+             uint32_t jidx, const OrPolicy& pol, Recorded rs = Recorded()) {
     Job j;
     j.cls = (rec[2] >> 16) & 0xFF;
     j.iters = rec[2] & 0xFFFF;
@@ -415,8 +420,15 @@ Job load_job(const Geometry& g, const uint32_t* rec, const uint32_t* ext, uint64
         uint64_t key = tg_key(seed, trace, jidx);
         j.y.resize(j.iters);
         j.q.resize(j.iters);
-        for (uint32_t i = 1; i <= j.iters; ++i)
-            tg_dyn_sample(key, i, j.b, j.slope_q8, j.sigma, j.q0, j.qslope, &j.y[i - 1], &j.q[i - 1]);
+        for (uint32_t i = 1; i <= j.iters; ++i) {
+            if (rs.pairs && rs.count > 0) {  // recorded series (a short one repeats its last sample; flagged on GPU)
+                uint64_t k = (i <= rs.count ? i : rs.count) - 1;
+                j.y[i - 1] = rs.pairs[2 * k];
+                j.q[i - 1] = rs.pairs[2 * k + 1];
+            } else {
+                tg_dyn_sample(key, i, j.b, j.slope_q8, j.sigma, j.q0, j.qslope, &j.y[i - 1], &j.q[i - 1]);
+            }
+        }
         // Grow-on-demand: start in the smallest partition (R16).
         j.e.req0_mib = g.mem(0);
         peak_memory_prediction(j.y, j.q, j.iters, pol, j.ws, &j.e);
@@ -980,13 +992,23 @@ void or_fit_once(const uint32_t* y, const uint32_t* q, uint32_t n, uint32_t T, c
 }
 
 // Per-job estimates for traces [0, n_traces) (trace ids trace_id0 + t).
+static Recorded recorded(const uint32_t* samples, const uint64_t* sample_off, uint64_t j) {
+    Recorded r;
+    if (samples && sample_off) {
+        r.pairs = samples + 2 * (sample_off[j] - sample_off[0]);
+        r.count = sample_off[j + 1] - sample_off[j];
+    }
+    return r;
+}
+
 int or_estimate(void* gp, const uint32_t* jobs, const uint32_t* ext, const uint64_t* trace_off, uint64_t n_traces,
-                uint64_t trace_id0, uint64_t seed, const OrPolicy* pol, OrEstimate* out) {
+                uint64_t trace_id0, uint64_t seed, const OrPolicy* pol, OrEstimate* out, const uint32_t* samples,
+                const uint64_t* sample_off) {
     Geometry* g = (Geometry*)gp;
     for (uint64_t t = 0; t < n_traces; ++t)
         for (uint64_t j = trace_off[t]; j < trace_off[t + 1]; ++j) {
             Job jb = load_job(*g, jobs + 4 * j, ext ? ext + 4 * j : nullptr, seed, trace_id0 + t,
-                              (uint32_t)(j - trace_off[t]), *pol);
+                              (uint32_t)(j - trace_off[t]), *pol, recorded(samples, sample_off, j));
             out[j] = jb.e;
         }
     return 0;
@@ -996,7 +1018,8 @@ int or_estimate(void* gp, const uint32_t* jobs, const uint32_t* ext, const uint6
 // policy only), the decision records are written there (up to rec_cap) and their count to *rec_n.
 int or_simulate(void* gp, const uint32_t* jobs, const uint32_t* ext, const uint64_t* trace_off, uint64_t t0,
                 uint64_t t1, uint64_t trace_id0, uint64_t seed, const OrPolicy* pols, uint32_t n_pol, OrResult* out,
-                uint64_t* rec, uint64_t rec_cap, uint64_t* rec_n) {
+                uint64_t* rec, uint64_t rec_cap, uint64_t* rec_n, const uint32_t* samples,
+                const uint64_t* sample_off) {
     Geometry* g = (Geometry*)gp;
     g_err.clear();
     for (uint64_t t = t0; t < t1; ++t) {
@@ -1009,7 +1032,7 @@ int or_simulate(void* gp, const uint32_t* jobs, const uint32_t* ext, const uint6
             std::vector<Job> js;
             for (uint64_t j = trace_off[t]; j < trace_off[t + 1]; ++j)
                 js.push_back(load_job(*g, jobs + 4 * j, ext ? ext + 4 * j : nullptr, seed, trace_id0 + t,
-                                      (uint32_t)(j - trace_off[t]), pols[p]));
+                                      (uint32_t)(j - trace_off[t]), pols[p], recorded(samples, sample_off, j)));
             std::vector<uint64_t> recs;
             Sim sim(*g, pols[p], js, rec ? &recs : nullptr);
             sim.run();

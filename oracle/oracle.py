@@ -80,10 +80,10 @@ def lib():
         L.or_fit_once.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(OrPolicy), C.c_uint32,
                                   C.POINTER(C.c_int64)] + [C.POINTER(C.c_double)] * 3
         L.or_estimate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
-                                  C.c_uint64, C.POINTER(OrPolicy), C.c_void_p]
+                                  C.c_uint64, C.POINTER(OrPolicy), C.c_void_p, C.c_void_p, C.c_void_p]
         L.or_simulate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                   C.c_uint64, C.c_uint64, C.POINTER(OrPolicy), C.c_uint32, C.c_void_p, C.c_void_p,
-                                  C.c_uint64, C.POINTER(C.c_uint64)]
+                                  C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -197,17 +197,26 @@ def fit_once(y, q, T, pol=None, ws=0):
     return P.value, phi.value, a.value, s.value
 
 
-def estimate(geom: Geometry, jobs, ext, trace_off, pol, seed=0, trace_id0=0):
+def _samples(samples, sample_off):
+    if samples is None:
+        return None, None
+    return np.ascontiguousarray(samples, np.uint32), np.ascontiguousarray(sample_off, np.uint64)
+
+
+def estimate(geom: Geometry, jobs, ext, trace_off, pol, seed=0, trace_id0=0, samples=None, sample_off=None):
     n_traces = len(trace_off) - 1
     out = np.zeros(int(trace_off[-1]), ESTIMATE_DTYPE)
     jobs = np.ascontiguousarray(jobs, np.uint32)
     ext = None if ext is None else np.ascontiguousarray(ext, np.uint32)
     off = np.ascontiguousarray(trace_off, np.uint64)
-    lib().or_estimate(geom.h, _ptr(jobs), _ptr(ext), _ptr(off), n_traces, trace_id0, seed, C.byref(pol), _ptr(out))
+    smp, soff = _samples(samples, sample_off)
+    lib().or_estimate(geom.h, _ptr(jobs), _ptr(ext), _ptr(off), n_traces, trace_id0, seed, C.byref(pol), _ptr(out),
+                      _ptr(smp), _ptr(soff))
     return out
 
 
-def simulate(geom: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, t0=0, t1=None, records=False):
+def simulate(geom: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, t0=0, t1=None, records=False,
+             samples=None, sample_off=None):
     """Run the oracle on traces [t0, t1). Returns results[(t1-t0), n_pol] (and the record list if records)."""
     if not isinstance(pols, (list, tuple)):
         pols = [pols]
@@ -223,8 +232,10 @@ def simulate(geom: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, t0
     if records:
         assert t1 - t0 == 1 and len(pols) == 1
         rec = np.zeros(1 << 16, np.uint64)
+    smp, soff = _samples(samples, sample_off)
     rc = lib().or_simulate(geom.h, _ptr(jobs), _ptr(ext), _ptr(off), t0, t1, trace_id0, seed, parr, len(pols),
-                           _ptr(out), _ptr(rec), 0 if rec is None else len(rec), C.byref(rec_n))
+                           _ptr(out), _ptr(rec), 0 if rec is None else len(rec), C.byref(rec_n), _ptr(smp),
+                           _ptr(soff))
     if rc != 0:
         raise RuntimeError(lib().or_last_error().decode())
     if records:

@@ -55,7 +55,7 @@ class mig_geometry_info(C.Structure):
 class mig_traces(C.Structure):
     _fields_ = [("jobs", C.c_void_p), ("jobs_ext", C.c_void_p), ("trace_off", C.c_void_p), ("n_traces", C.c_uint64),
                 ("trace_id0", C.c_uint64), ("seed", C.c_uint64), ("n_jobs", C.c_uint64), ("max_jobs", C.c_uint32),
-                ("reserved", C.c_uint32)]
+                ("reserved", C.c_uint32), ("samples", C.c_void_p), ("sample_off", C.c_void_p)]
 
 
 class mig_policy(C.Structure):
@@ -145,8 +145,10 @@ def policy(g: Geometry | None = None, kind=MIG_FUSION_FISSION, flags=0, ctx_mib=
 class Traces:
     """Device-resident traces: keeps the tensors alive and carries the mig_traces descriptor."""
 
-    def __init__(self, jobs, ext, trace_off, n_traces, seed=0, trace_id0=0, max_jobs=None, n_jobs=None):
+    def __init__(self, jobs, ext, trace_off, n_traces, seed=0, trace_id0=0, max_jobs=None, n_jobs=None,
+                 samples=None, sample_off=None):
         self.jobs, self.ext, self.trace_off = jobs, ext, trace_off
+        self.samples, self.sample_off = samples, sample_off
         self.n_traces = int(n_traces)
         self.n_jobs = int(jobs.shape[0]) if n_jobs is None else int(n_jobs)
         if max_jobs is None:
@@ -156,10 +158,13 @@ class Traces:
         self.max_jobs = int(max_jobs)
         self.desc = mig_traces(jobs.data_ptr() if self.n_jobs else None,
                                ext.data_ptr() if ext is not None else None, trace_off.data_ptr(), self.n_traces,
-                               trace_id0, seed, self.n_jobs, self.max_jobs, 0)
+                               trace_id0, seed, self.n_jobs, self.max_jobs, 0,
+                               None if samples is None else samples.data_ptr(),
+                               None if sample_off is None else sample_off.data_ptr())
 
 
-def traces_from_numpy(jobs, ext, trace_off, seed=0, trace_id0=0, device=None, max_jobs=None) -> Traces:
+def traces_from_numpy(jobs, ext, trace_off, seed=0, trace_id0=0, device=None, max_jobs=None, samples=None,
+                      sample_off=None) -> Traces:
     import torch
 
     dev = device or torch.device("cuda", torch.cuda.current_device())
@@ -169,7 +174,11 @@ def traces_from_numpy(jobs, ext, trace_off, seed=0, trace_id0=0, device=None, ma
     if max_jobs is None:
         lens = np.diff(np.asarray(trace_off, np.int64))
         max_jobs = max(1, int(lens.max())) if len(lens) else 1
-    return Traces(j, e, o, len(trace_off) - 1, seed, trace_id0, max_jobs)
+    smp = soff = None
+    if samples is not None:
+        smp = torch.from_numpy(np.ascontiguousarray(samples, np.uint32).view(np.int32).reshape(-1, 2)).to(dev)
+        soff = torch.from_numpy(np.ascontiguousarray(sample_off, np.uint64).view(np.int64)).to(dev)
+    return Traces(j, e, o, len(trace_off) - 1, seed, trace_id0, max_jobs, samples=smp, sample_off=soff)
 
 
 def _stream_ptr(stream):
@@ -215,7 +224,7 @@ def mig_simulate(g: Geometry, tr: Traces, pols, est=None, out=None, totals=None,
 
 
 def mig_simulate_host(g: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, max_jobs=None, out=None,
-                      totals=None):
+                      totals=None, samples=None, sample_off=None):
     """HOST buffers in, HOST results out (page-locked numpy views recommended). Returns (results [n_traces, n_pol]
     RESULT_DTYPE, totals [n_pol] TOTALS_DTYPE)."""
     parr, n = _policies(pols)
@@ -227,8 +236,13 @@ def mig_simulate_host(g: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0
         out = np.zeros((n_traces, n), RESULT_DTYPE)
     if totals is None:
         totals = np.zeros(n, TOTALS_DTYPE)
+    if samples is not None:
+        samples = np.ascontiguousarray(samples, np.uint32)
+        sample_off = np.ascontiguousarray(sample_off, np.uint64)
     desc = mig_traces(jobs.ctypes.data if len(jobs) else None, None if ext is None else ext.ctypes.data,
-                      trace_off.ctypes.data, n_traces, trace_id0, seed, int(trace_off[-1] - trace_off[0]), max_jobs, 0)
+                      trace_off.ctypes.data, n_traces, trace_id0, seed, int(trace_off[-1] - trace_off[0]), max_jobs, 0,
+                      None if samples is None else samples.ctypes.data,
+                      None if sample_off is None else sample_off.ctypes.data)
     _check(_lib.mig_simulate_host(g.h, C.byref(desc), parr, n, out.ctypes.data, totals.ctypes.data))
     return out, totals
 
@@ -245,3 +259,13 @@ def totals_numpy(tot_tensor):
 
 def estimates_numpy(est_tensor):
     return est_tensor.cpu().numpy().view(ESTIMATE_DTYPE).reshape(-1)
+
+
+def mig_workspace_bytes(cublas_workspace_config: str, n_layers: int = 1) -> int:
+    """Third-party workspace bytes from a CUBLAS_WORKSPACE_CONFIG string."""
+    out = C.c_uint64()
+    _check(_lib.mig_workspace_bytes(cublas_workspace_config.encode(), n_layers, C.byref(out)))
+    return out.value
+
+
+_lib.mig_workspace_bytes.argtypes = [C.c_char_p, C.c_uint32, C.POINTER(C.c_uint64)]

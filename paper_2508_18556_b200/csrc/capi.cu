@@ -81,6 +81,8 @@ mig_status check_traces(const mig_traces* tr) {
         return mig_set_error(MIG_E_INVALID_ARG, "traces.max_jobs must be 1.." +
                                                     std::to_string(MIG_MAX_JOBS_PER_TRACE));
     if (tr->reserved != 0) return mig_set_error(MIG_E_INVALID_ARG, "traces.reserved must be 0");
+    if ((tr->samples == nullptr) != (tr->sample_off == nullptr))
+        return mig_set_error(MIG_E_INVALID_ARG, "traces.samples and traces.sample_off go together");
     return MIG_OK;
 }
 
@@ -157,6 +159,37 @@ mig_geometry::~mig_geometry() {
 extern "C" {
 
 const char* mig_last_error(void) { return t_err.c_str(); }
+
+mig_status mig_workspace_bytes(const char* cfg, uint32_t n_layers, uint64_t* bytes) {
+    if (!cfg || !bytes) return mig_set_error(MIG_E_INVALID_ARG, "mig_workspace_bytes: null argument");
+    uint64_t total = 0;
+    const char* p = cfg;
+    while (*p == ' ') ++p;
+    while (*p) {
+        uint64_t v[2];
+        for (int k = 0; k < 2; ++k) {
+            if (*p != ':') return mig_set_error(MIG_E_PARSE, std::string("expected ':' at offset ") + std::to_string(p - cfg));
+            ++p;
+            if (*p < '0' || *p > '9') return mig_set_error(MIG_E_PARSE, std::string("expected a number at offset ") + std::to_string(p - cfg));
+            uint64_t x = 0;
+            while (*p >= '0' && *p <= '9') {
+                x = x * 10 + (uint64_t)(*p - '0');
+                if (x > (1ull << 40)) return mig_set_error(MIG_E_PARSE, "value too large");
+                ++p;
+            }
+            v[k] = x;
+        }
+        total += v[0] * 1024ull * v[1];
+        if (*p == ',') {
+            ++p;
+            if (!*p) return mig_set_error(MIG_E_PARSE, "trailing ','");
+        } else if (*p) {
+            return mig_set_error(MIG_E_PARSE, std::string("unexpected character at offset ") + std::to_string(p - cfg));
+        }
+    }
+    *bytes = total * n_layers;
+    return MIG_OK;
+}
 
 uint32_t mig_last_launch_count(void) { return t_launches; }
 
@@ -280,6 +313,17 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
             e = cudaMemcpyAsync(d_ext, (const uint8_t*)T.jobs_ext + jlo * 16, nj * 16, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(d_off, off + t0, (nt + 1) * 8, cudaMemcpyHostToDevice, s);
+        uint8_t* d_smp = nullptr;
+        uint64_t* d_soff = nullptr;
+        if (e == cudaSuccess && T.samples) {  // recorded samples of this chunk's jobs (stream-ordered scratch)
+            const uint64_t* so = T.sample_off;
+            const uint64_t slo = so[jlo] - so[0], shi = so[jhi] - so[0];
+            e = cudaMallocAsync(&d_smp, (shi - slo) * 8 + 8, s);
+            if (e == cudaSuccess) e = cudaMallocAsync(&d_soff, (nj + 1) * 8, s);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(d_smp, (const uint8_t*)T.samples + slo * 8, (shi - slo) * 8, cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(d_soff, so + jlo, (nj + 1) * 8, cudaMemcpyHostToDevice, s);
+        }
         if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, 64, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(d_tot, 0, n_policies * sizeof(mig_policy_totals), s);
         if (e != cudaSuccess) {
@@ -293,7 +337,11 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         ct.n_traces = nt;
         ct.trace_id0 = T.trace_id0 + t0;
         ct.n_jobs = nj;
+        ct.samples = d_smp;
+        ct.sample_off = d_soff;
         st = simulate_device(g, Gdev, dev, ct, policies, n_policies, nullptr, d_est, d_out, d_tot, d_cnt, s);
+        if (d_smp) cudaFreeAsync(d_smp, s);
+        if (d_soff) cudaFreeAsync(d_soff, s);
         if (st != MIG_OK) break;
         if (out)
             e = cudaMemcpyAsync(out + t0 * n_policies, d_out, nt * n_policies * sizeof(mig_trace_result),

@@ -24,6 +24,8 @@ struct EstParams {
     const uint64_t* off;
     uint64_t n_traces, trace_id0, seed;
     mig_job_estimate* out;
+    const uint2* samples;       // recorded samples or NULL (generator)
+    const uint64_t* sample_off;
     unsigned long long* counter;
     unsigned long long* err;
     uint32_t ctx, eps_num, eps_den, conv_k, min_n;
@@ -90,7 +92,8 @@ __device__ __forceinline__ void store_estimate(mig_job_estimate* dst, uint32_t r
 
 // Whole-warp estimation of one DYNAMIC job (lanes over iterations).
 __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t trace_id, uint32_t jidx, uint4 r,
-                                 uint4 e, uint32_t lane, mig_job_estimate* dst) {
+                                 uint4 e, uint32_t lane, mig_job_estimate* dst, const uint2* rec_samples,
+                                 uint32_t rec_count) {
     const uint32_t T = r.z & 0xFFFFu;
     const uint32_t b = r.x, q0 = r.y, ws = e.x, slope = e.z, sigma_n = e.w & 0xFFFFu, qs = e.w >> 16;
     const uint64_t key = tg_key(P.seed, trace_id, jidx);
@@ -102,7 +105,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         for (int k = 0; k < kMaxLevels; ++k)
             if ((uint32_t)k == l) fe[k] = v;
     };
-    const bool q_unit = q0 == 65536u && qs == 0;  // constant inverse reuse 1.0: phys = y + ws + ctx
+    const bool q_unit = !rec_samples && q0 == 65536u && qs == 0;  // generated, constant inverse reuse 1.0
     uint32_t lnext = 0;                          // lowest level whose first exceed is not yet known
     int64_t Sy = 0, Sty = 0, Syy = 0, Sq = 0, Stq = 0, Plast = 0, Lcarry = 0;
     uint32_t okprev = 0, conv = 0, pred = 0;
@@ -115,8 +118,14 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         const bool valid = n <= T;
         uint32_t y = 0, q = 0;
         if (valid) {
-            tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
-            bad |= (q == 0) | (y >= (1u << 18));
+            if (rec_samples) {  // recorded series (coalesced 8 B loads)
+                const uint2 v = __ldg(rec_samples + (n <= rec_count ? n : rec_count) - 1);  // short series: flagged
+                y = v.x;
+                q = v.y;
+            } else {
+                tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
+            }
+            bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
         }
         // first-exceed iteration of every memory level (R12): phys(i) = floor(y*65536/q) + ws + ctx > L.
         // Levels ascend, so fe[l] <= fe[l+1]: only the lowest level not yet crossed needs a ballot per chunk
@@ -237,7 +246,19 @@ __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstP
                 ee.y = __shfl_sync(FULL, e.y, L);
                 ee.z = __shfl_sync(FULL, e.z, L);
                 ee.w = __shfl_sync(FULL, e.w, L);
-                estimate_dynamic(G, P, P.trace_id0 + tr, c + L, rr, ee, lane, P.out + j0 + c + L);
+                const uint2* rs = nullptr;
+                uint32_t rcount = 0;
+                if (P.samples) {
+                    const uint64_t k = j0 + c + L;
+                    rs = P.samples + (P.sample_off[k] - P.sample_off[0]);
+                    const uint64_t cnt = P.sample_off[k + 1] - P.sample_off[k];
+                    rcount = cnt > 0xFFFFu ? 0xFFFFu : (uint32_t)cnt;
+                    if (rcount < (rr.z & 0xFFFFu)) {
+                        if (lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
+                        if (rcount == 0) rs = nullptr;  // nothing recorded: fall back to the declared generator
+                    }
+                }
+                estimate_dynamic(G, P, P.trace_id0 + tr, c + L, rr, ee, lane, P.out + j0 + c + L, rs, rcount);
             }
         }
     }
@@ -254,6 +275,8 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
     P.trace_id0 = tr.trace_id0;
     P.seed = tr.seed;
     P.out = out;
+    P.samples = (const uint2*)tr.samples;
+    P.sample_off = tr.sample_off;
     P.counter = scratch;
     P.err = scratch + 1;
     P.ctx = pol.ctx_mib;

@@ -79,3 +79,13 @@ def test_device_calls_fail_loudly_without_gpu():
     pol = mig.policy(g)
     rc = mig._lib.mig_simulate(g.h, C.byref(desc), C.byref(pol), 1, None, None, None, None)
     assert rc == 6 and "no CUDA device" in mig._lib.mig_last_error().decode()
+
+
+def test_workspace_parser_spec_examples():
+    # PAPER.md:358-362 (CUBLAS_WORKSPACE_CONFIG); SPEC.md:234-236 worked values
+    assert mig.mig_workspace_bytes(":4096:8", 1) == 33_554_432
+    assert mig.mig_workspace_bytes("", 10) == 0
+    assert mig.mig_workspace_bytes(":4096:2,:16:8", 3) == 3 * (4096 * 1024 * 2 + 16 * 1024 * 8) == 25_559_040
+    for bad in [":4096", "4096:8", ":4096:8,", ":a:8", ":4096:8;"]:
+        with pytest.raises(mig.MigError, match="MIG_E_PARSE"):
+            mig.mig_workspace_bytes(bad, 1)

@@ -118,3 +118,41 @@ def test_reuse_lowers_physical_forecast():
     e1 = orc.predict_series(y, [Q1] * 40, orc.policy(ctx_mib=0))
     e2 = orc.predict_series(y, [Q1 + 500 * i for i in range(1, 41)], orc.policy(ctx_mib=0))
     assert e2["pred_mib"] < e1["pred_mib"]
+
+
+def test_prediction_error_at_ten_percent():
+    # SPEC.md:480 / PAPER.md:765 analogue: the forecast made after 10% of the iterations is within 15% (mean
+    # relative error) of the realised peak physical memory on the synthetic dynamic workloads (configs 3 and 4).
+    from tracegen import tracegen as tg
+
+    for cfg, n in [(3, 80), (4, 120)]:
+        jobs, ext, off = tg.generate_host(cfg, n)
+        seed = tg.seed_of(cfg)
+        pol = orc.policy(ctx_mib=512)
+        errs = []
+        for t in range(n):
+            for j in range(int(off[t]), int(off[t + 1])):
+                if ((int(jobs[j, 2]) >> 16) & 0xFF) != 2:
+                    continue
+                T = int(jobs[j, 2]) & 0xFFFF
+                y, q = tg.dyn_samples(seed, t, j - int(off[t]), jobs[j], ext[j], T)
+                ws = int(ext[j, 0])
+                peak = int((y.astype(np.int64) * 65536 // q).max()) + ws + 512
+                P, _, _, _ = orc.fit_once(y[: max(3, T // 10)], q[: max(3, T // 10)], T, pol, ws)
+                errs.append(abs(P - peak) / peak)
+        assert len(errs) > 20 and np.mean(errs) <= 0.15, (cfg, np.mean(errs))
+
+
+def test_recorded_series_equals_generated():
+    # Recorded per-iteration samples fed explicitly give the same estimates as the generator.
+    from tracegen import tracegen as tg
+
+    jobs, ext, off = tg.generate_host(3, 60)
+    seed = tg.seed_of(3)
+    g = orc.Geometry(__import__("conftest").geom_path("a100-80gb"))
+    smp, soff = tg.explicit_samples(jobs, ext, off, seed)
+    a = orc.estimate(g, jobs, ext, off, orc.policy(), seed=seed)
+    b = orc.estimate(g, jobs, ext, off, orc.policy(), seed=12345, samples=smp, sample_off=soff)
+    dyn = ((jobs[:, 2] >> 16) & 0xFF) == 2
+    assert dyn.sum() > 10
+    assert np.array_equal(a[dyn], b[dyn])

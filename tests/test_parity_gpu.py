@@ -234,3 +234,28 @@ def test_wave_time_and_fold_variants(geo):
     got, want, tot = run_pair(geo, jobs, ext, off, specs, seed=5, common=dict(ctx_mib=128, reconfig_ticks=20))
     assert_same(got, want)
     check_totals(got, tot)
+
+
+@pytest.mark.parametrize("cfg,n", [(3, 300), (4, 1000)])
+def test_recorded_samples_parity(cfg, n, monkeypatch):
+    # the predictor on recorded traces: explicit per-iteration samples through the C ABI
+    jobs, ext, off = tg.generate_host(cfg, n)
+    seed = tg.seed_of(cfg)
+    smp, soff = tg.explicit_samples(jobs, ext, off, seed)
+    geo = tg.CONFIG_GEOMETRY[cfg]
+    g = mig.mig_geometry_load(f"builtin:{geo}")
+    og = orc.Geometry(geom_path(geo))
+    wrong_seed = seed ^ 0xABCDEF  # recorded samples must be what is used, not the generator
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=wrong_seed, samples=smp, sample_off=soff)
+    est = mig.estimates_numpy(mig.mig_estimate_memory(g, tr, mig.policy(g)))
+    ref = orc.estimate(og, jobs, ext, off, orc.policy(), seed=seed)  # generator with the right seed
+    for f in ESTIMATE_FIELDS:
+        assert np.array_equal(est[f], ref[f]), f
+    pols = [mig.policy(g, **s) for s in SPECS]
+    res, _ = mig.mig_simulate(g, tr, pols)
+    want = orc.simulate(og, jobs, ext, off, [orc.policy(**s) for s in SPECS], seed=wrong_seed, samples=smp,
+                        sample_off=soff)
+    assert_same(mig.results_numpy(res, len(pols)), want)
+    monkeypatch.setenv("MIG_HOST_CHUNK_JOBS", "3000")
+    hres, _ = mig.mig_simulate_host(g, jobs, ext, off, pols, seed=wrong_seed, samples=smp, sample_off=soff)
+    assert_same(hres, want)

@@ -125,3 +125,22 @@ def pack_traces(traces):
     J = np.array(jobs, np.uint32).reshape(-1, 4)
     E = np.array(ext, np.uint32).reshape(-1, 4)
     return J, E, np.array(off, np.uint64)
+
+
+def explicit_samples(jobs, ext, trace_off, seed, trace_id0=0):
+    """Materialise the per-iteration samples of every DYNAMIC job as a recorded series: (samples u32 [S, 2],
+    sample_off u64 [n_jobs + 1]) aligned with the job records (non-dynamic jobs get none)."""
+    n_traces = len(trace_off) - 1
+    chunks, off = [], [0]
+    for t in range(n_traces):
+        for j in range(int(trace_off[t]), int(trace_off[t + 1])):
+            cls = (int(jobs[j, 2]) >> 16) & 0xFF
+            T = int(jobs[j, 2]) & 0xFFFF
+            if cls == 2 and T > 0:
+                y, q = dyn_samples(seed, trace_id0 + t, j - int(trace_off[t]), jobs[j], ext[j], T)
+                chunks.append(np.stack([y, q], axis=1))
+                off.append(off[-1] + T)
+            else:
+                off.append(off[-1])
+    smp = np.concatenate(chunks).astype(np.uint32) if chunks else np.zeros((1, 2), np.uint32)
+    return smp, np.array(off, np.uint64)
