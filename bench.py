@@ -234,9 +234,9 @@ def run_mine(args):
     jobs, ext, off = tg.generate_device(cfg, n_per, trace_id0=t_id0, seed=seed, device=dev)
     J = tg.jobs_per_trace(cfg)
     tr = mig.Traces(jobs, ext, off, n_per, seed=seed, trace_id0=t_id0, max_jobs=J)
-    est = torch.empty((tr.n_jobs, 48), dtype=torch.uint8, device=dev)
-    res = torch.empty((n_per * n_pol, 80), dtype=torch.uint8, device=dev)
-    tot = torch.empty((n_pol, 160), dtype=torch.uint8, device=dev)
+    est = torch.empty((tr.n_jobs, 80), dtype=torch.uint8, device=dev)
+    res = torch.empty((n_per * n_pol, 96), dtype=torch.uint8, device=dev)
+    tot = torch.empty((n_pol, 192), dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     log(f"generated {n_per} traces of config {cfg} on {dev}")
 
@@ -255,7 +255,7 @@ def run_mine(args):
         if ev is not None:
             ev[2].record(stream)
         if world > 1:  # the per-policy metric reduce over NVLink (NCCL)
-            reduce_totals(tot.view(torch.int64).view(n_pol, 20), dist)
+            reduce_totals(tot.view(torch.int64).view(n_pol, 24), dist)
 
     for _ in range(args.warmup):
         step()
@@ -309,7 +309,7 @@ def run_mine(args):
         hoff = torch.empty(off.shape, dtype=torch.int64, pin_memory=True)
         hoff.copy_(off)
         ho = hoff.numpy().view("u8")
-        hres = torch.empty((n_per * n_pol, 80), dtype=torch.uint8, pin_memory=True)
+        hres = torch.empty((n_per * n_pol, 96), dtype=torch.uint8, pin_memory=True)
         hjn = hj.numpy().view("u4")
         hen = None if he is None else he.numpy().view("u4")
         hresn = hres.numpy().view(mig.RESULT_DTYPE).reshape(n_per, n_pol)
@@ -372,7 +372,7 @@ def run_mine(args):
                      "ncu_issue_slot_util": ncu.get("k_simulate_issue_slot_util"),
                      "ncu_active_lanes_per_instr": ncu.get("k_simulate_active_lanes_per_instr"),
                      "ncu_source": ncu.get("source")},
-        "hbm": {"algorithmic_bytes_per_launch": tr.n_jobs * 16 + n_per * n_pol * 80 + tr.n_jobs * 48 * 0,
+        "hbm": {"algorithmic_bytes_per_launch": tr.n_jobs * 16 + n_per * n_pol * 96,
                 "peak_gbs": peaks.get("hbm_gbs")},
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -168,28 +168,35 @@ typedef struct {
  * ---------------------------------------------------------------------------------------------------------------- */
 #define MIG_NEVER 0xFFFFu
 
-typedef struct {             /* 48 B, one per job                                                          */
+typedef struct {             /* 80 B, one per job                                                          */
     uint32_t req0_mib;       /* first memory requirement: est + ws + ctx, or the smallest slice (DYNAMIC) */
     uint32_t pred_mib;       /* converged forecast incl. ws + ctx (DYNAMIC), else 0                       */
     uint16_t conv_iter;      /* iteration at which the forecast converged (DYNAMIC), 0 = never            */
     uint16_t n_levels;
     uint16_t fe[6];          /* first iteration whose physical memory exceeds memory level l; MIG_NEVER   */
     double phi, a, sigma;    /* diagnostics of the last fit (DYNAMIC)                                     */
+    uint32_t mem_fe[5];      /* sum of the physical MiB over iterations 1..fe[l] (0 if fe[l] = NEVER)     */
+    uint32_t mem_conv;       /* ... over iterations 1..conv_iter                                          */
+    uint32_t mem_T;          /* ... over all iterations                                                   */
+    uint32_t reserved;
 } mig_job_estimate;
 
-typedef struct {             /* 80 B, one per (trace, policy)                                             */
+typedef struct {             /* 96 B, one per (trace, policy)                                             */
     uint32_t makespan, n_jobs, completed, rejected, failed, ooms, preempts, restarts, placements, waits,
         creates, destroys;
     uint64_t energy_wticks, turnaround_sum, busy_slice_ticks, decision_hash;
+    uint64_t mem_mib_ticks;  /* integral of the running jobs' physical MiB over time; memory utilisation =
+                                mem_mib_ticks / (GPU MiB * makespan)                      */
+    uint64_t wasted_ticks;   /* duration of runs that ended in OOM or early restart */
 } mig_trace_result;
 
 #define MIG_ERR_TRACE_TOO_LONG 1ull /* a trace has more than max_jobs jobs                             */
 #define MIG_ERR_BAD_RECORD 2ull     /* class > 2, iters > 4096, or a sample outside the predictor's range */
 
-typedef struct {             /* 160 B, one per policy: sums over traces (integer, exact in any order)     */
+typedef struct {             /* 192 B, one per policy: sums over traces (integer, exact in any order)     */
     uint64_t n_traces, n_jobs, completed, rejected, failed, ooms, preempts, restarts, placements, waits,
         creates, destroys, makespan_sum, makespan_max, energy_wticks, turnaround_sum, busy_slice_ticks,
-        decision_hash_sum, error_flags, reserved;
+        decision_hash_sum, mem_mib_ticks, wasted_ticks, error_flags, reserved[3];
 } mig_policy_totals;
 
 /* Per-job estimates for every job of the traces (DEVICE buffers; out has trace_off[n]-trace_off[0] entries).

@@ -61,20 +61,23 @@ struct OrPolicy {
     uint32_t eps_num, eps_den, conv_k, min_n;
 };
 
-struct OrEstimate {  // 48 B
+struct OrEstimate {  // 80 B
     uint32_t req0_mib, pred_mib;
     uint16_t conv_iter, n_levels;
     uint16_t fe[6];
     double phi, a, sigma;
+    uint32_t mem_fe[5], mem_conv, mem_T, pad;  // sum of physical MiB over iterations 1..k, k = fe[l], conv, T
 };
 
 struct OrResult {  // 80 B
     uint32_t makespan, n_jobs, completed, rejected, failed, ooms, preempts, restarts, placements, waits, creates,
         destroys;
     uint64_t energy_wticks, turnaround_sum, busy_slice_ticks, decision_hash;
+    uint64_t mem_mib_ticks;  // integral of the running jobs' physical memory over time
+    uint64_t wasted_ticks;   // time of runs that ended in OOM or early restart
 };
-static_assert(sizeof(OrEstimate) == 48, "estimate layout");
-static_assert(sizeof(OrResult) == 80, "result layout");
+static_assert(sizeof(OrEstimate) == 80, "estimate layout");
+static_assert(sizeof(OrResult) == 96, "result layout");
 
 enum { BASELINE = 0, STATIC = 1, DYNAMIC = 2, FUSION_FISSION = 3, SCHEME_A = 4 };
 enum { F_EARLY_RESTART = 1, F_WARP_FOLD = 2, F_EWMA = 4, F_WAVE_TIME = 8 };
@@ -387,6 +390,13 @@ uint64_t physical(const Job& j, uint32_t i, const OrPolicy& pol) {
     return (uint64_t)j.tru + j.ws + pol.ctx_mib;
 }
 
+// Sum of the physical memory over iterations 1..k.
+uint64_t memory_sum(const Job& j, uint32_t k, const OrPolicy& pol) {
+    uint64_t s = 0;
+    for (uint32_t i = 1; i <= k; ++i) s += physical(j, i, pol);
+    return s;
+}
+
 // First iteration (1..T) whose physical memory exceeds cap (R12); NEVER if none.
 uint16_t first_exceed(const Job& j, uint64_t cap, const OrPolicy& pol) {
     for (uint32_t i = 1; i <= j.iters; ++i)
@@ -439,6 +449,11 @@ Job load_job(const Geometry& g, const uint32_t* rec, const uint32_t* ext, uint64
         j.e.req0_mib = j.est + j.ws + pol.ctx_mib;
     }
     for (size_t l = 0; l < L.size() && l < 6; ++l) j.e.fe[l] = first_exceed(j, L[l], pol);
+    // memory integrals over the first k iterations (PAPER.md:675 memory utilisation)
+    for (size_t l = 0; l < L.size() && l < 5; ++l)
+        if (j.e.fe[l] != NEVER) j.e.mem_fe[l] = (uint32_t)memory_sum(j, j.e.fe[l], pol);
+    j.e.mem_conv = (uint32_t)memory_sum(j, j.e.conv_iter, pol);
+    j.e.mem_T = (uint32_t)memory_sum(j, j.iters, pol);
     j.req = j.e.req0_mib;
     return j;
 }
@@ -569,6 +584,10 @@ struct Sim {
         ev.tick = end;
         uint32_t comp = pol.kind == BASELINE ? g.d.n_compute : g.d.prof_compute[in.prof];
         r.busy_slice_ticks += (uint64_t)comp * (end - s);
+        // memory held while running: iterations 1..k at `ticks` each (k = OOM / preempt / last iteration)
+        uint32_t iters_run = ev.kind_order == 1 ? i_oom : ev.kind_order == 2 ? i_pre : T;
+        r.mem_mib_ticks += memory_sum(j, iters_run, pol) * ticks;
+        if (ev.kind_order != 0) r.wasted_ticks += end - s;
         events.push(ev);
     }
 

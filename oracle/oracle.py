@@ -25,11 +25,12 @@ RESULT_DTYPE = np.dtype([
     ("makespan", "<u4"), ("n_jobs", "<u4"), ("completed", "<u4"), ("rejected", "<u4"), ("failed", "<u4"),
     ("ooms", "<u4"), ("preempts", "<u4"), ("restarts", "<u4"), ("placements", "<u4"), ("waits", "<u4"),
     ("creates", "<u4"), ("destroys", "<u4"), ("energy_wticks", "<u8"), ("turnaround_sum", "<u8"),
-    ("busy_slice_ticks", "<u8"), ("decision_hash", "<u8")])
+    ("busy_slice_ticks", "<u8"), ("decision_hash", "<u8"), ("mem_mib_ticks", "<u8"), ("wasted_ticks", "<u8")])
 ESTIMATE_DTYPE = np.dtype([
     ("req0_mib", "<u4"), ("pred_mib", "<u4"), ("conv_iter", "<u2"), ("n_levels", "<u2"), ("fe", "<u2", (6,)),
-    ("phi", "<f8"), ("a", "<f8"), ("sigma", "<f8")])
-assert RESULT_DTYPE.itemsize == 80 and ESTIMATE_DTYPE.itemsize == 48
+    ("phi", "<f8"), ("a", "<f8"), ("sigma", "<f8"), ("mem_fe", "<u4", (5,)), ("mem_conv", "<u4"),
+    ("mem_T", "<u4"), ("pad", "<u4")])
+assert RESULT_DTYPE.itemsize == 96 and ESTIMATE_DTYPE.itemsize == 80
 
 
 class OrGeomDesc(C.Structure):

@@ -31,15 +31,17 @@ RESULT_DTYPE = np.dtype([
     ("makespan", "<u4"), ("n_jobs", "<u4"), ("completed", "<u4"), ("rejected", "<u4"), ("failed", "<u4"),
     ("ooms", "<u4"), ("preempts", "<u4"), ("restarts", "<u4"), ("placements", "<u4"), ("waits", "<u4"),
     ("creates", "<u4"), ("destroys", "<u4"), ("energy_wticks", "<u8"), ("turnaround_sum", "<u8"),
-    ("busy_slice_ticks", "<u8"), ("decision_hash", "<u8")])
+    ("busy_slice_ticks", "<u8"), ("decision_hash", "<u8"), ("mem_mib_ticks", "<u8"), ("wasted_ticks", "<u8")])
 ESTIMATE_DTYPE = np.dtype([
     ("req0_mib", "<u4"), ("pred_mib", "<u4"), ("conv_iter", "<u2"), ("n_levels", "<u2"), ("fe", "<u2", (6,)),
-    ("phi", "<f8"), ("a", "<f8"), ("sigma", "<f8")])
+    ("phi", "<f8"), ("a", "<f8"), ("sigma", "<f8"), ("mem_fe", "<u4", (5,)), ("mem_conv", "<u4"),
+    ("mem_T", "<u4"), ("pad", "<u4")])
 TOTALS_FIELDS = ["n_traces", "n_jobs", "completed", "rejected", "failed", "ooms", "preempts", "restarts",
                  "placements", "waits", "creates", "destroys", "makespan_sum", "makespan_max", "energy_wticks",
-                 "turnaround_sum", "busy_slice_ticks", "decision_hash_sum", "error_flags", "reserved"]
+                 "turnaround_sum", "busy_slice_ticks", "decision_hash_sum", "mem_mib_ticks", "wasted_ticks",
+                 "error_flags", "reserved0", "reserved1", "reserved2"]
 TOTALS_DTYPE = np.dtype([(f, "<u8") for f in TOTALS_FIELDS])
-assert RESULT_DTYPE.itemsize == 80 and ESTIMATE_DTYPE.itemsize == 48 and TOTALS_DTYPE.itemsize == 160
+assert RESULT_DTYPE.itemsize == 96 and ESTIMATE_DTYPE.itemsize == 80 and TOTALS_DTYPE.itemsize == 192
 
 
 class MigError(RuntimeError):
@@ -195,27 +197,27 @@ def _policies(pols):
 
 
 def mig_estimate_memory(g: Geometry, tr: Traces, pol: mig_policy, out=None, stream=None):
-    """Per-job estimates on the device. Returns a uint8 CUDA tensor [n_jobs, 48] (view with ESTIMATE_DTYPE)."""
+    """Per-job estimates on the device. Returns a uint8 CUDA tensor [n_jobs, 80] (view with ESTIMATE_DTYPE)."""
     import torch
 
     if out is None:
-        out = torch.empty((tr.n_jobs, 48), dtype=torch.uint8, device=tr.jobs.device)
+        out = torch.empty((tr.n_jobs, 80), dtype=torch.uint8, device=tr.jobs.device)
     _check(_lib.mig_estimate_memory(g.h, C.byref(tr.desc), C.byref(pol), C.c_void_p(out.data_ptr()),
                                     _stream_ptr(stream)))
     return out
 
 
 def mig_simulate(g: Geometry, tr: Traces, pols, est=None, out=None, totals=None, write_results=True, stream=None):
-    """Simulate every trace under each policy on the device. Returns (results uint8 [n_traces*n_pol, 80] or None,
-    totals uint8 [n_pol, 160]); view on the host with RESULT_DTYPE / TOTALS_DTYPE."""
+    """Simulate every trace under each policy on the device. Returns (results uint8 [n_traces*n_pol, 96] or None,
+    totals uint8 [n_pol, 192]); view on the host with RESULT_DTYPE / TOTALS_DTYPE."""
     import torch
 
     parr, n = _policies(pols)
     dev = tr.jobs.device
     if out is None and write_results:
-        out = torch.empty((tr.n_traces * n, 80), dtype=torch.uint8, device=dev)
+        out = torch.empty((tr.n_traces * n, 96), dtype=torch.uint8, device=dev)
     if totals is None:
-        totals = torch.empty((n, 160), dtype=torch.uint8, device=dev)
+        totals = torch.empty((n, 192), dtype=torch.uint8, device=dev)
     _check(_lib.mig_simulate(g.h, C.byref(tr.desc), parr, n,
                              None if est is None else C.c_void_p(est.data_ptr()),
                              None if out is None else C.c_void_p(out.data_ptr()), C.c_void_p(totals.data_ptr()),

@@ -366,9 +366,9 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
             for (uint32_t p = 0; p < n_policies; ++p) {
                 const uint64_t* src = reinterpret_cast<const uint64_t*>(&host_tot[c * n_policies + p]);
                 uint64_t* dst = reinterpret_cast<uint64_t*>(&totals[p]);
-                for (int f = 0; f < 20; ++f) {
+                for (int f = 0; f < 21; ++f) {
                     if (f == 13) dst[f] = std::max(dst[f], src[f]);
-                    else if (f == 18) dst[f] |= src[f];
+                    else if (f == 20) dst[f] |= src[f];
                     else dst[f] += src[f];
                 }
             }

@@ -80,14 +80,28 @@ __device__ __forceinline__ double slope_of(int64_t n, int64_t Sy, int64_t Sty) {
 
 __device__ __forceinline__ void store_estimate(mig_job_estimate* dst, uint32_t req0, uint32_t pred, uint32_t conv,
                                                uint32_t n_levels, const uint32_t fe[5], double phi, double a,
-                                               double sigma) {
+                                               double sigma, const uint32_t mfe[5], uint32_t mconv, uint32_t mT) {
     uint4 w0 = make_uint4(req0, pred, (conv & 0xFFFFu) | (n_levels << 16), fe[0] | (fe[1] << 16));
     uint4 w1 = make_uint4(fe[2] | (fe[3] << 16), fe[4] | (kNever << 16), __double2loint(phi), __double2hiint(phi));
     uint4 w2 = make_uint4(__double2loint(a), __double2hiint(a), __double2loint(sigma), __double2hiint(sigma));
+    uint4 w3 = make_uint4(mfe[0], mfe[1], mfe[2], mfe[3]);
+    uint4 w4 = make_uint4(mfe[4], mconv, mT, 0u);
     uint4* d = reinterpret_cast<uint4*>(dst);
     d[0] = w0;
     d[1] = w1;
     d[2] = w2;
+    d[3] = w3;
+    d[4] = w4;
+}
+
+// Warp inclusive prefix sum (32-bit).
+__device__ __forceinline__ uint32_t warp_scan_u32(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(FULL, v, d);
+        if (lane >= (uint32_t)d) v += o;
+    }
+    return v;
 }
 
 // Whole-warp estimation of one DYNAMIC job (lanes over iterations).
@@ -99,11 +113,16 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     const uint64_t key = tg_key(P.seed, trace_id, jidx);
     const int64_t ws_ctx = (int64_t)ws + P.ctx;
     uint32_t fe[5] = {kNever, kNever, kNever, kNever, kNever};
+    uint32_t mfe[5] = {0u, 0u, 0u, 0u, 0u};  // physical MiB summed over iterations 1..fe[l]
+    uint32_t Smem = 0, mconv = 0;            // running sum (memory integral)
     auto lvl_thr = [&](uint32_t l) -> int64_t { return (int64_t)G.level_mem[l] - ws_ctx; };  // phys > L <=> floor > thr
-    auto fe_set = [&](uint32_t l, uint32_t v) {
+    auto fe_set = [&](uint32_t l, uint32_t v, uint32_t m) {
 #pragma unroll
         for (int k = 0; k < kMaxLevels; ++k)
-            if ((uint32_t)k == l) fe[k] = v;
+            if ((uint32_t)k == l) {
+                fe[k] = v;
+                mfe[k] = m;
+            }
     };
     const bool q_unit = !rec_samples && q0 == 65536u && qs == 0;  // generated, constant inverse reuse 1.0
     uint32_t lnext = 0;                          // lowest level whose first exceed is not yet known
@@ -112,8 +131,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     double phi = 0.0, a = 0.0, sig = 0.0;
     bool done_pred = T < P.min_n;
     bool bad = false;
-    for (uint32_t base = 0; base < T; base += 32) {
-        if (done_pred && lnext >= G.n_levels) break;
+    for (uint32_t base = 0; base < T; base += 32) {  // to T: the memory integral needs every iteration
         const uint32_t n = base + lane + 1;
         const bool valid = n <= T;
         uint32_t y = 0, q = 0;
@@ -127,6 +145,9 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
             }
             bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
         }
+        // physical MiB of iteration n and its running sum (R22: requested / inverse reuse, + ws + ctx)
+        const uint32_t phys = valid ? (uint32_t)((q_unit ? (uint64_t)y : ((uint64_t)y * 65536ull) / q) + ws_ctx) : 0u;
+        const uint32_t pm = Smem + warp_scan_u32(phys, lane);
         // first-exceed iteration of every memory level (R12): phys(i) = floor(y*65536/q) + ws + ctx > L.
         // Levels ascend, so fe[l] <= fe[l+1]: only the lowest level not yet crossed needs a ballot per chunk
         // (more when one chunk crosses several levels).
@@ -136,9 +157,10 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
                                                            : (uint64_t)y * 65536ull >= (uint64_t)(th + 1) * q));
             const uint32_t m = __ballot_sync(FULL, over);
             if (!m) break;
-            fe_set(lnext, base + __ffs(m));
+            fe_set(lnext, base + __ffs(m), __shfl_sync(FULL, pm, __ffs(m) - 1));
             ++lnext;
         }
+        Smem = __shfl_sync(FULL, pm, 31);
         if (done_pred) continue;
         // exact integer moments at n = base + lane + 1 (inclusive warp scans + carried totals)
         const int64_t yi = y, qi = q, ni = n;
@@ -179,8 +201,10 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         const double phs = __shfl_sync(FULL, f.phi, src), ss = __shfl_sync(FULL, f.sigma, src);
         const int64_t nsrc = base + src + 1, sy_s = __shfl_sync(FULL, sy, src), sty_s = __shfl_sync(FULL, sty, src);
         const double as = (cm || (base + 32 >= T && T >= P.min_n)) ? slope_of(nsrc, sy_s, sty_s) : 0.0;
+        const uint32_t pm_src = __shfl_sync(FULL, pm, src);
         if (cm) {
             conv = base + src + 1;
+            mconv = pm_src;
             pred = (uint32_t)Ps;
             phi = phs;
             a = as;
@@ -202,7 +226,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
-    if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig);
+    if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig, mfe, mconv, Smem);
 }
 
 __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstParams P) {
@@ -227,11 +251,14 @@ __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstP
             if (valid && (cls > 2 || T > 4096 || (r.z >> 24) != 0)) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
             if (valid && cls != kClassDynamic && !P.dyn_only) {
                 const uint64_t phys = (uint64_t)r.y + e.x + P.ctx;
-                uint32_t fe[5];
+                uint32_t fe[5], mfe[5];
 #pragma unroll
-                for (int l = 0; l < kMaxLevels; ++l)
+                for (int l = 0; l < kMaxLevels; ++l) {
                     fe[l] = (l < (int)G.n_levels && T >= 1 && phys > G.level_mem[l]) ? 1u : kNever;
-                store_estimate(P.out + j0 + j, r.x + e.x + P.ctx, 0, 0, G.n_levels, fe, 0.0, 0.0, 0.0);
+                    mfe[l] = fe[l] == 1u ? (uint32_t)phys : 0u;
+                }
+                store_estimate(P.out + j0 + j, r.x + e.x + P.ctx, 0, 0, G.n_levels, fe, 0.0, 0.0, 0.0, mfe, 0u,
+                               (uint32_t)phys * T);
             }
             uint32_t dm = __ballot_sync(FULL, valid && cls == kClassDynamic);
             while (dm) {

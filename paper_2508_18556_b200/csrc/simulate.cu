@@ -45,7 +45,8 @@ struct SimParams {
 
 constexpr size_t kGeomBytes = (sizeof(DevGeom) + 15) & ~size_t(15);
 constexpr size_t kPolBytes = (kMaxPolicies * sizeof(mig_policy) + 15) & ~size_t(15);
-constexpr size_t kTotBytes = kMaxPolicies * 20 * 8;
+constexpr int kTotFields = 24;  // mig_policy_totals
+constexpr size_t kTotBytes = kMaxPolicies * kTotFields * 8;
 constexpr uint32_t kValid = 1u << 31, kBusy = 1u << 30;
 
 // A lane group of GW lanes simulates one trace (GW = 32: one trace per warp; GW = 8: four traces per warp).
@@ -92,6 +93,11 @@ __device__ __forceinline__ uint32_t wave_ticks(const DevGeom& G, uint32_t ticks,
     return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
 }
 
+// Run accounting on the lane-distributed accumulators: busy slice-ticks, memory integral, wasted time.
+__device__ __forceinline__ void acc_run(uint64_t& acc, uint32_t lane, uint64_t busy, uint64_t mem, uint64_t wasted) {
+    acc += lane == 1 ? busy : lane == 2 ? mem : lane == 3 ? wasted : 0ull;
+}
+
 // FNV-1a-64 step h = (h ^ (tick << 32 | lo)) * (2^40 + 0x1b3) mod 2^64, on the two 32-bit halves of h.
 __device__ __forceinline__ void rec(uint32_t& hl, uint32_t& hh, uint32_t tick, uint32_t lo) {
     const uint32_t x = hl ^ lo, y = hh ^ tick;
@@ -130,6 +136,16 @@ struct JobStore {
         return WIDE ? A[j].w : (gext ? __ldg(&gext[j].y) : 0u);
     }
     __device__ __forceinline__ uint32_t pred(uint32_t j) const { return WIDE ? B[j].x : A[j].z; }
+    // Physical MiB summed over the iterations 1..k a run executed (memory integral): ek = end kind
+    // (0 COMPLETE after T, 1 OOM after fe, 2 PREEMPT after conv). DYNAMIC jobs read the estimator's prefix sums.
+    __device__ __forceinline__ uint64_t mem_sum(uint32_t j, uint32_t lev, uint32_t ek, uint32_t k) const {
+        const uint4 a = A[j];
+        if (((a.x >> 16) & 0xFFu) == kClassDynamic) {
+            const uint32_t* m = reinterpret_cast<const uint32_t*>(gest + j) + 12;  // mem_fe[5], mem_conv, mem_T
+            return __ldg(m + (ek == 1 ? lev : ek == 2 ? 5u : 6u));
+        }
+        return (uint64_t)(WIDE ? B[j].x : a.z) * k;  // constant footprint
+    }
     // NARROW only: requeue FIFO as a linked list through the spare high half of A[j].w
     __device__ __forceinline__ uint32_t next(uint32_t j) const { return A[j].w >> 16; }
     __device__ __forceinline__ void set_next(uint32_t j, uint32_t nx) const { A[j].w = (A[j].w & 0xFFFFu) | (nx << 16); }
@@ -144,21 +160,22 @@ struct JobStore {
             pred = b.x;
             conv = b.y & 0xFFFFu;
             fe = reinterpret_cast<const uint16_t*>(&B[j])[3 + lev];
-        } else if (((a.x >> 16) & 0xFFu) == kClassDynamic) {
-            pred = a.z;
-            conv = a.w & 0xFFFFu;
-            fe = __ldg(reinterpret_cast<const unsigned short*>(gest + j) + 6 + lev);
         } else {
             pred = 0;
             conv = 0;
             fe = (T >= 1 && a.z > G.level_mem[lev]) ? 1u : kNever;  // R12: static jobs OOM at iteration 1
+            if (__builtin_expect(((a.x >> 16) & 0xFFu) == kClassDynamic, 0)) {  // a real branch, not predicated
+                pred = a.z;
+                conv = a.w & 0xFFFFu;
+                fe = __ldg(reinterpret_cast<const unsigned short*>(gest + j) + 6 + lev);
+            }
         }
     }
 };
 
 struct TraceOut {
     uint32_t K0, K1, K2, K3;  // placements|creates<<16, destroys|waits<<16, rejected|ooms<<16, preempts|failed<<16
-    uint64_t turn, busy;
+    uint64_t acc;             // lane-distributed: lane 0 turnaround, 1 busy slice-ticks, 2 MiB-ticks, 3 wasted ticks
     uint32_t hl, hh;          // decision hash halves
     uint32_t makespan;
 };
@@ -167,10 +184,11 @@ struct TraceOut {
 // partition state and no requeue (an OOM on the whole GPU is FAILED). Straight-line code producing the same
 // decision/event record stream as the general loop: [REJECT]* PLACE [REJECT]* WAIT <event> PLACE ...
 template <bool WIDE>
-__device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n, const JobStore<WIDE>& J) {
+__device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n, const JobStore<WIDE>& J,
+                                                   uint32_t lane) {
     TraceOut o;
     o.K0 = o.K1 = o.K2 = o.K3 = 0;
-    o.turn = o.busy = 0;
+    o.acc = 0;
     o.hl = (uint32_t)kFnvOffset;
     o.hh = (uint32_t)(kFnvOffset >> 32);
     const uint32_t fp = G.full_prof, pi = G.pinfo[fp];
@@ -192,7 +210,8 @@ __device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n,
         J.run_info(G, j, lev, T, ticks, fe, pred, conv);
         const bool oom = fe <= T;  // first exceed of the whole GPU (R12); no early restart on baseline
         const uint32_t end = t + (oom ? fe : T) * ticks;
-        o.busy += (uint64_t)comp * (end - t);
+        acc_run(o.acc, lane, (uint64_t)comp * (end - t), J.mem_sum(j, lev, oom ? 1u : 0u, oom ? fe : T) * ticks,
+                oom ? end - t : 0u);
         ++qh;
         while (qh < n) {  // the rest of the pass at t: rejections, then the head waits
             const uint32_t need2 = J.need(qh);
@@ -214,7 +233,7 @@ __device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n,
             o.K3 += 1u << 16;
         } else {
             rec(o.hl, o.hh, t, (j << 16) | (K_COMPLETE << 12) | ev_lo);
-            o.turn += t;
+            if (lane == 0) o.acc += t;
         }
     }
     o.makespan = t;
@@ -234,7 +253,7 @@ __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<G
     constexpr uint32_t kNone = 0xFFFFFFFFu;
     TraceOut o;
     o.K0 = o.K1 = o.K2 = o.K3 = 0;
-    o.turn = o.busy = 0;
+    o.acc = 0;
     o.hl = (uint32_t)kFnvOffset;
     o.hh = (uint32_t)(kFnvOffset >> 32);
     uint32_t t = 0, glen = 0;
@@ -297,7 +316,8 @@ __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<G
                 nxt += ns;
             }
             BM |= ((si >> 8) & 0xFFu) << s;
-            o.busy += (uint64_t)((si >> 4) & 0xFu) * (end - rs);
+            acc_run(o.acc, lane, (uint64_t)((si >> 4) & 0xFu) * (end - rs),
+                    J.mem_sum(j, lev, ek, ek == 1 ? fe : ek == 2 ? i_pre : T) * ticks, ek ? end - rs : 0u);
         }
     };
     auto next_group = [&]() -> bool {  // set_homogeneous_slices(next non-empty group)
@@ -359,7 +379,7 @@ __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<G
             uint32_t req = 0;
             if (ek == 0) {
                 rec(o.hl, o.hh, t, lo | (K_COMPLETE << 12));
-                o.turn += t;
+                if (lane == 0) o.acc += t;
             } else if (ek == 1) {
                 rec(o.hl, o.hh, t, lo | (K_OOM << 12));
                 const uint32_t nl = G.level_next[si & 0xFu];
@@ -409,7 +429,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
                                                    uint32_t full_mem) {
     const uint32_t lane = g.gl;
     if constexpr (KIND == MIG_BASELINE) {
-        return baseline_trace<WIDE>(G, n, J);
+        return baseline_trace<WIDE>(G, n, J, g.gl);
     }
     uint32_t ii = 0, iend = 0, ijk = 0;  // lane-resident instance (slot = lane)
     uint32_t occ = 0, SM = 0, EM = 0, BM = 0;
@@ -426,7 +446,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
     }
     TraceOut o;
     o.K0 = o.K1 = o.K2 = o.K3 = 0;
-    o.turn = o.busy = 0;
+    o.acc = 0;
     o.hl = (uint32_t)kFnvOffset;
     o.hh = (uint32_t)(kFnvOffset >> 32);
     // queue = jobs[qh..n) ++ requeued jobs (tail, R13): a u16 ring (WIDE) or a list linked through the staged
@@ -562,7 +582,8 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
                     ijk = j | (ek << 16);
                 }
                 BM |= ((si >> 8) & 0xFFu) << s;
-                o.busy += (uint64_t)((si >> 4) & 0xFu) * (end - rs);
+                acc_run(o.acc, lane, (uint64_t)((si >> 4) & 0xFu) * (end - rs),
+                        J.mem_sum(j, lev, ek, ek == 1 ? fe : ek == 2 ? i_pre : T) * ticks, ek ? end - rs : 0u);
             }
         pop:
             if (qh < n) {
@@ -598,7 +619,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
             uint32_t req = 0;
             if (ek == 0) {
                 rec(o.hl, o.hh, t, lo | (K_COMPLETE << 12));
-                o.turn += t;
+                if (lane == 0) o.acc += t;
             } else if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
                 rec(o.hl, o.hh, t, lo | (K_OOM << 12));
                 const uint32_t nl = G.level_next[si & 0xFu];
@@ -676,7 +697,7 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
 #pragma unroll
             for (int k = 0; k < kMaxPolicies; ++k) s_pol[k] = P.pol[k];
         }
-        for (uint32_t i = threadIdx.x; i < kMaxPolicies * 20; i += blockDim.x) s_tot[i] = 0;
+        for (uint32_t i = threadIdx.x; i < kMaxPolicies * kTotFields; i += blockDim.x) s_tot[i] = 0;
     }
     __syncthreads();
     const uint32_t full_mem = G.full_mem;
@@ -728,7 +749,7 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
 #pragma unroll
                     for (int l = 0; l < kMaxLevels; ++l)
                         fe[l] = (l < (int)G.n_levels && T >= 1 && phys > G.level_mem[l]) ? 1u : kNever;
-                    Bv = make_uint4(0u, fe[0] << 16, fe[1] | (fe[2] << 16), fe[3] | (fe[4] << 16));
+                    Bv = make_uint4(phys, fe[0] << 16, fe[1] | (fe[2] << 16), fe[3] | (fe[4] << 16));
                 } else {
                     A.z = phys;
                     A.w = 0;  // conv = 0; high half: requeue link
@@ -782,19 +803,23 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
                            waits = o.K1 >> 16, rejected = o.K2 & 0xFFFFu, ooms = o.K2 >> 16,
                            preempts = o.K3 & 0xFFFFu, failed = o.K3 >> 16;
             const uint32_t completed = n - rejected - failed, restarts = ooms - failed + preempts;
-            const uint64_t energy = (uint64_t)pol.idle_w * o.makespan + (uint64_t)pol.w_per_slice * o.busy;
-            if (P.out && lane < 5) {
+            const uint64_t turn = g.shfl64(o.acc, 0), busy = g.shfl64(o.acc, 1), memt = g.shfl64(o.acc, 2),
+                           wasted = g.shfl64(o.acc, 3);
+            const uint64_t energy = (uint64_t)pol.idle_w * o.makespan + (uint64_t)pol.w_per_slice * busy;
+            if (P.out && lane < 6) {
                 uint4 v;
                 if (lane == 0) v = make_uint4(o.makespan, n, completed, rejected);
                 else if (lane == 1) v = make_uint4(failed, ooms, preempts, restarts);
                 else if (lane == 2) v = make_uint4(placements, waits, creates, destroys);
-                else if (lane == 3) v = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)o.turn,
-                                                   (uint32_t)(o.turn >> 32));
-                else v = make_uint4((uint32_t)o.busy, (uint32_t)(o.busy >> 32), o.hl, o.hh);
+                else if (lane == 3) v = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)turn,
+                                                   (uint32_t)(turn >> 32));
+                else if (lane == 4) v = make_uint4((uint32_t)busy, (uint32_t)(busy >> 32), o.hl, o.hh);
+                else v = make_uint4((uint32_t)memt, (uint32_t)(memt >> 32), (uint32_t)wasted,
+                                    (uint32_t)(wasted >> 32));
                 reinterpret_cast<uint4*>(P.out + tr * P.n_pol + p)[lane] = v;
             }
             // ---- a12: per-policy totals (shared-memory atomics, flushed once per CTA) ----
-            for (uint32_t f = lane; f < 19; f += GW) {
+            for (uint32_t f = lane; f < 21; f += GW) {
                 uint64_t v;
                 switch (f) {
                     case 0: v = 1; break;
@@ -812,27 +837,29 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
                     case 12:
                     case 13: v = o.makespan; break;
                     case 14: v = energy; break;
-                    case 15: v = o.turn; break;
-                    case 16: v = o.busy; break;
+                    case 15: v = turn; break;
+                    case 16: v = busy; break;
                     case 17: v = ((uint64_t)o.hh << 32) | o.hl; break;
+                    case 18: v = memt; break;
+                    case 19: v = wasted; break;
                     default: v = err; break;
                 }
-                if (f == 13) atomicMax(&s_tot[p * 20 + 13], (unsigned long long)v);
-                else if (f == 18) { if (v) atomicOr(&s_tot[p * 20 + 18], (unsigned long long)v); }
-                else atomicAdd(&s_tot[p * 20 + f], (unsigned long long)v);
+                if (f == 13) atomicMax(&s_tot[p * kTotFields + 13], (unsigned long long)v);
+                else if (f == 20) { if (v) atomicOr(&s_tot[p * kTotFields + 20], (unsigned long long)v); }
+                else atomicAdd(&s_tot[p * kTotFields + f], (unsigned long long)v);
             }
         }
     }
     __syncthreads();
     if (P.totals && blockIdx.x == 0 && threadIdx.x < P.n_pol && P.est_err && *P.est_err)
-        atomicOr(reinterpret_cast<unsigned long long*>(P.totals + threadIdx.x) + 18, *P.est_err);
+        atomicOr(reinterpret_cast<unsigned long long*>(P.totals + threadIdx.x) + 20, *P.est_err);
     if (P.totals) {
-        for (uint32_t i = threadIdx.x; i < P.n_pol * 20; i += blockDim.x) {
+        for (uint32_t i = threadIdx.x; i < P.n_pol * kTotFields; i += blockDim.x) {
             unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals) + i;
-            const uint32_t f = i % 20;
+            const uint32_t f = i % kTotFields;
             if (f == 13) atomicMax(dst, s_tot[i]);
-            else if (f == 18) { if (s_tot[i]) atomicOr(dst, s_tot[i]); }
-            else if (f < 18) atomicAdd(dst, s_tot[i]);
+            else if (f == 20) { if (s_tot[i]) atomicOr(dst, s_tot[i]); }
+            else if (f < 20) atomicAdd(dst, s_tot[i]);
         }
     }
 }

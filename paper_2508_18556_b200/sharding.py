@@ -8,7 +8,8 @@ totals are bit-identical for any W.
 """
 from __future__ import annotations
 
-MAX_FIELDS = (13, 18)  # makespan_max, error_flags
+N_FIELDS = 24
+MAX_FIELDS = (13, 20)  # makespan_max, error_flags
 
 
 def shard_range(rank: int, world: int, n_per_rank: int = 0, n_total: int = 0):
@@ -21,7 +22,7 @@ def shard_range(rank: int, world: int, n_per_rank: int = 0, n_total: int = 0):
 
 
 def reduce_totals(t64, dist, group=None):
-    """In-place all_reduce of an int64 [n_policies, 20] totals tensor (NCCL over NVLink, or gloo on CPU)."""
+    """In-place all_reduce of an int64 [n_policies, 24] totals tensor (NCCL over NVLink, or gloo on CPU)."""
     mx = t64[:, list(MAX_FIELDS)].clone()
     dist.all_reduce(t64, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)

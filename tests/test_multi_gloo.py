@@ -15,9 +15,9 @@ CFG, N_TOTAL = 3, 64
 
 
 def totals_of(res):
-    """mig_policy_totals layout from per-trace results [n_traces, n_pol]."""
+    """mig_policy_totals layout (24 u64) from per-trace results [n_traces, n_pol]."""
     n_pol = res.shape[1]
-    t = np.zeros((n_pol, 20), np.uint64)
+    t = np.zeros((n_pol, 24), np.uint64)
     for p in range(n_pol):
         r = res[:, p]
         t[p, 0] = len(r)
@@ -30,6 +30,8 @@ def totals_of(res):
         t[p, 15] = r["turnaround_sum"].sum(dtype=np.uint64)
         t[p, 16] = r["busy_slice_ticks"].sum(dtype=np.uint64)
         t[p, 17] = r["decision_hash"].sum(dtype=np.uint64)
+        t[p, 18] = r["mem_mib_ticks"].sum(dtype=np.uint64)
+        t[p, 19] = r["wasted_ticks"].sum(dtype=np.uint64)
     return t
 
 

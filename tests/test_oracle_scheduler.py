@@ -269,3 +269,23 @@ def test_wave_time_closed_form():
     jobs, ext, off = tg.pack_traces([[tg.pack_job(15000, 15000, 1, 0, 100, warps=3000)]])
     r = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, flags=orc.WAVE_TIME, **kw))[0, 0]
     assert int(r["makespan"]) == 200  # tight fit = 3g (fewer compute), two waves
+
+
+def test_memory_utilisation_and_wasted_time():
+    # PAPER.md:675 memory utilisation; one constant 4.7 GB job alone on a 40 GB GPU for the whole run
+    # -> 4.7 / 40 = 0.1175 of the GPU memory
+    g = orc.Geometry(geom_path("a100-40gb"))
+    mib = int(4.7 * 1024)
+    jobs, ext, off = tg.pack_traces([[tg.pack_job(mib, mib, 10, 0, 100)]])
+    r = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, ctx_mib=0, reconfig_ticks=0))[0, 0]
+    assert r["mem_mib_ticks"] / (40960 * r["makespan"]) == pytest.approx(0.1175, abs=2e-4)
+    # example E: wasted run time 420 ticks (OOM at iteration 42) without prediction, 60 with early restart
+    # ("avoids nearly the entire wasted execution span")
+    jobs, ext, off = tg.pack_traces([[dyn_job(1000, 100, 50, 10)]])
+    kw = dict(ctx_mib=0, reconfig_ticks=0)
+    a = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, **kw))[0, 0]
+    b = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, flags=orc.EARLY_RESTART, **kw))[0, 0]
+    assert (int(a["wasted_ticks"]), int(b["wasted_ticks"])) == (420, 60)
+    # memory integral of the dynamic run: sum over iterations of (1000 + 100 i) x 10 ticks
+    assert int(b["mem_mib_ticks"]) == 10 * (sum(1000 + 100 * i for i in range(1, 7)) +
+                                            sum(1000 + 100 * i for i in range(1, 51)))

@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 
 SPECS = [dict(kind=0), dict(kind=1), dict(kind=2), dict(kind=3), dict(kind=3, flags=1), dict(kind=4),
          dict(kind=4, flags=1)]
-ESTIMATE_FIELDS = ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe", "phi", "a", "sigma"]
+ESTIMATE_FIELDS = ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe", "phi", "a", "sigma", "mem_fe",
+                   "mem_conv", "mem_T"]
 
 
 def run_pair(geo, jobs, ext, off, specs, seed=0, common=None, max_jobs=None):
@@ -53,7 +54,8 @@ def check_totals(got, tot):
         t = tot[p]
         assert t["n_traces"] == len(r) and t["error_flags"] == 0
         for f in ["n_jobs", "completed", "rejected", "failed", "ooms", "preempts", "restarts", "placements",
-                  "waits", "creates", "destroys", "energy_wticks", "turnaround_sum", "busy_slice_ticks"]:
+                  "waits", "creates", "destroys", "energy_wticks", "turnaround_sum", "busy_slice_ticks",
+                  "mem_mib_ticks", "wasted_ticks"]:
             assert int(t[f]) == int(r[f].astype(np.uint64).sum()), f
         assert int(t["makespan_sum"]) == int(r["makespan"].astype(np.uint64).sum())
         assert int(t["makespan_max"]) == int(r["makespan"].max(initial=0))
@@ -90,7 +92,7 @@ def test_estimates_match_oracle(cfg, n):
     tr = mig.traces_from_numpy(jobs, ext, off, seed=tg.seed_of(cfg))
     est = mig.estimates_numpy(mig.mig_estimate_memory(g, tr, mig.policy(g)))
     want = orc.estimate(og, jobs, ext, off, orc.policy(), seed=tg.seed_of(cfg))
-    for f in ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe"]:
+    for f in ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe", "mem_fe", "mem_conv", "mem_T"]:
         assert np.array_equal(est[f], want[f]), f
     for f in ["phi", "a", "sigma"]:
         np.testing.assert_allclose(est[f], want[f], rtol=1e-6, atol=1e-9)
@@ -195,7 +197,7 @@ def test_full_size_sampled_parity(cfg, n_full, n_sample):
     torch.cuda.synchronize()
     rng = np.random.default_rng(cfg)
     idx = np.unique(np.concatenate([rng.integers(0, n_full, n_sample), [0, n_full - 1]]))
-    got_all = res.view(-1, len(pols), 80)
+    got_all = res.view(-1, len(pols), 96)
     got = got_all[torch.from_numpy(idx).to(res.device)].cpu().numpy().view(mig.RESULT_DTYPE).reshape(-1, len(pols))
     want = np.zeros((len(idx), len(pols)), orc.RESULT_DTYPE)
     for k, t in enumerate(idx):
