@@ -15,7 +15,7 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream);
+                            cudaStream_t stream, uint32_t* launches);
 }  // namespace mig
 
 namespace {
@@ -116,7 +116,7 @@ mig_status check_policies(const mig_geometry* g, const mig_policy* pols, uint32_
     return MIG_OK;
 }
 
-// Device path shared by mig_simulate and the host pipeline. scratch must hold 3 zeroed u64 counters.
+// Device path shared by mig_simulate and the host pipeline. scratch must hold 4 zeroed u64 counters.
 mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, const mig_traces& tr,
                            const mig_policy* pols, uint32_t n_pol, const mig_job_estimate* est,
                            mig_job_estimate* est_scratch, mig_trace_result* out, mig_policy_totals* totals,
@@ -129,9 +129,11 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
         ++launches;
         est = est_scratch;
     }
-    e = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1, sm_count_of(dev), s);
+    uint32_t nl = 0;
+    e = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1, sm_count_of(dev), s,
+                             &nl);
     if (e != cudaSuccess) return cuda_fail(e, "k_simulate launch");
-    ++launches;
+    launches += nl;
     t_launches += launches;
     return MIG_OK;
 }

@@ -147,7 +147,8 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
         // physical MiB of iteration n and its running sum (R22: requested / inverse reuse, + ws + ctx)
         const uint32_t phys = valid ? (uint32_t)((q_unit ? (uint64_t)y : ((uint64_t)y * 65536ull) / q) + ws_ctx) : 0u;
-        const uint32_t pm = Smem + warp_scan_u32(phys, lane);
+        // running sum of the memory integral: one reduction per chunk, prefixes only where needed
+        auto prefix = [&](uint32_t m) { return Smem + __reduce_add_sync(FULL, lane <= m ? phys : 0u); };
         // first-exceed iteration of every memory level (R12): phys(i) = floor(y*65536/q) + ws + ctx > L.
         // Levels ascend, so fe[l] <= fe[l+1]: only the lowest level not yet crossed needs a ballot per chunk
         // (more when one chunk crosses several levels).
@@ -157,11 +158,14 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
                                                            : (uint64_t)y * 65536ull >= (uint64_t)(th + 1) * q));
             const uint32_t m = __ballot_sync(FULL, over);
             if (!m) break;
-            fe_set(lnext, base + __ffs(m), __shfl_sync(FULL, pm, __ffs(m) - 1));
+            fe_set(lnext, base + __ffs(m), prefix((uint32_t)__ffs(m) - 1u));
             ++lnext;
         }
-        Smem = __shfl_sync(FULL, pm, 31);
-        if (done_pred) continue;
+        const uint32_t Snext = Smem + __reduce_add_sync(FULL, phys);
+        if (done_pred) {
+            Smem = Snext;
+            continue;
+        }
         // exact integer moments at n = base + lane + 1 (inclusive warp scans + carried totals)
         const int64_t yi = y, qi = q, ni = n;
         const int64_t sy = Sy + warp_scan_i64(yi, lane);
@@ -201,10 +205,9 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         const double phs = __shfl_sync(FULL, f.phi, src), ss = __shfl_sync(FULL, f.sigma, src);
         const int64_t nsrc = base + src + 1, sy_s = __shfl_sync(FULL, sy, src), sty_s = __shfl_sync(FULL, sty, src);
         const double as = (cm || (base + 32 >= T && T >= P.min_n)) ? slope_of(nsrc, sy_s, sty_s) : 0.0;
-        const uint32_t pm_src = __shfl_sync(FULL, pm, src);
         if (cm) {
             conv = base + src + 1;
-            mconv = pm_src;
+            mconv = prefix(src);
             pred = (uint32_t)Ps;
             phi = phs;
             a = as;
@@ -224,6 +227,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
             Plast = __shfl_sync(FULL, f.P, 31);
             okprev = M;
         }
+        Smem = Snext;
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
     if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig, mfe, mconv, Smem);

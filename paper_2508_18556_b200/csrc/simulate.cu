@@ -39,7 +39,9 @@ struct SimParams {
     const unsigned long long* est_err;  // error word of k_estimate (merged into the totals)
     uint32_t max_jobs, n_pol, ctx;
     uint32_t ring_cap;  // = max_jobs
-    uint32_t scheme_a;  // some policy is MIG_SCHEME_A: per-trace group lists are staged
+    uint32_t scheme_a;  // this launch runs the MIG_SCHEME_A policies (group lists are staged)
+    uint32_t n_pol_all; // policies of the mig_simulate call (result stride)
+    uint32_t pol_idx[kMaxPolicies];  // caller index of each policy of this launch
     mig_policy pol[kMaxPolicies];
 };
 
@@ -136,37 +138,41 @@ struct JobStore {
         return WIDE ? A[j].w : (gext ? __ldg(&gext[j].y) : 0u);
     }
     __device__ __forceinline__ uint32_t pred(uint32_t j) const { return WIDE ? B[j].x : A[j].z; }
-    // Physical MiB summed over the iterations 1..k a run executed (memory integral): ek = end kind
-    // (0 COMPLETE after T, 1 OOM after fe, 2 PREEMPT after conv). DYNAMIC jobs read the estimator's prefix sums.
-    __device__ __forceinline__ uint64_t mem_sum(uint32_t j, uint32_t lev, uint32_t ek, uint32_t k) const {
-        const uint4 a = A[j];
-        if (((a.x >> 16) & 0xFFu) == kClassDynamic) {
-            const uint32_t* m = reinterpret_cast<const uint32_t*>(gest + j) + 12;  // mem_fe[5], mem_conv, mem_T
-            return __ldg(m + (ek == 1 ? lev : ek == 2 ? 5u : 6u));
-        }
-        return (uint64_t)(WIDE ? B[j].x : a.z) * k;  // constant footprint
+    // Memory integral of a run in MiB x ticks: a constant footprint times the run's duration, or
+    // for a DYNAMIC job (phys == 0) the estimator's prefix sum over the iterations it ran (ek: 0 COMPLETE after T,
+    // 1 OOM after fe, 2 PREEMPT after conv) times the iteration ticks.
+    __device__ __forceinline__ uint64_t run_mem(uint32_t j, uint32_t phys, uint32_t lev, uint32_t ek, uint32_t dur,
+                                                uint32_t ticks) const {
+        if (__builtin_expect(phys != 0u, 1)) return (uint64_t)phys * dur;
+        const uint32_t* m = reinterpret_cast<const uint32_t*>(gest + j) + 12;  // mem_fe[5], mem_conv, mem_T
+        return (uint64_t)__ldg(m + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) * ticks;
     }
     // NARROW only: requeue FIFO as a linked list through the spare high half of A[j].w
     __device__ __forceinline__ uint32_t next(uint32_t j) const { return A[j].w >> 16; }
     __device__ __forceinline__ void set_next(uint32_t j, uint32_t nx) const { A[j].w = (A[j].w & 0xFFFFu) | (nx << 16); }
     // T, ticks, first-exceed iteration of memory level lev, converged forecast (pred, conv; conv = 0 if none)
+    // phys: the constant footprint of a STATIC/MODEL job (0 for DYNAMIC) for the memory integral.
     __device__ __forceinline__ void run_info(const DevGeom& G, uint32_t j, uint32_t lev, uint32_t& T, uint32_t& ticks,
-                                             uint32_t& fe, uint32_t& pred, uint32_t& conv) const {
+                                             uint32_t& fe, uint32_t& pred, uint32_t& conv, uint32_t& phys) const {
         const uint4 a = A[j];
         T = a.x & 0xFFFFu;
         ticks = a.y;
+        const bool dyn = ((a.x >> 16) & 0xFFu) == kClassDynamic;
         if (WIDE) {
             const uint4 b = B[j];
             pred = b.x;
             conv = b.y & 0xFFFFu;
             fe = reinterpret_cast<const uint16_t*>(&B[j])[3 + lev];
+            phys = dyn ? 0u : b.x;
         } else {
             pred = 0;
             conv = 0;
+            phys = a.z;
             fe = (T >= 1 && a.z > G.level_mem[lev]) ? 1u : kNever;  // R12: static jobs OOM at iteration 1
-            if (__builtin_expect(((a.x >> 16) & 0xFFu) == kClassDynamic, 0)) {  // a real branch, not predicated
+            if (__builtin_expect(dyn, 0)) {  // a real branch, not predicated
                 pred = a.z;
                 conv = a.w & 0xFFFFu;
+                phys = 0;
                 fe = __ldg(reinterpret_cast<const unsigned short*>(gest + j) + 6 + lev);
             }
         }
@@ -206,11 +212,11 @@ __device__ __forceinline__ TraceOut baseline_trace(const DevGeom& G, uint32_t n,
         }
         rec(o.hl, o.hh, t, (j << 16) | place_lo);
         o.K0 += 1u;
-        uint32_t T, ticks, fe, pred, conv;
-        J.run_info(G, j, lev, T, ticks, fe, pred, conv);
+        uint32_t T, ticks, fe, pred, conv, phys;
+        J.run_info(G, j, lev, T, ticks, fe, pred, conv, phys);
         const bool oom = fe <= T;  // first exceed of the whole GPU (R12); no early restart on baseline
         const uint32_t end = t + (oom ? fe : T) * ticks;
-        acc_run(o.acc, lane, (uint64_t)comp * (end - t), J.mem_sum(j, lev, oom ? 1u : 0u, oom ? fe : T) * ticks,
+        acc_run(o.acc, lane, (uint64_t)comp * (end - t), J.run_mem(j, phys, lev, oom ? 1u : 0u, end - t, ticks),
                 oom ? end - t : 0u);
         ++qh;
         while (qh < n) {  // the rest of the pass at t: rejections, then the head waits
@@ -291,8 +297,8 @@ __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<G
             rec(o.hl, o.hh, t, (j << 16) | (K_PLACE_GROUP << 12) | (s << 8) | (((si >> 20) & 0xFu) << 4));
             o.K0 += 1u;
             const uint32_t lev = si & 0xFu;
-            uint32_t T, ticks, fe, pred, conv;
-            J.run_info(G, j, lev, T, ticks, fe, pred, conv);
+            uint32_t T, ticks, fe, pred, conv, phys;
+            J.run_info(G, j, lev, T, ticks, fe, pred, conv, phys);
             if (wave) ticks = wave_ticks(G, ticks, J.warps(j), (si >> 20) & 0xFu);
             const uint32_t rs = t < ready ? t + reconfig : t;  // first run on a freshly created slice
             const uint32_t cap_m = G.level_mem[lev];
@@ -316,8 +322,8 @@ __device__ __forceinline__ TraceOut scheme_a_trace(const DevGeom& G, const Grp<G
                 nxt += ns;
             }
             BM |= ((si >> 8) & 0xFFu) << s;
-            acc_run(o.acc, lane, (uint64_t)((si >> 4) & 0xFu) * (end - rs),
-                    J.mem_sum(j, lev, ek, ek == 1 ? fe : ek == 2 ? i_pre : T) * ticks, ek ? end - rs : 0u);
+            acc_run(o.acc, lane, (uint64_t)((si >> 4) & 0xFu) * (end - rs), J.run_mem(j, phys, lev, ek, end - rs, ticks),
+                    ek ? end - rs : 0u);
         }
     };
     auto next_group = [&]() -> bool {  // set_homogeneous_slices(next non-empty group)
@@ -558,8 +564,8 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
                 o.K0 += created ? 0x10001u : 1u;
                 o.K1 += nd;
                 const uint32_t lev = si & 0xFu;
-                uint32_t T, ticks, fe, pred, conv;  // conv = 0 unless a converged DYNAMIC forecast
-                J.run_info(G, j, lev, T, ticks, fe, pred, conv);
+                uint32_t T, ticks, fe, pred, conv, phys;  // conv = 0 unless a converged DYNAMIC forecast
+                J.run_info(G, j, lev, T, ticks, fe, pred, conv, phys);
                 if (wave) ticks = wave_ticks(G, ticks, J.warps(j), (si >> 20) & 0xFu);
                 const uint32_t rs = t + (created ? reconfig : 0u);
                 const uint32_t cap = G.level_mem[lev];
@@ -583,7 +589,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
                 }
                 BM |= ((si >> 8) & 0xFFu) << s;
                 acc_run(o.acc, lane, (uint64_t)((si >> 4) & 0xFu) * (end - rs),
-                        J.mem_sum(j, lev, ek, ek == 1 ? fe : ek == 2 ? i_pre : T) * ticks, ek ? end - rs : 0u);
+                        J.run_mem(j, phys, lev, ek, end - rs, ticks), ek ? end - rs : 0u);
             }
         pop:
             if (qh < n) {
@@ -672,7 +678,7 @@ __device__ __forceinline__ TraceOut simulate_trace(const DevGeom& G, const Grp<G
     return o;
 }
 
-template <int GW, bool WIDE, int WARPS>
+template <int GW, bool WIDE, int WARPS, bool SA>
 __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGeom* __restrict__ Gg, const SimParams P) {
     extern __shared__ __align__(16) uint8_t smem[];
     DevGeom& G = *reinterpret_cast<DevGeom*>(smem);
@@ -784,7 +790,7 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
             g.sync();
             const JobStore<WIDE> J{jobA, jobB, P.jobs + j0, P.ext ? P.ext + j0 : nullptr, P.est + j0, P.ctx};
             TraceOut o;
-            if (kind == MIG_SCHEME_A)
+            if (SA)  // separate instantiation: Scheme A's state does not raise the Scheme B loop's registers
                 o = scheme_a_trace<GW, WIDE>(G, g, n, J, GL, P.max_jobs, er, fold, wave, pol.reconfig_ticks, full_mem);
             else if (kind == MIG_FUSION_FISSION)
                 o = simulate_trace<MIG_FUSION_FISSION, GW, WIDE>(G, g, n, J, ring, P.ring_cap, er, fold, wave,
@@ -816,7 +822,7 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
                 else if (lane == 4) v = make_uint4((uint32_t)busy, (uint32_t)(busy >> 32), o.hl, o.hh);
                 else v = make_uint4((uint32_t)memt, (uint32_t)(memt >> 32), (uint32_t)wasted,
                                     (uint32_t)(wasted >> 32));
-                reinterpret_cast<uint4*>(P.out + tr * P.n_pol + p)[lane] = v;
+                reinterpret_cast<uint4*>(P.out + tr * P.n_pol_all + P.pol_idx[p])[lane] = v;
             }
             // ---- a12: per-policy totals (shared-memory atomics, flushed once per CTA) ----
             for (uint32_t f = lane; f < 21; f += GW) {
@@ -852,11 +858,12 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
     }
     __syncthreads();
     if (P.totals && blockIdx.x == 0 && threadIdx.x < P.n_pol && P.est_err && *P.est_err)
-        atomicOr(reinterpret_cast<unsigned long long*>(P.totals + threadIdx.x) + 20, *P.est_err);
+        atomicOr(reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx[threadIdx.x]) + 20, *P.est_err);
     if (P.totals) {
         for (uint32_t i = threadIdx.x; i < P.n_pol * kTotFields; i += blockDim.x) {
-            unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals) + i;
             const uint32_t f = i % kTotFields;
+            unsigned long long* dst =
+                reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx[i / kTotFields]) + f;
             if (f == 13) atomicMax(dst, s_tot[i]);
             else if (f == 20) { if (s_tot[i]) atomicOr(dst, s_tot[i]); }
             else if (f < 20) atomicAdd(dst, s_tot[i]);
@@ -872,15 +879,16 @@ size_t simulate_smem_bytes(uint32_t max_jobs, int gw, bool wide, bool scheme_a) 
     return kGeomBytes + kPolBytes + kTotBytes + (size_t)(warps_per_cta(wide) * 32 / gw) * per_group;
 }
 
-template <int GW, bool WIDE>
+template <int GW, bool WIDE, bool SA>
 static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n_traces, int sm_count,
                              cudaStream_t stream) {
     constexpr int kW = warps_per_cta(WIDE);
-    const size_t smem = simulate_smem_bytes(P.max_jobs, GW, WIDE, P.scheme_a != 0);
-    cudaError_t e = cudaFuncSetAttribute(k_simulate<GW, WIDE, kW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = simulate_smem_bytes(P.max_jobs, GW, WIDE, SA);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_simulate<GW, WIDE, kW, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate<GW, WIDE, kW>, kW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate<GW, WIDE, kW, SA>, kW * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint64_t groups = (uint64_t)kW * 32 / GW;
@@ -888,7 +896,7 @@ static cudaError_t launch_gw(const DevGeom* Gdev, const SimParams& P, uint64_t n
     uint64_t blocks = (uint64_t)per_sm * sm_count;
     if (want < blocks) blocks = want;
     if (blocks < 1) blocks = 1;
-    k_simulate<GW, WIDE, kW><<<(unsigned)blocks, kW * 32, smem, stream>>>(Gdev, P);
+    k_simulate<GW, WIDE, kW, SA><<<(unsigned)blocks, kW * 32, smem, stream>>>(Gdev, P);
     return cudaGetLastError();
 }
 
@@ -915,10 +923,22 @@ bool simulate_wide_layout(uint32_t max_jobs) {
     return max_jobs <= 32;
 }
 
+template <bool SA>
+static cudaError_t launch_variant(const DevGeom* Gdev, const SimParams& P, const mig_traces& tr, int sm_count,
+                                  cudaStream_t stream) {
+    const bool wide = simulate_wide_layout(tr.max_jobs);
+    if (simulate_group_width(tr.max_jobs, SA) == 8)
+        return wide ? launch_gw<8, true, SA>(Gdev, P, tr.n_traces, sm_count, stream)
+                    : launch_gw<8, false, SA>(Gdev, P, tr.n_traces, sm_count, stream);
+    return wide ? launch_gw<32, true, SA>(Gdev, P, tr.n_traces, sm_count, stream)
+                : launch_gw<32, false, SA>(Gdev, P, tr.n_traces, sm_count, stream);
+}
+
+// counter: two zeroed u64 trace counters (one per launch: Scheme B policies, Scheme A policies).
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, uint32_t* launches) {
     SimParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -932,18 +952,31 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     P.est_err = est_err;
     P.max_jobs = tr.max_jobs;
     P.ring_cap = tr.max_jobs;
-    P.n_pol = n_pol;
+    P.n_pol_all = n_pol;
     P.ctx = pols[0].ctx_mib;
+    SimParams PA = P;  // Scheme A policies
+    P.n_pol = PA.n_pol = 0;
     for (uint32_t i = 0; i < n_pol; ++i) {
-        P.pol[i] = pols[i];
-        if (pols[i].kind == MIG_SCHEME_A) P.scheme_a = 1;
+        SimParams& Q = pols[i].kind == MIG_SCHEME_A ? PA : P;
+        Q.pol_idx[Q.n_pol] = i;
+        Q.pol[Q.n_pol++] = pols[i];
     }
-    const bool wide = simulate_wide_layout(tr.max_jobs);
-    if (simulate_group_width(tr.max_jobs, P.scheme_a != 0) == 8)
-        return wide ? launch_gw<8, true>(Gdev, P, tr.n_traces, sm_count, stream)
-                    : launch_gw<8, false>(Gdev, P, tr.n_traces, sm_count, stream);
-    return wide ? launch_gw<32, true>(Gdev, P, tr.n_traces, sm_count, stream)
-                : launch_gw<32, false>(Gdev, P, tr.n_traces, sm_count, stream);
+    PA.scheme_a = 1;
+    PA.counter = counter + 1;
+    cudaError_t e = cudaSuccess;
+    *launches = 0;
+    if (P.n_pol) {
+        e = launch_variant<false>(Gdev, P, tr, sm_count, stream);
+        if (e != cudaSuccess) return e;
+        ++*launches;
+    }
+    if (PA.n_pol) {
+        if (P.n_pol) PA.est_err = nullptr;  // merged once
+        e = launch_variant<true>(Gdev, PA, tr, sm_count, stream);
+        if (e != cudaSuccess) return e;
+        ++*launches;
+    }
+    return e;
 }
 
 }  // namespace mig
