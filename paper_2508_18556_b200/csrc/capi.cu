@@ -19,6 +19,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
 }  // namespace mig
 
 namespace {
+constexpr size_t kCounterBytes = 16 * sizeof(unsigned long long);
 thread_local std::string t_err;
 thread_local uint32_t t_launches = 0;
 
@@ -116,7 +117,8 @@ mig_status check_policies(const mig_geometry* g, const mig_policy* pols, uint32_
     return MIG_OK;
 }
 
-// Device path shared by mig_simulate and the host pipeline. scratch must hold 4 zeroed u64 counters.
+// Device path shared by mig_simulate and the host pipeline. counters: kCounterBytes of zeroed scratch
+// ([0] estimate, [1] estimate error word, [2..] simulate trace counters).
 mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, const mig_traces& tr,
                            const mig_policy* pols, uint32_t n_pol, const mig_job_estimate* est,
                            mig_job_estimate* est_scratch, mig_trace_result* out, mig_policy_totals* totals,
@@ -242,12 +244,12 @@ mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const m
     if (traces->n_traces == 0) return MIG_OK;
     size_t est_bytes = est ? 0 : traces->n_jobs * sizeof(mig_job_estimate);
     uint8_t* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, 64 + est_bytes, s);
+    cudaError_t e = cudaMallocAsync(&scratch, kCounterBytes + est_bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scratch)");
-    e = cudaMemsetAsync(scratch, 0, 64, s);
+    e = cudaMemsetAsync(scratch, 0, kCounterBytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(scratch)");
     st = simulate_device(g, Gdev, dev, *traces, policies, n_policies, est,
-                         est ? nullptr : reinterpret_cast<mig_job_estimate*>(scratch + 64), out, totals,
+                         est ? nullptr : reinterpret_cast<mig_job_estimate*>(scratch + kCounterBytes), out, totals,
                          reinterpret_cast<unsigned long long*>(scratch), s);
     cudaFreeAsync(scratch, s);
     return st;
@@ -278,7 +280,7 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
     const size_t jb = al(chunk_jobs_cap * 16), eb = T.jobs_ext ? al(chunk_jobs_cap * 16) : 0,
                  ob = al((chunk_traces + 1) * 8), esb = al(chunk_jobs_cap * sizeof(mig_job_estimate)),
                  rb = al(chunk_traces * n_policies * sizeof(mig_trace_result));
-    const size_t per = jb + eb + ob + esb + rb + 64;
+    const size_t per = jb + eb + ob + esb + rb + kCounterBytes;
     cudaStream_t ss[2];
     uint8_t* buf[2] = {nullptr, nullptr};
     std::vector<mig_policy_totals> host_tot(n_chunks * n_policies);
@@ -326,7 +328,7 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
                 e = cudaMemcpyAsync(d_smp, (const uint8_t*)T.samples + slo * 8, (shi - slo) * 8, cudaMemcpyHostToDevice, s);
             if (e == cudaSuccess) e = cudaMemcpyAsync(d_soff, so + jlo, (nj + 1) * 8, cudaMemcpyHostToDevice, s);
         }
-        if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, 64, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, kCounterBytes, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(d_tot, 0, n_policies * sizeof(mig_policy_totals), s);
         if (e != cudaSuccess) {
             st = cuda_fail(e, "host pipeline H2D");

@@ -139,11 +139,11 @@ struct JobStore {
     }
     __device__ __forceinline__ uint32_t pred(uint32_t j) const { return WIDE ? B[j].x : A[j].z; }
     // Memory integral of a run in MiB x ticks: a constant footprint times the run's duration, or
-    // for a DYNAMIC job (phys == 0) the estimator's prefix sum over the iterations it ran (ek: 0 COMPLETE after T,
+    // for a DYNAMIC job the estimator's prefix sum over the iterations it ran (ek: 0 COMPLETE after T,
     // 1 OOM after fe, 2 PREEMPT after conv) times the iteration ticks.
     __device__ __forceinline__ uint64_t run_mem(uint32_t j, uint32_t phys, uint32_t lev, uint32_t ek, uint32_t dur,
                                                 uint32_t ticks) const {
-        if (__builtin_expect(phys != 0u, 1)) return (uint64_t)phys * dur;
+        if (__builtin_expect(((A[j].x >> 16) & 0xFFu) != kClassDynamic, 1)) return (uint64_t)phys * dur;
         const uint32_t* m = reinterpret_cast<const uint32_t*>(gest + j) + 12;  // mem_fe[5], mem_conv, mem_T
         return (uint64_t)__ldg(m + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) * ticks;
     }
@@ -934,7 +934,27 @@ static cudaError_t launch_variant(const DevGeom* Gdev, const SimParams& P, const
                 : launch_gw<32, false, SA>(Gdev, P, tr.n_traces, sm_count, stream);
 }
 
-// counter: two zeroed u64 trace counters (one per launch: Scheme B policies, Scheme A policies).
+uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count);
+uint32_t simulate_lane_threads();
+cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, const mig_policy& pol, uint32_t pol_idx,
+                                 uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
+                                 mig_policy_totals* totals, unsigned long long* counter,
+                                 const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
+                                 cudaStream_t stream);
+
+// Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
+// (8 or 32 lanes per trace).
+bool simulate_use_lane() {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* env = getenv("MIG_LANES_PER_TRACE");
+        forced = env ? atoi(env) : 1;
+    }
+    return forced == 1;
+}
+
+// counter: kSimCounters zeroed u64 trace counters ([0] group kernel Scheme B, [1] group kernel Scheme A,
+// [2 + i] lane kernel, policy i).
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
@@ -965,7 +985,19 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     PA.counter = counter + 1;
     cudaError_t e = cudaSuccess;
     *launches = 0;
-    if (P.n_pol) {
+    if (P.n_pol && simulate_use_lane()) {
+        const uint64_t blocks = simulate_lane_grid(tr.n_traces, sm_count);
+        uint16_t* ring = nullptr;
+        e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * tr.max_jobs * sizeof(uint16_t), stream);
+        if (e != cudaSuccess) return e;
+        for (uint32_t k = 0; k < P.n_pol && e == cudaSuccess; ++k) {
+            e = launch_simulate_lane(Gdev, tr, P.pol[k], P.pol_idx[k], n_pol, est, out, totals, counter + 2 + k,
+                                     est_err, ring, blocks, stream);
+            ++*launches;
+        }
+        cudaFreeAsync(ring, stream);
+        if (e != cudaSuccess) return e;
+    } else if (P.n_pol) {
         e = launch_variant<false>(Gdev, P, tr, sm_count, stream);
         if (e != cudaSuccess) return e;
         ++*launches;

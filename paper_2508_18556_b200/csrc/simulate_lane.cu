@@ -1,0 +1,662 @@
+// simulate_lane.cu — k_simulate_lane: the MIGM scheduler + partition-manager event loop (SURVEY.md §8(a) rows a1,
+// a4-a12) with ONE LANE PER (trace, policy) unit, for the Scheme B family of policies (BASELINE, STATIC, DYNAMIC,
+// FUSION_FISSION, +EARLY_RESTART / WARP_FOLD / WAVE_TIME).
+//
+// Why a lane per trace. A trace is a sequential discrete-event loop whose per-decision work is a handful of bitmask
+// operations; the group kernel (simulate.cu, 8 or 32 lanes per trace) spends most issue slots on work that is
+// uniform across the group. Here every lane runs its own trace, and the whole decision procedure is reduced to
+// O(1) table lookups and bit arithmetic on per-lane registers:
+//   Alg. 2 ...... s_alloc[occupancy][profile]: the argmax-fcr legal start (tie -> highest, R5),
+//                                    evaluated once per CTA from the fcr table of Alg. 1 (the
+//                                    reachability "can be precomputed offline"), so a decision is one LDS
+//   reuse (R7) ....... idle instance starts & a per-profile "tightly fits" mask over the per-slot
+//                                    profile nibbles (<= 7 idle instances, highest start first)
+//   fusion / fission (R8) .......... the instance boundary masks SM/EM, evaluated only when Alg. 2 fails
+//   next event (R28) ............... min over eight end-tick registers; ties by (kind, job) from shared memory
+// The loop is a flat state machine (PASS: one head evaluation; EVT: one event; FIN: write the unit's result and take
+// the next unit), so the 32 lanes of a warp stay in one loop even though their traces are at different points:
+// the cost of an iteration is the sum of the branches present in the warp, not the slowest trace. Units are taken
+// from an atomic counter one ahead (lane-level work stealing); per-policy totals are per-lane shared-memory partials
+// reduced once per CTA.
+//
+// Per-lane state: occupancy occ, instance starts SM / ends EM, busy starts BS / busy slots BM (u8 masks), profile
+// nibble per start slot (prof4), end tick per start slot (endt[8], registers), job|kind per slot (shared memory),
+// the head job's record (prefetched when the queue advances), a requeue FIFO in global scratch (rare: OOM /
+// preempt restarts, R13), packed 16-bit counters, FNV-1a-64 hash halves, four u64 accumulators.
+//
+// The record stream, counters and accumulators are exactly those of the group kernel and the oracle (DESIGN.md
+// "Decision record"), so results are bit-identical (tests/test_kernel_variants_gpu.py, MIG_LANES_PER_TRACE=1).
+#include <stdlib.h>
+#include <string.h>
+
+#include "device_common.cuh"
+
+namespace mig {
+
+struct LaneParams {
+    const uint4* jobs;
+    const uint4* ext;
+    const uint64_t* off;
+    const mig_job_estimate* est;
+    uint64_t n_traces;
+    mig_trace_result* out;
+    mig_policy_totals* totals;
+    unsigned long long* counter;
+    const unsigned long long* est_err;  // error word of k_estimate (merged into this policy's totals)
+    uint16_t* ring;                     // [grid threads][ring_cap] requeue FIFOs: job | need << 10 (15 = none)
+    uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
+    mig_policy pol;
+};
+
+constexpr int kLaneThreads = 128;
+constexpr int kLaneMinBlocks = 6;
+constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
+constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
+
+// mig_policy_totals fields accumulated per lane: 32-bit counts (index -> totals field) and 64-bit sums.
+constexpr int kT32 = 14, kT64 = 7;
+__constant__ const uint8_t kF32[kT32] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 20};
+__constant__ const uint8_t kF64[kT64] = {12, 14, 15, 16, 17, 18, 19};
+
+struct LaneShared {
+    DevGeom G;
+    uint8_t alloc[256 * 16];  // Alg. 2 result by (occupancy, profile): start, or 0xFF = FAIL
+    uint16_t reuse_ok[16];    // FF: profiles q whose idle instance tightly fits profile p (same memory, compute >=)
+    uint8_t scand[16];        // STATIC: layout starts whose slice can hold profile p
+    uint8_t lvl_first[8];     // first profile of each memory level ([n_levels] = 0xFF)
+    uint32_t jk[8][kLaneThreads];  // per lane and start slot: job | end kind << 16 of the running job
+    // per-lane partial totals (no atomics: 64-bit shared atomics are CAS loops), reduced once per CTA
+    uint32_t c32[kT32][kLaneThreads];
+    unsigned long long c64[kT64][kLaneThreads];
+};
+
+// FNV-1a-64 step on the two 32-bit halves of h (same as simulate.cu).
+__device__ __forceinline__ void lrec(uint32_t& hl, uint32_t& hh, uint32_t tick, uint32_t lo) {
+    const uint32_t x = hl ^ lo, y = hh ^ tick;
+    const uint64_t p = (uint64_t)x * 0x1b3u;
+    hl = (uint32_t)p;
+    hh = (uint32_t)(p >> 32) + y * 0x1b3u + (x << 8);
+}
+
+// Tight fit (R6, R30): the smallest-memory profile holding req (ties -> fewer compute
+// slices; profiles are sorted by (memory, compute)), with warp folding the same wave count as the whole GPU.
+__device__ __forceinline__ uint32_t lane_tight_fit(const LaneShared& S, uint32_t req, uint32_t warps, bool fold) {
+    const DevGeom& G = S.G;
+    if (!fold || warps == 0) {
+        uint32_t L = 0;
+#pragma unroll
+        for (int l = 0; l < kMaxLevels; ++l) L += ((uint32_t)l < G.n_levels && G.level_mem[l] < req) ? 1u : 0u;
+        return S.lvl_first[L];
+    }
+    const uint32_t cf = G.wave_cap[G.full_prof];
+    for (uint32_t p = 0; p < G.n_prof; ++p) {
+        if (G.mem[p] < req) continue;
+        const uint32_t cp = G.wave_cap[p];
+        if ((warps + cp - 1) / cp != (warps + cf - 1) / cf) continue;
+        return p;
+    }
+    return kNoNeed;
+}
+
+__device__ __forceinline__ uint32_t lane_wave_ticks(const DevGeom& G, uint32_t ticks, uint32_t warps, uint32_t prof) {
+    if (warps == 0) return ticks;
+    const uint32_t cp = G.wave_cap[prof], cf = G.wave_cap[G.full_prof];
+    const uint32_t wp = (warps + cp - 1) / cp, wf = (warps + cf - 1) / cf;
+    return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
+}
+
+__device__ __forceinline__ uint32_t lane_overlap_extent(uint32_t occ, uint32_t SM, uint32_t EM, uint32_t lo,
+                                                        uint32_t hi) {
+    const uint32_t a = ((occ >> lo) & 1u) ? 31u - __clz(SM & ((2u << lo) - 1u)) : lo;
+    const uint32_t b = ((occ >> hi) & 1u) ? (uint32_t)__ffs(EM & ~((1u << hi) - 1u)) - 1u : hi;
+    return occ & ((2u << b) - 1u) & ~((1u << a) - 1u);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
+    k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
+    __shared__ __align__(16) LaneShared S;
+    const uint32_t tid = threadIdx.x;
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&S.G);
+        for (uint32_t i = tid; i < sizeof(DevGeom) / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+#pragma unroll
+        for (int f = 0; f < kT32; ++f) S.c32[f][tid] = 0;
+#pragma unroll
+        for (int f = 0; f < kT64; ++f) S.c64[f][tid] = 0;
+    }
+    __syncthreads();
+    {
+        const DevGeom& G = S.G;
+        for (uint32_t i = tid; i < 256 * 16; i += blockDim.x) {  // Alg. 2 for every (occupancy, profile)
+            const uint32_t occ = i >> 4, p = i & 15u;
+            uint32_t best = 0;
+            if (p < G.n_prof && occ < (1u << G.n_slots)) {
+                for (uint32_t k = 0; k < G.n_place[p]; ++k) {
+                    const uint32_t pl = G.place[p][k], qm = pl >> 8;
+                    const uint32_t score = (pl && !(occ & qm)) ? ((uint32_t)G.fcr[occ | qm] << 8) | (pl & 0xFFu) : 0u;
+                    best = max(best, score);
+                }
+            }
+            S.alloc[i] = best ? (uint8_t)(best & 0xFFu) : (uint8_t)0xFFu;
+        }
+        if (tid < 16) {
+            uint32_t ok = 0, sc = 0;
+            if (tid < G.n_prof) {
+                for (uint32_t q = 0; q < G.n_prof; ++q)
+                    if (G.level[q] == G.level[tid] && G.comp[q] >= G.comp[tid]) ok |= 1u << q;
+                for (uint32_t i = 0; i < G.n_layout; ++i) {
+                    const uint32_t lp = G.layout_prof[i];
+                    if (G.level[lp] >= G.level[tid] && G.comp[lp] >= G.comp[tid]) sc |= 1u << G.layout_start[i];
+                }
+            }
+            S.reuse_ok[tid] = (uint16_t)ok;
+            S.scand[tid] = (uint8_t)sc;
+        }
+        if (tid < 8) {
+            uint32_t f = 0xFFu;
+            for (uint32_t p = G.n_prof; p-- > 0;)
+                if (G.level[p] == tid) f = p;
+            S.lvl_first[tid] = (uint8_t)(tid < G.n_levels ? f : 0xFFu);
+        }
+    }
+    __syncthreads();
+    const DevGeom& G = S.G;
+
+    const mig_policy& pol = P.pol;
+    const bool fold = (pol.flags & MIG_WARP_FOLD) != 0;
+    const bool er = (pol.flags & MIG_EARLY_RESTART) != 0;
+    const bool wave = (pol.flags & MIG_WAVE_TIME) != 0;
+    const uint32_t reconfig = pol.reconfig_ticks, full_mem = G.full_mem;
+    const uint64_t jbase = P.off[0];
+    uint16_t* ring = P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap;
+    uint32_t* jk = &S.jk[0][tid];
+    const uint32_t fp = G.full_prof;
+
+    // ---- unit state ----
+    unsigned long long tr = atomicAdd(P.counter, 1ull);
+    unsigned long long tr_next = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
+    uint64_t j0 = 0;
+    uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
+    uint32_t occ = 0, SM = 0, EM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0;
+    uint32_t endt[8];
+    uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
+    uint64_t a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
+    uint32_t hj = kNoJob, hneed = kUnk;  // head job and its tight fit (kUnk: not yet computed)
+    uint4 hr = make_uint4(0, 0, 0, 0), he = make_uint4(0, 0, 0, 0);
+    // BASELINE only: the running job (one at a time on the whole GPU)
+    uint32_t bjob = 0, bend = 0;
+    bool bbusy = false, boom = false;
+
+    auto fetch_head = [&]() {  // queue = jobs[qh..n) ++ requeue FIFO
+        if (qh < n) {
+            hj = qh;
+            hneed = kUnk;
+        } else if (KIND != MIG_BASELINE && rn) {
+            const uint32_t v = ring[rh];
+            hj = v & 0x3FFu;
+            hneed = v >> 10;
+            if (hneed == 15u) hneed = kNoNeed;
+        } else {
+            hj = kNoJob;
+            return;
+        }
+        hr = __ldg(P.jobs + j0 + hj);
+        he = P.ext ? __ldg(P.ext + j0 + hj) : make_uint4(0, 0, 0, 0);
+    };
+    auto init_unit = [&]() {
+        const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
+        j0 = o0 - jbase;
+        const uint64_t n64 = o1 - o0;
+        err = 0;
+        n = (uint32_t)n64;
+        if (n64 > P.max_jobs) {
+            err = (uint32_t)MIG_ERR_TRACE_TOO_LONG;
+            n = 0;
+        }
+        t = qh = rh = rn = evm = 0;
+        BS = BM = 0;
+        occ = SM = EM = prof4 = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) endt[k] = kNoEnd;
+        if (KIND == MIG_STATIC) {
+            for (uint32_t i = 0; i < G.n_layout; ++i) {
+                const uint32_t p = G.layout_prof[i], s = G.layout_start[i];
+                SM |= 1u << s;
+                prof4 |= p << (4 * s);
+                occ |= G.lenmask[p] << s;
+            }
+        }
+        K0 = K1 = K2 = K3 = 0;
+        a_turn = a_busy = a_mem = a_waste = 0;
+        hl = (uint32_t)kFnvOffset;
+        hh = (uint32_t)(kFnvOffset >> 32);
+        bbusy = false;
+        mode = 0;
+        fetch_head();
+    };
+    auto pop = [&]() {
+        if (qh < n) {
+            ++qh;
+        } else {
+            rh = rh + 1 == P.ring_cap ? 0u : rh + 1u;
+            --rn;
+        }
+        fetch_head();
+    };
+    // Start a run of job j (record hr/he) on the instance at slot s of profile pr: end tick and
+    // kind (OOM > COMPLETE > PREEMPT in one iteration, R29; early restart R25), power, memory integral, waste.
+    auto start_run = [&](uint32_t j, uint32_t s, uint32_t pr, uint32_t rs, uint32_t& end, uint32_t& ek) {
+        const uint32_t si = G.pinfo[pr];
+        const uint32_t lev = si & 0xFu, comp = (si >> 4) & 0xFu;
+        const uint32_t T = hr.z & 0xFFFFu;
+        uint32_t ticks = hr.w;
+        const bool dyn = ((hr.z >> 16) & 0xFFu) == kClassDynamic;
+        uint32_t fe, pred = 0, conv = 0, phys = 0;
+        const mig_job_estimate* ej = P.est + j0 + j;
+        if (__builtin_expect(dyn, 0)) {
+            const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(ej));
+            pred = e0.y;
+            conv = e0.z & 0xFFFFu;
+            fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
+        } else {
+            const uint64_t phys64 = (uint64_t)hr.y + he.x + P.ctx;
+            phys = phys64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)phys64;
+            fe = (T >= 1 && phys > G.level_mem[lev]) ? 1u : kNever;  // R12: static jobs OOM at iteration 1
+        }
+        if (KIND != MIG_BASELINE && wave) ticks = lane_wave_ticks(G, ticks, he.y, pr);
+        const uint32_t cap = G.level_mem[lev];
+        uint32_t i_pre = 0xFFFFFFFFu;
+        if (KIND != MIG_BASELINE && er && conv > 0 && pred > cap && cap < full_mem) i_pre = conv;
+        if (fe <= min(T, i_pre)) {
+            ek = 1;
+            end = rs + fe * ticks;
+        } else if (i_pre < T) {
+            ek = 2;
+            end = rs + i_pre * ticks;
+        } else {
+            ek = 0;
+            end = rs + T * ticks;
+        }
+        const uint32_t dur = end - rs;
+        a_busy += (uint64_t)comp * dur;
+        if (__builtin_expect(dyn, 0)) {
+            const uint32_t* m = reinterpret_cast<const uint32_t*>(ej) + 12;  // mem_fe[5], mem_conv, mem_T
+            a_mem += (uint64_t)__ldg(m + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) * ticks;
+        } else {
+            a_mem += (uint64_t)phys * dur;
+        }
+        if (ek) a_waste += dur;
+    };
+    auto head_need = [&]() {  // first evaluation of an initial queue entry: tight fit of req0 + record checks
+        if (hneed == kUnk) {
+            const uint32_t cls = (hr.z >> 16) & 0xFFu, T = hr.z & 0xFFFFu;
+            if (cls > 2 || T > 4096 || (hr.z >> 24) != 0) err |= (uint32_t)MIG_ERR_BAD_RECORD;
+            const uint32_t req0 = cls == kClassDynamic ? G.mem[0] : hr.x + he.x + P.ctx;  // R16 / est + ws + ctx
+            hneed = lane_tight_fit(S, req0, he.y, fold);
+        }
+        return hneed;
+    };
+
+    bool active = tr < P.n_traces;
+    if (active) init_unit();
+    while (active) {
+        if constexpr (KIND == MIG_BASELINE) {
+            // ---- BASELINE: one job at a time on the whole GPU, queue order ----
+            if (mode == 0) {
+                bool ev = false;
+                if (hj == kNoJob) {  // queue drained: the last run's end, then the unit is done
+                    ev = bbusy;
+                    mode = 2;
+                } else {
+                    const uint32_t j = hj, need = head_need();
+                    if (need == kNoNeed) {
+                        lrec(hl, hh, t, (j << 16) | (K_REJECT << 12) | 0xFF0u);
+                        K2 += 1u;
+                        pop();
+                    } else if (bbusy) {  // the head waits for the running job
+                        lrec(hl, hh, t, (j << 16) | (K_WAIT << 12) | 0xF00u | (need << 4));
+                        K1 += 1u << 16;
+                        ev = true;
+                    } else {
+                        lrec(hl, hh, t, (j << 16) | (K_PLACE_BASELINE << 12) | (fp << 4));
+                        K0 += 1u;
+                        uint32_t end, ek;
+                        start_run(j, 0, fp, t, end, ek);
+                        bjob = j;
+                        bend = end;
+                        boom = ek == 1;
+                        bbusy = true;
+                        pop();
+                    }
+                }
+                if (ev) {  // the run's end event: COMPLETE, or OOM on the whole GPU = FAILED
+                    t = bend;
+                    const uint32_t lo = (bjob << 16) | (fp << 4);
+                    if (boom) {
+                        lrec(hl, hh, t, lo | (K_OOM << 12));
+                        lrec(hl, hh, t, lo | (K_FAILED << 12));
+                        K2 += 1u << 16;
+                        K3 += 1u << 16;
+                    } else {
+                        lrec(hl, hh, t, lo | (K_COMPLETE << 12));
+                        a_turn += t;
+                    }
+                    bbusy = false;
+                }
+            }
+        } else {
+            // ---- PASS: evaluate the head of the queue (Alg. 4, one decision) ----
+            if (mode == 0) {
+                if (hj == kNoJob) {
+                    mode = 1;
+                } else {
+                    const uint32_t j = hj, need = head_need(), jsh = j << 16;
+                    bool popit = true;
+                    if (need == kNoNeed) {  // no profile can ever hold the job: REJECT
+                        lrec(hl, hh, t, jsh | (K_REJECT << 12) | 0xFF0u);
+                        K2 += 1u;
+                    } else {
+                        const uint32_t pn = G.pinfo[need];
+                        uint32_t s = 0, kd = 0, nd = 0, pr = need;
+                        bool created = false;
+                        if (KIND == MIG_STATIC) {  // smallest idle fitting layout slice, tie -> highest start (R11)
+                            const uint32_t cand = S.scand[need];
+                            uint32_t m = cand & ~BS, bk = 0;
+                            while (m) {
+                                const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                                m &= m - 1u;
+                                const uint32_t il = G.pinfo[(prof4 >> (4 * k)) & 0xFu] & 0xFu;
+                                bk = max(bk, (((15u - il) << 5) | k) + 1u);
+                            }
+                            if (bk) {
+                                s = (bk - 1u) & 31u;
+                                pr = (prof4 >> (4 * s)) & 0xFu;
+                                kd = K_PLACE_STATIC;
+                            } else if (cand) {
+                                lrec(hl, hh, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                                K1 += 1u << 16;
+                                popit = false;
+                                mode = 1;
+                            } else {
+                                lrec(hl, hh, t, jsh | (K_REJECT << 12) | 0xF00u | (need << 4));
+                                K2 += 1u;
+                            }
+                        } else {
+                            if (KIND == MIG_FUSION_FISSION) {  // an idle slice that tightly fits (R7)
+                                uint32_t m = SM & ~BS;
+                                const uint32_t ok = S.reuse_ok[need];
+                                while (m) {
+                                    const uint32_t k = 31u - __clz(m);
+                                    if ((ok >> ((prof4 >> (4 * k)) & 0xFu)) & 1u) {
+                                        s = k;
+                                        pr = (prof4 >> (4 * k)) & 0xFu;
+                                        kd = K_REUSE;
+                                        break;
+                                    }
+                                    m &= ~(1u << k);
+                                }
+                            }
+                            if (!kd) {
+                                const uint32_t a = S.alloc[(occ << 4) | need];  // Alg. 2
+                                const uint32_t nlen = (pn >> 16) & 0xFu;
+                                if (a != 0xFFu) {
+                                    s = a;
+                                    kd = K_ALLOC;
+                                } else if (KIND == MIG_FUSION_FISSION && (SM & ~BS)) {
+                                    // fusion / fission: destroy the idle instances a placement overlaps (none busy,
+                                    // >= 1), best (fcr(result), -#destroyed, start) (R8)
+                                    uint32_t bs = 0;
+                                    for (uint32_t k = 0; k < G.n_place[need]; ++k) {
+                                        const uint32_t pl = G.place[need][k], qm = pl >> 8;
+                                        if (!(qm & BM) && (qm & occ)) {
+                                            const uint32_t lo = pl & 0xFFu;
+                                            const uint32_t rm = lane_overlap_extent(occ, SM, EM, lo, lo + nlen - 1u);
+                                            bs = max(bs, ((uint32_t)G.fcr[(occ & ~rm) | qm] << 16) |
+                                                             ((15u - __popc(SM & rm)) << 8) | lo);
+                                        }
+                                    }
+                                    if (bs) {
+                                        s = bs & 0xFFu;
+                                        nd = 15u - ((bs >> 8) & 0xFFu);
+                                        const uint32_t rm = lane_overlap_extent(occ, SM, EM, s, s + nlen - 1u);
+                                        occ &= ~rm;
+                                        SM &= ~rm;
+                                        EM &= ~rm;
+                                        kd = K_RECONF;
+                                    }
+                                }
+                                if (!kd) {  // sleep() until a running job finishes
+                                    lrec(hl, hh, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
+                                    K1 += 1u << 16;
+                                    popit = false;
+                                    mode = 1;
+                                } else {  // create the instance (try_new_mig_slice)
+                                    created = true;
+                                    occ |= ((pn >> 8) & 0xFFu) << s;
+                                    if (KIND == MIG_FUSION_FISSION) {
+                                        SM |= 1u << s;
+                                        EM |= 1u << (s + nlen - 1u);
+                                    }
+                                    prof4 = (prof4 & ~(0xFu << (4 * s))) | (need << (4 * s));
+                                }
+                            }
+                        }
+                        if (kd) {  // the decision record, then start the run
+                            lrec(hl, hh, t, jsh | (kd << 12) | (s << 8) | (pr << 4) | nd);
+                            K0 += created ? 0x10001u : 1u;
+                            K1 += nd;
+                            uint32_t end, ek;
+                            start_run(j, s, pr, t + (created ? reconfig : 0u), end, ek);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k)
+                                if ((uint32_t)k == s) endt[k] = end;
+                            jk[s * kLaneThreads] = j | (ek << 16);
+                            BS |= 1u << s;
+                            BM |= ((G.pinfo[pr] >> 8) & 0xFFu) << s;
+                        }
+                    }
+                    if (popit) pop();
+                }
+            }
+            // ---- EVT: apply one event (min end tick; ties COMPLETE < OOM < PREEMPT, then job id, R28) ----
+            if (mode == 1) {
+                if (!evm) {
+                    uint32_t tn = endt[0];
+#pragma unroll
+                    for (int k = 1; k < 8; ++k) tn = min(tn, endt[k]);
+                    if (tn == kNoEnd) {
+                        mode = 2;
+                    } else {
+                        t = tn;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) evm |= (endt[k] == tn ? 1u : 0u) << k;
+                    }
+                }
+                if (evm) {
+                    uint32_t s = (uint32_t)__ffs(evm) - 1u;
+                    uint32_t v = jk[s * kLaneThreads];
+                    if (evm & (evm - 1u)) {
+                        uint32_t m = evm & (evm - 1u);
+                        while (m) {
+                            const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                            m &= m - 1u;
+                            const uint32_t w = jk[k * kLaneThreads];
+                            if (w < v) {
+                                v = w;
+                                s = k;
+                            }
+                        }
+                    }
+                    evm &= ~(1u << s);
+                    const uint32_t job = v & 0xFFFFu, ek = v >> 16;
+                    const uint32_t pr = (prof4 >> (4 * s)) & 0xFu, si = G.pinfo[pr];
+                    const uint32_t lo = (job << 16) | (s << 8) | (pr << 4);
+                    uint32_t req = 0;
+                    if (ek == 0) {
+                        lrec(hl, hh, t, lo | (K_COMPLETE << 12));
+                        a_turn += t;
+                    } else if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
+                        lrec(hl, hh, t, lo | (K_OOM << 12));
+                        const uint32_t nl = G.level_next[si & 0xFu];
+                        K2 += 1u << 16;
+                        if (nl == 0) {
+                            lrec(hl, hh, t, lo | (K_FAILED << 12));
+                            K3 += 1u << 16;
+                        } else {
+                            req = nl;
+                        }
+                    } else {  // PREEMPT: restart on the slice meeting the forecast (R25)
+                        lrec(hl, hh, t, lo | (K_PREEMPT << 12));
+                        K3 += 1u;
+                        req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
+                    }
+                    if (req) {  // back to the queue tail (R13) with the new tight fit
+                        const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
+                        const uint32_t nn = lane_tight_fit(S, req, w, fold);
+                        uint32_t pos = rh + rn;
+                        if (pos >= P.ring_cap) pos -= P.ring_cap;
+                        ring[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
+                        ++rn;
+                        if (hj == kNoJob) fetch_head();
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if ((uint32_t)k == s) endt[k] = kNoEnd;
+                    const uint32_t ext = ((si >> 8) & 0xFFu) << s;
+                    BS &= ~(1u << s);
+                    BM &= ~ext;
+                    if (KIND == MIG_DYNAMIC) {  // free on completion (R10)
+                        occ &= ~ext;
+                        K1 += 1u;
+                    }
+                    if (!evm) mode = 0;
+                }
+            }
+        }
+        // ---- FIN: the unit's result (96 B) and totals; take the next unit ----
+        if (mode == 2) {
+            const uint32_t placements = K0 & 0xFFFFu, creates = K0 >> 16, destroys = K1 & 0xFFFFu, waits = K1 >> 16,
+                           rejected = K2 & 0xFFFFu, ooms = K2 >> 16, preempts = K3 & 0xFFFFu, failed = K3 >> 16;
+            const uint32_t completed = n - rejected - failed, restarts = ooms - failed + preempts;
+            const uint32_t makespan = t;
+            const uint64_t energy = (uint64_t)pol.idle_w * makespan + (uint64_t)pol.w_per_slice * a_busy;
+            if (P.out) {
+                uint4* o = reinterpret_cast<uint4*>(P.out + tr * P.n_pol_all + P.pol_idx);
+                o[0] = make_uint4(makespan, n, completed, rejected);
+                o[1] = make_uint4(failed, ooms, preempts, restarts);
+                o[2] = make_uint4(placements, waits, creates, destroys);
+                o[3] = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)a_turn,
+                                  (uint32_t)(a_turn >> 32));
+                o[4] = make_uint4((uint32_t)a_busy, (uint32_t)(a_busy >> 32), hl, hh);
+                o[5] = make_uint4((uint32_t)a_mem, (uint32_t)(a_mem >> 32), (uint32_t)a_waste,
+                                  (uint32_t)(a_waste >> 32));
+            }
+            {  // a12: per-lane partial totals (slots of this lane only)
+                uint32_t* c = &S.c32[0][tid];
+                c[0 * kLaneThreads] += 1u;
+                c[1 * kLaneThreads] += n;
+                c[2 * kLaneThreads] += completed;
+                c[3 * kLaneThreads] += rejected;
+                c[4 * kLaneThreads] += failed;
+                c[5 * kLaneThreads] += ooms;
+                c[6 * kLaneThreads] += preempts;
+                c[7 * kLaneThreads] += restarts;
+                c[8 * kLaneThreads] += placements;
+                c[9 * kLaneThreads] += waits;
+                c[10 * kLaneThreads] += creates;
+                c[11 * kLaneThreads] += destroys;
+                c[12 * kLaneThreads] = max(c[12 * kLaneThreads], makespan);
+                c[13 * kLaneThreads] |= err;
+                unsigned long long* d = &S.c64[0][tid];
+                d[0 * kLaneThreads] += makespan;
+                d[1 * kLaneThreads] += energy;
+                d[2 * kLaneThreads] += a_turn;
+                d[3 * kLaneThreads] += a_busy;
+                d[4 * kLaneThreads] += ((unsigned long long)hh << 32) | hl;
+                d[5 * kLaneThreads] += a_mem;
+                d[6 * kLaneThreads] += a_waste;
+            }
+            tr = tr_next;
+            if (tr < P.n_traces) {
+                tr_next = atomicAdd(P.counter, 1ull);
+                init_unit();
+            } else {
+                active = false;
+            }
+        }
+    }
+    __syncthreads();
+    if (P.totals) {
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);
+        if (tid == 0 && blockIdx.x == 0 && P.est_err && *P.est_err) atomicOr(dst + 20, *P.est_err);
+        if (tid < kT32 + kT64) {  // one thread per field reduces the CTA's lanes
+            unsigned long long v = 0;
+            if (tid < kT32) {
+                for (int k = 0; k < kLaneThreads; ++k) {
+                    const uint32_t x = S.c32[tid][k];
+                    v = tid == 12 ? max(v, (unsigned long long)x) : tid == 13 ? (v | x) : v + x;
+                }
+            } else {
+                for (int k = 0; k < kLaneThreads; ++k) v += S.c64[tid - kT32][k];
+            }
+            const uint32_t f = tid < kT32 ? kF32[tid] : kF64[tid - kT32];
+            if (v) {
+                if (f == 13) atomicMax(dst + 13, v);
+                else if (f == 20) atomicOr(dst + 20, v);
+                else atomicAdd(dst + f, v);
+            }
+        }
+    }
+}
+
+// Grid: resident CTAs per SM x SMs (persistent; units are taken from the counter), capped by the unit count.
+uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate_lane<MIG_FUSION_FISSION>, kLaneThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t blocks = (uint64_t)per_sm * sm_count;
+    const uint64_t want = (n_traces + kLaneThreads - 1) / kLaneThreads;
+    if (want < blocks) blocks = want;
+    return blocks < 1 ? 1 : blocks;
+}
+
+uint32_t simulate_lane_threads() { return kLaneThreads; }
+
+// One launch per policy. counter: a zeroed u64; ring: blocks * kLaneThreads * max_jobs u16 of scratch.
+cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, const mig_policy& pol, uint32_t pol_idx,
+                                 uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
+                                 mig_policy_totals* totals, unsigned long long* counter,
+                                 const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
+                                 cudaStream_t stream) {
+    LaneParams P;
+    memset(&P, 0, sizeof(P));
+    P.jobs = (const uint4*)tr.jobs;
+    P.ext = (const uint4*)tr.jobs_ext;
+    P.off = tr.trace_off;
+    P.est = est;
+    P.n_traces = tr.n_traces;
+    P.out = out;
+    P.totals = totals;
+    P.counter = counter;
+    P.est_err = est_err;
+    P.ring = ring;
+    P.ring_cap = tr.max_jobs;
+    P.max_jobs = tr.max_jobs;
+    P.ctx = pol.ctx_mib;
+    P.n_pol_all = n_pol_all;
+    P.pol_idx = pol_idx;
+    P.pol = pol;
+    const dim3 grid((unsigned)blocks), block(kLaneThreads);
+    switch (pol.kind) {
+        case MIG_BASELINE: k_simulate_lane<MIG_BASELINE><<<grid, block, 0, stream>>>(Gdev, P); break;
+        case MIG_STATIC: k_simulate_lane<MIG_STATIC><<<grid, block, 0, stream>>>(Gdev, P); break;
+        case MIG_DYNAMIC: k_simulate_lane<MIG_DYNAMIC><<<grid, block, 0, stream>>>(Gdev, P); break;
+        case MIG_FUSION_FISSION: k_simulate_lane<MIG_FUSION_FISSION><<<grid, block, 0, stream>>>(Gdev, P); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace mig

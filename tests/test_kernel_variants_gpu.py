@@ -1,5 +1,5 @@
-"""Every k_simulate variant (lanes per trace 8 | 32, job staging layout wide | narrow) is parity-checked against
-the oracle. The variant is chosen per process from MIG_LANES_PER_TRACE / MIG_JOB_LAYOUT, so each runs in a
+"""Every k_simulate variant (one lane per trace: k_simulate_lane; or a group of 8 | 32 lanes per trace with job
+staging layout wide | narrow) is parity-checked against the oracle. The variant is chosen per process from MIG_LANES_PER_TRACE / MIG_JOB_LAYOUT, so each runs in a
 subprocess."""
 import os
 import subprocess
@@ -34,8 +34,8 @@ print("variant OK")
 '''
 
 
-@pytest.mark.parametrize("lanes", ["8", "32"])
-@pytest.mark.parametrize("layout", ["wide", "narrow"])
+@pytest.mark.parametrize("lanes,layout", [("1", "narrow"), ("8", "wide"), ("8", "narrow"), ("32", "wide"),
+                                          ("32", "narrow")])
 def test_variant_parity(lanes, layout):
     env = dict(os.environ, MIG_LANES_PER_TRACE=lanes, MIG_JOB_LAYOUT=layout)
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
