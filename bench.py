@@ -234,7 +234,6 @@ def run_mine(args):
     jobs, ext, off = tg.generate_device(cfg, n_per, trace_id0=t_id0, seed=seed, device=dev)
     J = tg.jobs_per_trace(cfg)
     tr = mig.Traces(jobs, ext, off, n_per, seed=seed, trace_id0=t_id0, max_jobs=J)
-    est = torch.empty((tr.n_jobs, 80), dtype=torch.uint8, device=dev)
     res = torch.empty((n_per * n_pol, 96), dtype=torch.uint8, device=dev)
     tot = torch.empty((n_pol, 192), dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
@@ -242,18 +241,12 @@ def run_mine(args):
 
     launches = 0
 
-    def step(ev=None):
+    def step():
+        # one call = the whole hot path: k_estimate (a3 for DYNAMIC jobs; a2 is fused into k_simulate's head
+        # evaluation) + k_simulate (a4-a12), per-trace results and per-policy totals in HBM
         nonlocal launches
-        if ev is not None:
-            ev[0].record(stream)
-        mig.mig_estimate_memory(g, tr, pols[0], out=est, stream=stream)
+        mig.mig_simulate(g, tr, pols, est=None, out=res, totals=tot, stream=stream)
         launches += mig.mig_last_launch_count()
-        if ev is not None:
-            ev[1].record(stream)
-        mig.mig_simulate(g, tr, pols, est=est, out=res, totals=tot, stream=stream)
-        launches += mig.mig_last_launch_count()
-        if ev is not None:
-            ev[2].record(stream)
         if world > 1:  # the per-policy metric reduce over NVLink (NCCL)
             reduce_totals(tot.view(torch.int64).view(n_pol, 24), dist)
 
@@ -266,24 +259,26 @@ def run_mine(args):
     launches = 0
     clocks = ClockSampler(local)
     clocks.start()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    mig.mig_timing_enable(True)  # CUDA events around each kernel group, on the launching stream
     t_start.record(stream)
     for k in range(args.steps):
-        step(evs[k])
+        step()
     t_end.record(stream)
     torch.cuda.synchronize()
+    ktimes = mig.mig_timing_query()
+    mig.mig_timing_enable(False)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     log(f"timed {args.steps} steps: {t_start.elapsed_time(t_end):.1f} ms")
     elapsed_ms = t_start.elapsed_time(t_end)
-    est_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    sim_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    est_ms = ktimes.get("k_estimate", (0.0, 0))[0] / args.steps
+    sim_ms = ktimes.get("k_simulate", (0.0, 0))[0] / args.steps
     if world > 1:
         m = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)

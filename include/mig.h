@@ -226,6 +226,18 @@ mig_status mig_workspace_bytes(const char* cublas_workspace_config, uint32_t n_l
 /* Number of kernel launches issued by the last device call on this thread (bench accounting). */
 uint32_t mig_last_launch_count(void);
 
+/* Kernel timing (bench accounting). While enabled on a thread, every device call of that thread brackets its
+ * kernel launches with CUDA events on the call's stream, grouped as "k_estimate" (the estimation kernel) and
+ * "k_simulate" (all simulation kernels of the call). mig_timing_query synchronises the recorded events, writes up
+ * to cap entries {name, total milliseconds, launch count} and clears the record. Enabling or disabling clears it. */
+typedef struct {
+    char name[16];
+    double ms;
+    uint32_t launches, reserved;
+} mig_kernel_time;
+void mig_timing_enable(int on);
+mig_status mig_timing_query(mig_kernel_time* out, uint32_t cap, uint32_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

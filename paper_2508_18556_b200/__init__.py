@@ -93,6 +93,27 @@ def mig_last_launch_count() -> int:
     return int(_lib.mig_last_launch_count())
 
 
+class mig_kernel_time(C.Structure):
+    _fields_ = [("name", C.c_char * 16), ("ms", C.c_double), ("launches", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+_lib.mig_timing_enable.argtypes = [C.c_int]
+_lib.mig_timing_query.argtypes = [C.POINTER(mig_kernel_time), C.c_uint32, C.POINTER(C.c_uint32)]
+
+
+def mig_timing_enable(on: bool = True) -> None:
+    """Bracket this thread's kernel launches with CUDA events (include/mig.h: mig_timing_enable)."""
+    _lib.mig_timing_enable(1 if on else 0)
+
+
+def mig_timing_query() -> dict:
+    """{kernel group name: (total ms, launches)} since the last enable/query (synchronises the events)."""
+    buf = (mig_kernel_time * 8)()
+    n = C.c_uint32(0)
+    _check(_lib.mig_timing_query(buf, 8, C.byref(n)))
+    return {buf[i].name.decode(): (buf[i].ms, int(buf[i].launches)) for i in range(min(n.value, 8))}
+
+
 class Geometry:
     """A loaded geometry (opaque mig_geometry*), with its info and profile table."""
 

@@ -15,13 +15,50 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream, uint32_t* launches);
+                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof);
 }  // namespace mig
 
 namespace {
 constexpr size_t kCounterBytes = 16 * sizeof(unsigned long long);
 thread_local std::string t_err;
 thread_local uint32_t t_launches = 0;
+
+// mig_timing_enable / mig_timing_query: events bracketing each group of launches (name, start, stop, launches)
+struct TimedRec {
+    const char* name;
+    cudaEvent_t a, b;
+    uint32_t launches;
+};
+thread_local bool t_timing = false;
+thread_local std::vector<TimedRec> t_recs;
+
+void clear_recs() {
+    for (auto& r : t_recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    t_recs.clear();
+}
+
+// Runs launch() (which returns the number of kernels it launched, or -1 on error) between two events when timing.
+template <class F>
+cudaError_t timed(const char* name, cudaStream_t s, F&& launch) {
+    if (!t_timing) return launch(nullptr);
+    TimedRec r{name, nullptr, nullptr, 0};
+    cudaError_t e = cudaEventCreate(&r.a);
+    if (e == cudaSuccess) e = cudaEventCreate(&r.b);
+    if (e == cudaSuccess) e = cudaEventRecord(r.a, s);
+    if (e != cudaSuccess) return e;
+    e = launch(&r.launches);
+    if (e == cudaSuccess) e = cudaEventRecord(r.b, s);
+    if (e != cudaSuccess) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+        return e;
+    }
+    t_recs.push_back(r);
+    return cudaSuccess;
+}
 
 mig_status cuda_fail(cudaError_t e, const char* what) {
     return mig_set_error(MIG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -126,14 +163,21 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
     cudaError_t e;
     uint32_t launches = 0;
     if (!est) {
-        e = mig::launch_estimate(g->dg, tr, pols[0], est_scratch, counters, sm_count_of(dev), true, s);
+        e = timed("k_estimate", s, [&](uint32_t* nl) {
+            if (nl) *nl = 1;
+            return mig::launch_estimate(g->dg, tr, pols[0], est_scratch, counters, sm_count_of(dev), true, s);
+        });
         if (e != cudaSuccess) return cuda_fail(e, "k_estimate launch");
         ++launches;
         est = est_scratch;
     }
     uint32_t nl = 0;
-    e = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1, sm_count_of(dev), s,
-                             &nl);
+    e = timed("k_simulate", s, [&](uint32_t* tl) {
+        cudaError_t e2 = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1,
+                                              sm_count_of(dev), s, &nl, g->dg.n_prof);
+        if (tl) *tl = nl;
+        return e2;
+    });
     if (e != cudaSuccess) return cuda_fail(e, "k_simulate launch");
     launches += nl;
     t_launches += launches;
@@ -197,6 +241,41 @@ mig_status mig_workspace_bytes(const char* cfg, uint32_t n_layers, uint64_t* byt
 
 uint32_t mig_last_launch_count(void) { return t_launches; }
 
+void mig_timing_enable(int on) {
+    clear_recs();
+    t_timing = on != 0;
+}
+
+mig_status mig_timing_query(mig_kernel_time* out, uint32_t cap, uint32_t* n_out) {
+    if (!n_out || (cap && !out)) return mig_set_error(MIG_E_INVALID_ARG, "mig_timing_query: null argument");
+    std::vector<mig_kernel_time> agg;
+    for (auto& r : t_recs) {
+        cudaError_t e = cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess) {
+            clear_recs();
+            return cuda_fail(e, "mig_timing_query");
+        }
+        mig_kernel_time* k = nullptr;
+        for (auto& x : agg)
+            if (strncmp(x.name, r.name, sizeof(x.name)) == 0) k = &x;
+        if (!k) {
+            mig_kernel_time z;
+            memset(&z, 0, sizeof(z));
+            strncpy(z.name, r.name, sizeof(z.name) - 1);
+            agg.push_back(z);
+            k = &agg.back();
+        }
+        k->ms += ms;
+        k->launches += r.launches;
+    }
+    clear_recs();
+    *n_out = (uint32_t)agg.size();
+    for (uint32_t i = 0; i < cap && i < agg.size(); ++i) out[i] = agg[i];
+    return MIG_OK;
+}
+
 mig_status mig_estimate_memory(const mig_geometry* g, const mig_traces* traces, const mig_policy* policy,
                                mig_job_estimate* out, void* stream) {
     t_launches = 0;
@@ -216,7 +295,10 @@ mig_status mig_estimate_memory(const mig_geometry* g, const mig_traces* traces, 
     cudaError_t e = cudaMallocAsync(&scratch, 2 * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scratch)");
     cudaMemsetAsync(scratch, 0, 2 * sizeof(unsigned long long), s);
-    e = mig::launch_estimate(g->dg, *traces, *policy, out, scratch, sm_count_of(dev), false, s);
+    e = timed("k_estimate", s, [&](uint32_t* nl) {
+        if (nl) *nl = 1;
+        return mig::launch_estimate(g->dg, *traces, *policy, out, scratch, sm_count_of(dev), false, s);
+    });
     cudaFreeAsync(scratch, s);
     if (e != cudaSuccess) return cuda_fail(e, "k_estimate launch");
     t_launches = 1;

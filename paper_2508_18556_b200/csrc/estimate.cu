@@ -6,7 +6,7 @@
 //   DYNAMIC jobs: Alg. 3 PeakMemoryPrediction over the per-iteration samples, plus the
 //   first-exceed iteration of every memory level (where the job would OOM).
 //
-// Layout: one warp per trace (persistent CTAs, atomic trace counter). Lanes take the trace's jobs 32 at a time;
+// Layout: one warp per batch of traces (persistent CTAs, atomic counter). Lanes take the jobs 32 at a time;
 // each DYNAMIC job is then processed by the whole warp, lanes over iterations: lane i draws sample base+i+1
 // in-kernel (counter-based generator, tracegen.h), the exact integer moments Sum y, Sum t*y, Sum y^2, Sum q,
 // Sum t*q are warp inclusive scans (__shfl_up_sync), every lane evaluates the forecast P_n for its own n, the
@@ -233,26 +233,34 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig, mfe, mconv, Smem);
 }
 
+// Traces are taken kBatch at a time (one atomic per batch); the warp streams the batch's job records as one
+// contiguous range, 32 coalesced 16-B records per step, so STATIC/MODEL-only workloads run at scan speed; a DYNAMIC
+// job's trace is found by a ballot over the batch's offsets held one per lane.
+constexpr uint32_t kEstBatch = 32;
+
 __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstParams P) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t j_base = P.off[0];
     for (;;) {
-        unsigned long long tr = 0;
-        if (lane == 0) tr = atomicAdd(P.counter, 1ull);
-        tr = __shfl_sync(FULL, tr, 0);
-        if (tr >= P.n_traces) break;
-        const uint64_t j0 = P.off[tr] - j_base;
-        const uint32_t n = (uint32_t)(P.off[tr + 1] - P.off[tr]);
-        for (uint32_t c = 0; c < n; c += 32) {
-            const uint32_t j = c + lane;
-            const bool valid = j < n;
+        unsigned long long t0 = 0;
+        if (lane == 0) t0 = atomicAdd(P.counter, (unsigned long long)kEstBatch);
+        t0 = __shfl_sync(FULL, t0, 0);
+        if (t0 >= P.n_traces) break;
+        const uint32_t nb = (uint32_t)min((unsigned long long)kEstBatch, P.n_traces - t0);
+        const uint64_t my_off = lane < nb ? P.off[t0 + lane] - j_base : ~0ull;  // first job of batch trace `lane`
+        const uint64_t gend = P.off[t0 + nb] - j_base;
+        const uint64_t gbeg = __shfl_sync(FULL, my_off, 0);
+        for (uint64_t c = gbeg; c < gend; c += 32) {
+            const uint64_t g = c + lane;
+            const bool valid = g < gend;
             uint4 r = make_uint4(0, 0, 0, 0), e = make_uint4(0, 0, 0, 0);
             if (valid) {
-                r = __ldg(P.jobs + j0 + j);
-                if (P.ext) e = __ldg(P.ext + j0 + j);
+                r = __ldg(P.jobs + g);
+                if (P.ext) e = __ldg(P.ext + g);
             }
             const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
-            if (valid && (cls > 2 || T > 4096 || (r.z >> 24) != 0)) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
+            if (__any_sync(FULL, valid && (cls > 2 || T > 4096 || (r.z >> 24) != 0)) && lane == 0)
+                atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
             if (valid && cls != kClassDynamic && !P.dyn_only) {
                 const uint64_t phys = (uint64_t)r.y + e.x + P.ctx;
                 uint32_t fe[5], mfe[5];
@@ -261,13 +269,17 @@ __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstP
                     fe[l] = (l < (int)G.n_levels && T >= 1 && phys > G.level_mem[l]) ? 1u : kNever;
                     mfe[l] = fe[l] == 1u ? (uint32_t)phys : 0u;
                 }
-                store_estimate(P.out + j0 + j, r.x + e.x + P.ctx, 0, 0, G.n_levels, fe, 0.0, 0.0, 0.0, mfe, 0u,
+                store_estimate(P.out + g, r.x + e.x + P.ctx, 0, 0, G.n_levels, fe, 0.0, 0.0, 0.0, mfe, 0u,
                                (uint32_t)phys * T);
             }
             uint32_t dm = __ballot_sync(FULL, valid && cls == kClassDynamic);
             while (dm) {
                 const uint32_t L = (uint32_t)__ffs(dm) - 1;
                 dm &= dm - 1;
+                const uint64_t gL = c + L;
+                // the batch trace holding job gL: the last trace whose first job is <= gL
+                const uint32_t tb = 31u - __clz(__ballot_sync(FULL, lane < nb && my_off <= gL));
+                const uint32_t jt = (uint32_t)(gL - __shfl_sync(FULL, my_off, tb));
                 uint4 rr, ee;
                 rr.x = __shfl_sync(FULL, r.x, L);
                 rr.y = __shfl_sync(FULL, r.y, L);
@@ -280,16 +292,15 @@ __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstP
                 const uint2* rs = nullptr;
                 uint32_t rcount = 0;
                 if (P.samples) {
-                    const uint64_t k = j0 + c + L;
-                    rs = P.samples + (P.sample_off[k] - P.sample_off[0]);
-                    const uint64_t cnt = P.sample_off[k + 1] - P.sample_off[k];
+                    rs = P.samples + (P.sample_off[gL] - P.sample_off[0]);
+                    const uint64_t cnt = P.sample_off[gL + 1] - P.sample_off[gL];
                     rcount = cnt > 0xFFFFu ? 0xFFFFu : (uint32_t)cnt;
                     if (rcount < (rr.z & 0xFFFFu)) {
                         if (lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
                         if (rcount == 0) rs = nullptr;  // nothing recorded: fall back to the declared generator
                     }
                 }
-                estimate_dynamic(G, P, P.trace_id0 + tr, c + L, rr, ee, lane, P.out + j0 + c + L, rs, rcount);
+                estimate_dynamic(G, P, P.trace_id0 + t0 + tb, jt, rr, ee, lane, P.out + gL, rs, rcount);
             }
         }
     }
@@ -322,7 +333,7 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate, threads, 0);
     if (per_sm < 1) per_sm = 1;
-    uint64_t want = (tr.n_traces + 7) / 8;
+    uint64_t want = (tr.n_traces + 8 * kEstBatch - 1) / (8 * kEstBatch);
     uint64_t blocks = (uint64_t)per_sm * sm_count;
     if (want < blocks) blocks = want;
     if (blocks < 1) blocks = 1;

@@ -958,7 +958,7 @@ bool simulate_use_lane() {
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream, uint32_t* launches) {
+                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof) {
     SimParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -985,7 +985,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     PA.counter = counter + 1;
     cudaError_t e = cudaSuccess;
     *launches = 0;
-    if (P.n_pol && simulate_use_lane()) {
+    if (P.n_pol && simulate_use_lane() && n_prof <= 8) {  // the lane kernel packs idle masks per profile in a u64
         const uint64_t blocks = simulate_lane_grid(tr.n_traces, sm_count);
         uint16_t* ring = nullptr;
         e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * tr.max_jobs * sizeof(uint16_t), stream);

@@ -61,7 +61,9 @@ __constant__ const uint8_t kF64[kT64] = {12, 14, 15, 16, 17, 18, 19};
 struct LaneShared {
     DevGeom G;
     uint8_t alloc[256 * 16];  // Alg. 2 result by (occupancy, profile): start, or 0xFF = FAIL
-    uint16_t reuse_ok[16];    // FF: profiles q whose idle instance tightly fits profile p (same memory, compute >=)
+    uint8_t nobusy[256 * 16]; // FF: placements k of profile p (bit k) that touch no busy slot, by busy-slot mask
+    unsigned long long reuse_sel[16];  // FF: byte q = 0xFF if an idle instance of profile q tightly fits profile p
+                                       // (same memory, compute >=; R7), selecting from the idle-by-profile masks
     uint8_t scand[16];        // STATIC: layout starts whose slice can hold profile p
     uint8_t lvl_first[8];     // first profile of each memory level ([n_levels] = 0xFF)
     uint32_t jk[8][kLaneThreads];  // per lane and start slot: job | end kind << 16 of the running job
@@ -116,7 +118,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) LaneShared S;
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
         uint32_t* dst = reinterpret_cast<uint32_t*>(&S.G);
@@ -140,6 +142,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 }
             }
             S.alloc[i] = best ? (uint8_t)(best & 0xFFu) : (uint8_t)0xFFu;
+            uint32_t nb = 0;  // here occ plays the busy-slot mask BM
+            if (p < G.n_prof)
+                for (uint32_t k = 0; k < G.n_place[p]; ++k) nb |= ((G.place[p][k] >> 8) & occ) ? 0u : 1u << k;
+            S.nobusy[i] = (uint8_t)nb;
         }
         if (tid < 16) {
             uint32_t ok = 0, sc = 0;
@@ -151,7 +157,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     if (G.level[lp] >= G.level[tid] && G.comp[lp] >= G.comp[tid]) sc |= 1u << G.layout_start[i];
                 }
             }
-            S.reuse_ok[tid] = (uint16_t)ok;
+            unsigned long long sel = 0;
+            for (uint32_t q = 0; q < 8; ++q)
+                if ((ok >> q) & 1u) sel |= 0xFFull << (8 * q);
+            S.reuse_sel[tid] = sel;
             S.scand[tid] = (uint8_t)sc;
         }
         if (tid < 8) {
@@ -180,6 +189,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     uint64_t j0 = 0;
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
     uint32_t occ = 0, SM = 0, EM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0;
+    uint64_t IPM = 0;  // FF: idle instances by profile, byte p bit s = an idle instance of profile p starts at s
     uint32_t endt[8];
     uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
     uint64_t a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
@@ -218,6 +228,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         t = qh = rh = rn = evm = 0;
         BS = BM = 0;
         occ = SM = EM = prof4 = 0;
+        IPM = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) endt[k] = kNoEnd;
         if (KIND == MIG_STATIC) {
@@ -301,7 +312,11 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
 
     bool active = tr < P.n_traces;
     if (active) init_unit();
-    while (active) {
+    else mode = 3;
+    // Every lane of a warp advances one step per iteration; the vote at the top and the __syncwarp points between
+    // the phases keep the warp converged (without them the compiler's reconvergence points are too coarse and the
+    // divergent paths of an iteration ran one after another: 4.5 active lanes per instruction).
+    while (__any_sync(FULL, active)) {
         if constexpr (KIND == MIG_BASELINE) {
             // ---- BASELINE: one job at a time on the whole GPU, queue order ----
             if (mode == 0) {
@@ -348,118 +363,148 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             }
         } else {
             // ---- PASS: evaluate the head of the queue (Alg. 4, one decision) ----
-            if (mode == 0) {
-                if (hj == kNoJob) {
-                    mode = 1;
-                } else {
-                    const uint32_t j = hj, need = head_need(), jsh = j << 16;
-                    bool popit = true;
-                    if (need == kNoNeed) {  // no profile can ever hold the job: REJECT
-                        lrec(hl, hh, t, jsh | (K_REJECT << 12) | 0xFF0u);
-                        K2 += 1u;
+            // P1 (local decision) | A7 (fusion/fission, warp-cooperative) | P2 (record, run start, pop), with the
+            // warp reconverged between phases: every decision path then shares one copy of the common code.
+            if (mode == 0 && hj == kNoJob) mode = 1;
+            const bool pass = mode == 0;
+            uint32_t j = 0, need = 0, s = 0, kd = 0, nd = 0, pr = 0, lo = 0, cm = 0;
+            if (pass) {
+                j = hj;
+                need = head_need();
+                pr = need;
+                const uint32_t jsh = j << 16;
+                if (need == kNoNeed) {  // no profile can ever hold the job: REJECT
+                    lo = jsh | (K_REJECT << 12) | 0xFF0u;
+                    kd = K_REJECT;
+                } else if (KIND == MIG_STATIC) {  // smallest idle fitting layout slice, tie -> highest start (R11)
+                    const uint32_t cand = S.scand[need];
+                    uint32_t m = cand & ~BS, bk = 0;
+                    while (m) {
+                        const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                        m &= m - 1u;
+                        const uint32_t il = G.pinfo[(prof4 >> (4 * k)) & 0xFu] & 0xFu;
+                        bk = max(bk, (((15u - il) << 5) | k) + 1u);
+                    }
+                    if (bk) {
+                        s = (bk - 1u) & 31u;
+                        pr = (prof4 >> (4 * s)) & 0xFu;
+                        kd = K_PLACE_STATIC;
                     } else {
-                        const uint32_t pn = G.pinfo[need];
-                        uint32_t s = 0, kd = 0, nd = 0, pr = need;
-                        bool created = false;
-                        if (KIND == MIG_STATIC) {  // smallest idle fitting layout slice, tie -> highest start (R11)
-                            const uint32_t cand = S.scand[need];
-                            uint32_t m = cand & ~BS, bk = 0;
-                            while (m) {
-                                const uint32_t k = (uint32_t)__ffs(m) - 1u;
-                                m &= m - 1u;
-                                const uint32_t il = G.pinfo[(prof4 >> (4 * k)) & 0xFu] & 0xFu;
-                                bk = max(bk, (((15u - il) << 5) | k) + 1u);
-                            }
-                            if (bk) {
-                                s = (bk - 1u) & 31u;
-                                pr = (prof4 >> (4 * s)) & 0xFu;
-                                kd = K_PLACE_STATIC;
-                            } else if (cand) {
-                                lrec(hl, hh, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
-                                K1 += 1u << 16;
-                                popit = false;
-                                mode = 1;
-                            } else {
-                                lrec(hl, hh, t, jsh | (K_REJECT << 12) | 0xF00u | (need << 4));
-                                K2 += 1u;
-                            }
-                        } else {
-                            if (KIND == MIG_FUSION_FISSION) {  // an idle slice that tightly fits (R7)
-                                uint32_t m = SM & ~BS;
-                                const uint32_t ok = S.reuse_ok[need];
-                                while (m) {
-                                    const uint32_t k = 31u - __clz(m);
-                                    if ((ok >> ((prof4 >> (4 * k)) & 0xFu)) & 1u) {
-                                        s = k;
-                                        pr = (prof4 >> (4 * k)) & 0xFu;
-                                        kd = K_REUSE;
-                                        break;
-                                    }
-                                    m &= ~(1u << k);
-                                }
-                            }
-                            if (!kd) {
-                                const uint32_t a = S.alloc[(occ << 4) | need];  // Alg. 2
-                                const uint32_t nlen = (pn >> 16) & 0xFu;
-                                if (a != 0xFFu) {
-                                    s = a;
-                                    kd = K_ALLOC;
-                                } else if (KIND == MIG_FUSION_FISSION && (SM & ~BS)) {
-                                    // fusion / fission: destroy the idle instances a placement overlaps (none busy,
-                                    // >= 1), best (fcr(result), -#destroyed, start) (R8)
-                                    uint32_t bs = 0;
-                                    for (uint32_t k = 0; k < G.n_place[need]; ++k) {
-                                        const uint32_t pl = G.place[need][k], qm = pl >> 8;
-                                        if (!(qm & BM) && (qm & occ)) {
-                                            const uint32_t lo = pl & 0xFFu;
-                                            const uint32_t rm = lane_overlap_extent(occ, SM, EM, lo, lo + nlen - 1u);
-                                            bs = max(bs, ((uint32_t)G.fcr[(occ & ~rm) | qm] << 16) |
-                                                             ((15u - __popc(SM & rm)) << 8) | lo);
-                                        }
-                                    }
-                                    if (bs) {
-                                        s = bs & 0xFFu;
-                                        nd = 15u - ((bs >> 8) & 0xFFu);
-                                        const uint32_t rm = lane_overlap_extent(occ, SM, EM, s, s + nlen - 1u);
-                                        occ &= ~rm;
-                                        SM &= ~rm;
-                                        EM &= ~rm;
-                                        kd = K_RECONF;
-                                    }
-                                }
-                                if (!kd) {  // sleep() until a running job finishes
-                                    lrec(hl, hh, t, jsh | (K_WAIT << 12) | 0xF00u | (need << 4));
-                                    K1 += 1u << 16;
-                                    popit = false;
-                                    mode = 1;
-                                } else {  // create the instance (try_new_mig_slice)
-                                    created = true;
-                                    occ |= ((pn >> 8) & 0xFFu) << s;
-                                    if (KIND == MIG_FUSION_FISSION) {
-                                        SM |= 1u << s;
-                                        EM |= 1u << (s + nlen - 1u);
-                                    }
-                                    prof4 = (prof4 & ~(0xFu << (4 * s))) | (need << (4 * s));
-                                }
-                            }
-                        }
-                        if (kd) {  // the decision record, then start the run
-                            lrec(hl, hh, t, jsh | (kd << 12) | (s << 8) | (pr << 4) | nd);
-                            K0 += created ? 0x10001u : 1u;
-                            K1 += nd;
-                            uint32_t end, ek;
-                            start_run(j, s, pr, t + (created ? reconfig : 0u), end, ek);
-#pragma unroll
-                            for (int k = 0; k < 8; ++k)
-                                if ((uint32_t)k == s) endt[k] = end;
-                            jk[s * kLaneThreads] = j | (ek << 16);
-                            BS |= 1u << s;
-                            BM |= ((G.pinfo[pr] >> 8) & 0xFFu) << s;
+                        kd = cand ? K_WAIT : K_REJECT;
+                        lo = jsh | ((cand ? K_WAIT : K_REJECT) << 12) | 0xF00u | (need << 4);
+                    }
+                } else {
+                    if (KIND == MIG_FUSION_FISSION) {  // an idle slice that tightly fits (R7)
+                        uint64_t x = IPM & S.reuse_sel[need];
+                        x |= x >> 32;
+                        x |= x >> 16;
+                        x |= x >> 8;
+                        const uint32_t cand = (uint32_t)x & 0xFFu;
+                        if (cand) {
+                            s = 31u - __clz(cand);
+                            pr = (prof4 >> (4 * s)) & 0xFu;
+                            kd = K_REUSE;
                         }
                     }
-                    if (popit) pop();
+                    if (!kd) {
+                        const uint32_t a = S.alloc[(occ << 4) | need];  // Alg. 2
+                        if (a != 0xFFu) {
+                            s = a;
+                            kd = K_ALLOC;
+                        } else {
+                            // fusion / fission candidates: placements touching no busy slot (none: WAIT)
+                            if (KIND == MIG_FUSION_FISSION && (SM & ~BS)) cm = S.nobusy[(BM << 4) | need];
+                            if (!cm) {  // sleep() until a running job finishes
+                                kd = K_WAIT;
+                                lo = jsh | (K_WAIT << 12) | 0xF00u | (need << 4);
+                            }
+                        }
+                    }
                 }
             }
+            if (KIND == MIG_FUSION_FISSION) {
+                // ---- A7: fusion / fission (R8), warp-cooperative: each requesting lane's
+                // candidate placements are scored by eight lanes: destroy the idle instances placement k overlaps
+                // (none busy, >= 1); best (fcr(result), -#destroyed, start) ----
+                __syncwarp();
+                uint32_t a7m = __ballot_sync(FULL, cm != 0);
+                while (a7m) {  // up to four requests per round: lanes 8r..8r+7 score request r's placements
+                    const uint32_t r = lane >> 3, k = lane & 7u;
+                    const uint32_t m1 = a7m & (a7m - 1u), m2 = m1 & (m1 - 1u), m3 = m2 & (m2 - 1u);
+                    const uint32_t mr = r == 0 ? a7m : r == 1 ? m1 : r == 2 ? m2 : m3;
+                    const uint32_t src = mr ? (uint32_t)__ffs(mr) - 1u : 0u;
+                    const uint32_t o = __shfl_sync(FULL, occ, src), sm = __shfl_sync(FULL, SM, src),
+                                   em = __shfl_sync(FULL, EM, src), nn = __shfl_sync(FULL, need, src),
+                                   c = __shfl_sync(FULL, cm, src);
+                    uint32_t sc = 0;
+                    if (mr && ((c >> k) & 1u)) {
+                        const uint32_t pl = G.place[nn][k], qm = pl >> 8;
+                        if (qm & o) {
+                            const uint32_t ql = pl & 0xFFu, nlen = (G.pinfo[nn] >> 16) & 0xFu;
+                            const uint32_t rm = lane_overlap_extent(o, sm, em, ql, ql + nlen - 1u);
+                            sc = ((uint32_t)G.fcr[(o & ~rm) | qm] << 16) | ((15u - __popc(sm & rm)) << 8) | ql;
+                        }
+                    }
+                    sc = max(sc, __shfl_xor_sync(FULL, sc, 1));
+                    sc = max(sc, __shfl_xor_sync(FULL, sc, 2));
+                    sc = max(sc, __shfl_xor_sync(FULL, sc, 4));
+                    // requester of round slot rr (its rank among the round's requests) reads lane 8 * rr
+                    const uint32_t rr = __popc(a7m & ((1u << lane) - 1u));
+                    const uint32_t best = __shfl_sync(FULL, sc, (rr & 3u) * 8u);
+                    if (((a7m >> lane) & 1u) && rr < 4) cm = best | 0x80000000u;
+                    a7m = m3 & (m3 - 1u);
+                }
+                if (cm) {
+                    const uint32_t bs = cm & 0x7FFFFFFFu;
+                    if (bs) {
+                        s = bs & 0xFFu;
+                        nd = 15u - ((bs >> 8) & 0xFFu);
+                        const uint32_t rm =
+                            lane_overlap_extent(occ, SM, EM, s, s + ((G.pinfo[need] >> 16) & 0xFu) - 1u);
+                        IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
+                        occ &= ~rm;
+                        SM &= ~rm;
+                        EM &= ~rm;
+                        kd = K_RECONF;
+                    } else {
+                        kd = K_WAIT;
+                        lo = (j << 16) | (K_WAIT << 12) | 0xF00u | (need << 4);
+                    }
+                }
+            }
+            __syncwarp();
+            if (pass) {
+                // ---- P2: create (ALLOC / RECONF, try_new_mig_slice PAPER.md:609), the decision record, the run ----
+                const bool created = kd == K_ALLOC || kd == K_RECONF;
+                const bool place = kd != K_WAIT && kd != K_REJECT;
+                if (created) {
+                    const uint32_t pn = G.pinfo[need];
+                    occ |= ((pn >> 8) & 0xFFu) << s;
+                    if (KIND == MIG_FUSION_FISSION) {
+                        SM |= 1u << s;
+                        EM |= 1u << (s + ((pn >> 16) & 0xFu) - 1u);
+                    }
+                    prof4 = (prof4 & ~(0xFu << (4 * s))) | (need << (4 * s));
+                }
+                if (KIND == MIG_FUSION_FISSION && kd == K_REUSE) IPM &= ~(1ull << (8 * pr + s));
+                if (place) lo = (j << 16) | (kd << 12) | (s << 8) | (pr << 4) | nd;
+                lrec(hl, hh, t, lo);
+                K0 += place ? (created ? 0x10001u : 1u) : 0u;
+                K1 += kd == K_WAIT ? 1u << 16 : nd;
+                K2 += kd == K_REJECT ? 1u : 0u;
+                if (place) {
+                    uint32_t end, ek;
+                    start_run(j, s, pr, t + (created ? reconfig : 0u), end, ek);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) endt[k] = (uint32_t)k == s ? end : endt[k];
+                    jk[s * kLaneThreads] = j | (ek << 16);
+                    BS |= 1u << s;
+                    BM |= ((G.pinfo[pr] >> 8) & 0xFFu) << s;
+                }
+                if (kd == K_WAIT) mode = 1;
+                else pop();
+            }
+            __syncwarp();
             // ---- EVT: apply one event (min end tick; ties COMPLETE < OOM < PREEMPT, then job id, R28) ----
             if (mode == 1) {
                 if (!evm) {
@@ -475,8 +520,8 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     }
                 }
                 if (evm) {
-                    uint32_t s = (uint32_t)__ffs(evm) - 1u;
-                    uint32_t v = jk[s * kLaneThreads];
+                    uint32_t es = (uint32_t)__ffs(evm) - 1u;
+                    uint32_t v = jk[es * kLaneThreads];
                     if (evm & (evm - 1u)) {
                         uint32_t m = evm & (evm - 1u);
                         while (m) {
@@ -485,31 +530,26 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                             const uint32_t w = jk[k * kLaneThreads];
                             if (w < v) {
                                 v = w;
-                                s = k;
+                                es = k;
                             }
                         }
                     }
-                    evm &= ~(1u << s);
+                    evm &= ~(1u << es);
                     const uint32_t job = v & 0xFFFFu, ek = v >> 16;
-                    const uint32_t pr = (prof4 >> (4 * s)) & 0xFu, si = G.pinfo[pr];
-                    const uint32_t lo = (job << 16) | (s << 8) | (pr << 4);
+                    const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = G.pinfo[epr];
+                    const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
+                    lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7 / PREEMPT 8
+                    a_turn += ek == 0 ? t : 0u;
+                    K2 += ek == 1 ? 1u << 16 : 0u;
+                    K3 += ek == 2 ? 1u : 0u;
                     uint32_t req = 0;
-                    if (ek == 0) {
-                        lrec(hl, hh, t, lo | (K_COMPLETE << 12));
-                        a_turn += t;
-                    } else if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
-                        lrec(hl, hh, t, lo | (K_OOM << 12));
-                        const uint32_t nl = G.level_next[si & 0xFu];
-                        K2 += 1u << 16;
-                        if (nl == 0) {
-                            lrec(hl, hh, t, lo | (K_FAILED << 12));
+                    if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
+                        req = G.level_next[si & 0xFu];
+                        if (req == 0) {
+                            lrec(hl, hh, t, elo | (K_FAILED << 12));
                             K3 += 1u << 16;
-                        } else {
-                            req = nl;
                         }
-                    } else {  // PREEMPT: restart on the slice meeting the forecast (R25)
-                        lrec(hl, hh, t, lo | (K_PREEMPT << 12));
-                        K3 += 1u;
+                    } else if (ek == 2) {  // PREEMPT: restart on the slice meeting the forecast (R25)
                         req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
                     }
                     if (req) {  // back to the queue tail (R13) with the new tight fit
@@ -522,19 +562,20 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         if (hj == kNoJob) fetch_head();
                     }
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if ((uint32_t)k == s) endt[k] = kNoEnd;
-                    const uint32_t ext = ((si >> 8) & 0xFFu) << s;
-                    BS &= ~(1u << s);
+                    for (int k = 0; k < 8; ++k) endt[k] = (uint32_t)k == es ? kNoEnd : endt[k];
+                    const uint32_t ext = ((si >> 8) & 0xFFu) << es;
+                    BS &= ~(1u << es);
                     BM &= ~ext;
                     if (KIND == MIG_DYNAMIC) {  // free on completion (R10)
                         occ &= ~ext;
                         K1 += 1u;
                     }
+                    if (KIND == MIG_FUSION_FISSION) IPM |= 1ull << (8 * epr + es);  // the instance is idle
                     if (!evm) mode = 0;
                 }
             }
         }
+        __syncwarp();
         // ---- FIN: the unit's result (96 B) and totals; take the next unit ----
         if (mode == 2) {
             const uint32_t placements = K0 & 0xFFFFu, creates = K0 >> 16, destroys = K1 & 0xFFFFu, waits = K1 >> 16,
@@ -584,6 +625,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 init_unit();
             } else {
                 active = false;
+                mode = 3;  // done: the lane keeps voting (and passing the __syncwarp points) until its warp is done
             }
         }
     }

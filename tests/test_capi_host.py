@@ -89,3 +89,9 @@ def test_workspace_parser_spec_examples():
     for bad in [":4096", "4096:8", ":4096:8,", ":a:8", ":4096:8;"]:
         with pytest.raises(mig.MigError, match="MIG_E_PARSE"):
             mig.mig_workspace_bytes(bad, 1)
+
+
+def test_timing_hook_without_launches():
+    mig.mig_timing_enable(True)
+    assert mig.mig_timing_query() == {}
+    mig.mig_timing_enable(False)
