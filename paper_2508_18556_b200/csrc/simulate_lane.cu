@@ -20,7 +20,7 @@
 // reduced once per CTA.
 //
 // Per-lane state: occupancy occ, instance starts SM / ends EM, busy starts BS / busy slots BM (u8 masks), profile
-// nibble per start slot (prof4), end tick per start slot (endt[8], registers), job|kind per slot (shared memory),
+// nibble per start slot (prof4), end tick and job|kind per start slot (shared memory, [slot][lane]),
 // the head job's record (prefetched when the queue advances), a requeue FIFO in global scratch (rare: OOM /
 // preempt restarts, R13), packed 16-bit counters, FNV-1a-64 hash halves, four u64 accumulators.
 //
@@ -53,20 +53,23 @@ constexpr int kLaneMinBlocks = 6;
 constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
 constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
 
-// mig_policy_totals fields accumulated per lane: 32-bit counts (index -> totals field) and 64-bit sums.
-constexpr int kT32 = 14, kT64 = 7;
-__constant__ const uint8_t kF32[kT32] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 20};
-__constant__ const uint8_t kF64[kT64] = {12, 14, 15, 16, 17, 18, 19};
+// mig_policy_totals fields accumulated per lane: 32-bit counts (index -> totals field) and 64-bit sums. completed,
+// restarts and energy are linear in these (n - rejected - failed; ooms - failed + preempts; idle_w * makespan +
+// w_per_slice * busy) and are derived once per CTA.
+constexpr int kT32 = 12, kT64 = 6;
+__constant__ const uint8_t kF32[kT32] = {0, 1, 3, 4, 5, 6, 8, 9, 10, 11, 13, 20};
+__constant__ const uint8_t kF64[kT64] = {12, 15, 16, 17, 18, 19};
 
 struct LaneShared {
     DevGeom G;
-    uint8_t alloc[256 * 16];  // Alg. 2 result by (occupancy, profile): start, or 0xFF = FAIL
-    uint8_t nobusy[256 * 16]; // FF: placements k of profile p (bit k) that touch no busy slot, by busy-slot mask
+    uint8_t alloc[256 * 8];   // Alg. 2 result by (occupancy, profile): start, or 0xFF = FAIL
+    uint8_t nobusy[256 * 8];  // FF: placements k of profile p (bit k) that touch no busy slot, by busy-slot mask
     unsigned long long reuse_sel[16];  // FF: byte q = 0xFF if an idle instance of profile q tightly fits profile p
                                        // (same memory, compute >=; R7), selecting from the idle-by-profile masks
     uint8_t scand[16];        // STATIC: layout starts whose slice can hold profile p
     uint8_t lvl_first[8];     // first profile of each memory level ([n_levels] = 0xFF)
     uint32_t jk[8][kLaneThreads];  // per lane and start slot: job | end kind << 16 of the running job
+    uint32_t et[8][kLaneThreads];  // per lane and start slot: end tick of the running job (kNoEnd = idle)
     // per-lane partial totals (no atomics: 64-bit shared atomics are CAS loops), reduced once per CTA
     uint32_t c32[kT32][kLaneThreads];
     unsigned long long c64[kT64][kLaneThreads];
@@ -131,8 +134,8 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     __syncthreads();
     {
         const DevGeom& G = S.G;
-        for (uint32_t i = tid; i < 256 * 16; i += blockDim.x) {  // Alg. 2 for every (occupancy, profile)
-            const uint32_t occ = i >> 4, p = i & 15u;
+        for (uint32_t i = tid; i < 256 * 8; i += blockDim.x) {  // Alg. 2 for every (occupancy, profile)
+            const uint32_t occ = i >> 3, p = i & 7u;
             uint32_t best = 0;
             if (p < G.n_prof && occ < (1u << G.n_slots)) {
                 for (uint32_t k = 0; k < G.n_place[p]; ++k) {
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     const uint64_t jbase = P.off[0];
     uint16_t* ring = P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap;
     uint32_t* jk = &S.jk[0][tid];
+    uint32_t* et = &S.et[0][tid];
     const uint32_t fp = G.full_prof;
 
     // ---- unit state ----
@@ -190,7 +194,6 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
     uint32_t occ = 0, SM = 0, EM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0;
     uint64_t IPM = 0;  // FF: idle instances by profile, byte p bit s = an idle instance of profile p starts at s
-    uint32_t endt[8];
     uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
     uint64_t a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
     uint32_t hj = kNoJob, hneed = kUnk;  // head job and its tight fit (kUnk: not yet computed)
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         occ = SM = EM = prof4 = 0;
         IPM = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) endt[k] = kNoEnd;
+        for (int k = 0; k < 8; ++k) et[k * kLaneThreads] = kNoEnd;
         if (KIND == MIG_STATIC) {
             for (uint32_t i = 0; i < G.n_layout; ++i) {
                 const uint32_t p = G.layout_prof[i], s = G.layout_start[i];
@@ -407,13 +410,13 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         }
                     }
                     if (!kd) {
-                        const uint32_t a = S.alloc[(occ << 4) | need];  // Alg. 2
+                        const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2
                         if (a != 0xFFu) {
                             s = a;
                             kd = K_ALLOC;
                         } else {
                             // fusion / fission candidates: placements touching no busy slot (none: WAIT)
-                            if (KIND == MIG_FUSION_FISSION && (SM & ~BS)) cm = S.nobusy[(BM << 4) | need];
+                            if (KIND == MIG_FUSION_FISSION && (SM & ~BS)) cm = S.nobusy[(BM << 3) | need];
                             if (!cm) {  // sleep() until a running job finishes
                                 kd = K_WAIT;
                                 lo = jsh | (K_WAIT << 12) | 0xF00u | (need << 4);
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 // candidate placements are scored by eight lanes: destroy the idle instances placement k overlaps
                 // (none busy, >= 1); best (fcr(result), -#destroyed, start) ----
                 __syncwarp();
-                uint32_t a7m = __ballot_sync(FULL, cm != 0);
+                uint32_t a7m = __ballot_sync(FULL, cm != 0), a7rm = 0;
                 while (a7m) {  // up to four requests per round: lanes 8r..8r+7 score request r's placements
                     const uint32_t r = lane >> 3, k = lane & 7u;
                     const uint32_t m1 = a7m & (a7m - 1u), m2 = m1 & (m1 - 1u), m3 = m2 & (m2 - 1u);
@@ -436,13 +439,15 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     const uint32_t o = __shfl_sync(FULL, occ, src), sm = __shfl_sync(FULL, SM, src),
                                    em = __shfl_sync(FULL, EM, src), nn = __shfl_sync(FULL, need, src),
                                    c = __shfl_sync(FULL, cm, src);
-                    uint32_t sc = 0;
+                    uint32_t sc = 0, rm = 0;
                     if (mr && ((c >> k) & 1u)) {
                         const uint32_t pl = G.place[nn][k], qm = pl >> 8;
                         if (qm & o) {
                             const uint32_t ql = pl & 0xFFu, nlen = (G.pinfo[nn] >> 16) & 0xFu;
-                            const uint32_t rm = lane_overlap_extent(o, sm, em, ql, ql + nlen - 1u);
-                            sc = ((uint32_t)G.fcr[(o & ~rm) | qm] << 16) | ((15u - __popc(sm & rm)) << 8) | ql;
+                            rm = lane_overlap_extent(o, sm, em, ql, ql + nlen - 1u);
+                            // (fcr(result), -#destroyed, start); the scoring lane k rides in the low bits
+                            sc = ((uint32_t)G.fcr[(o & ~rm) | qm] << 16) | ((15u - __popc(sm & rm)) << 8) | (ql << 3) |
+                                 k;
                         }
                     }
                     sc = max(sc, __shfl_xor_sync(FULL, sc, 1));
@@ -451,16 +456,19 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     // requester of round slot rr (its rank among the round's requests) reads lane 8 * rr
                     const uint32_t rr = __popc(a7m & ((1u << lane) - 1u));
                     const uint32_t best = __shfl_sync(FULL, sc, (rr & 3u) * 8u);
-                    if (((a7m >> lane) & 1u) && rr < 4) cm = best | 0x80000000u;
+                    const uint32_t brm = __shfl_sync(FULL, rm, (rr & 3u) * 8u + (best & 7u));
+                    if (((a7m >> lane) & 1u) && rr < 4) {
+                        cm = best | 0x80000000u;
+                        a7rm = brm;
+                    }
                     a7m = m3 & (m3 - 1u);
                 }
                 if (cm) {
                     const uint32_t bs = cm & 0x7FFFFFFFu;
                     if (bs) {
-                        s = bs & 0xFFu;
+                        s = (bs >> 3) & 0x1Fu;
                         nd = 15u - ((bs >> 8) & 0xFFu);
-                        const uint32_t rm =
-                            lane_overlap_extent(occ, SM, EM, s, s + ((G.pinfo[need] >> 16) & 0xFu) - 1u);
+                        const uint32_t rm = a7rm;
                         IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
                         occ &= ~rm;
                         SM &= ~rm;
@@ -495,8 +503,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 if (place) {
                     uint32_t end, ek;
                     start_run(j, s, pr, t + (created ? reconfig : 0u), end, ek);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) endt[k] = (uint32_t)k == s ? end : endt[k];
+                    et[s * kLaneThreads] = end;
                     jk[s * kLaneThreads] = j | (ek << 16);
                     BS |= 1u << s;
                     BM |= ((G.pinfo[pr] >> 8) & 0xFFu) << s;
@@ -508,15 +515,18 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             // ---- EVT: apply one event (min end tick; ties COMPLETE < OOM < PREEMPT, then job id, R28) ----
             if (mode == 1) {
                 if (!evm) {
-                    uint32_t tn = endt[0];
+                    uint32_t e8[8];
 #pragma unroll
-                    for (int k = 1; k < 8; ++k) tn = min(tn, endt[k]);
+                    for (int k = 0; k < 8; ++k) e8[k] = et[k * kLaneThreads];
+                    uint32_t tn = e8[0];
+#pragma unroll
+                    for (int k = 1; k < 8; ++k) tn = min(tn, e8[k]);
                     if (tn == kNoEnd) {
                         mode = 2;
                     } else {
                         t = tn;
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) evm |= (endt[k] == tn ? 1u : 0u) << k;
+                        for (int k = 0; k < 8; ++k) evm |= (e8[k] == tn ? 1u : 0u) << k;
                     }
                 }
                 if (evm) {
@@ -561,8 +571,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         ++rn;
                         if (hj == kNoJob) fetch_head();
                     }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) endt[k] = (uint32_t)k == es ? kNoEnd : endt[k];
+                    et[es * kLaneThreads] = kNoEnd;
                     const uint32_t ext = ((si >> 8) & 0xFFu) << es;
                     BS &= ~(1u << es);
                     BM &= ~ext;
@@ -598,26 +607,23 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 uint32_t* c = &S.c32[0][tid];
                 c[0 * kLaneThreads] += 1u;
                 c[1 * kLaneThreads] += n;
-                c[2 * kLaneThreads] += completed;
-                c[3 * kLaneThreads] += rejected;
-                c[4 * kLaneThreads] += failed;
-                c[5 * kLaneThreads] += ooms;
-                c[6 * kLaneThreads] += preempts;
-                c[7 * kLaneThreads] += restarts;
-                c[8 * kLaneThreads] += placements;
-                c[9 * kLaneThreads] += waits;
-                c[10 * kLaneThreads] += creates;
-                c[11 * kLaneThreads] += destroys;
-                c[12 * kLaneThreads] = max(c[12 * kLaneThreads], makespan);
-                c[13 * kLaneThreads] |= err;
+                c[2 * kLaneThreads] += rejected;
+                c[3 * kLaneThreads] += failed;
+                c[4 * kLaneThreads] += ooms;
+                c[5 * kLaneThreads] += preempts;
+                c[6 * kLaneThreads] += placements;
+                c[7 * kLaneThreads] += waits;
+                c[8 * kLaneThreads] += creates;
+                c[9 * kLaneThreads] += destroys;
+                c[10 * kLaneThreads] = max(c[10 * kLaneThreads], makespan);
+                c[11 * kLaneThreads] |= err;
                 unsigned long long* d = &S.c64[0][tid];
                 d[0 * kLaneThreads] += makespan;
-                d[1 * kLaneThreads] += energy;
-                d[2 * kLaneThreads] += a_turn;
-                d[3 * kLaneThreads] += a_busy;
-                d[4 * kLaneThreads] += ((unsigned long long)hh << 32) | hl;
-                d[5 * kLaneThreads] += a_mem;
-                d[6 * kLaneThreads] += a_waste;
+                d[1 * kLaneThreads] += a_turn;
+                d[2 * kLaneThreads] += a_busy;
+                d[3 * kLaneThreads] += ((unsigned long long)hh << 32) | hl;
+                d[4 * kLaneThreads] += a_mem;
+                d[5 * kLaneThreads] += a_waste;
             }
             tr = tr_next;
             if (tr < P.n_traces) {
@@ -633,21 +639,30 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     if (P.totals) {
         unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);
         if (tid == 0 && blockIdx.x == 0 && P.est_err && *P.est_err) atomicOr(dst + 20, *P.est_err);
+        __shared__ unsigned long long red[24];
         if (tid < kT32 + kT64) {  // one thread per field reduces the CTA's lanes
             unsigned long long v = 0;
             if (tid < kT32) {
                 for (int k = 0; k < kLaneThreads; ++k) {
                     const uint32_t x = S.c32[tid][k];
-                    v = tid == 12 ? max(v, (unsigned long long)x) : tid == 13 ? (v | x) : v + x;
+                    v = tid == 10 ? max(v, (unsigned long long)x) : tid == 11 ? (v | x) : v + x;
                 }
             } else {
                 for (int k = 0; k < kLaneThreads; ++k) v += S.c64[tid - kT32][k];
             }
-            const uint32_t f = tid < kT32 ? kF32[tid] : kF64[tid - kT32];
+            red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
+        }
+        __syncthreads();
+        if (tid < 21) {
+            unsigned long long v;
+            if (tid == 2) v = red[1] - red[3] - red[4];  // completed
+            else if (tid == 7) v = red[5] - red[4] + red[6];  // restarts
+            else if (tid == 14) v = (unsigned long long)pol.idle_w * red[12] + (unsigned long long)pol.w_per_slice * red[16];
+            else v = red[tid];
             if (v) {
-                if (f == 13) atomicMax(dst + 13, v);
-                else if (f == 20) atomicOr(dst + 20, v);
-                else atomicAdd(dst + f, v);
+                if (tid == 13) atomicMax(dst + 13, v);
+                else if (tid == 20) atomicOr(dst + 20, v);
+                else atomicAdd(dst + tid, v);
             }
         }
     }
