@@ -15,7 +15,8 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof);
+                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint32_t* trans,
+                            uint32_t n_q);
 }  // namespace mig
 
 namespace {
@@ -105,6 +106,18 @@ mig_status device_geometry(const mig_geometry* gc, mig::DevGeom** out, int* dev_
         }
         g->dev[dev] = p;
     }
+    if (!g->trans_dev[dev] && !g->trans.empty()) {
+        uint32_t* t = nullptr;
+        const size_t bytes = g->trans.size() * sizeof(uint32_t);
+        e = cudaMalloc(&t, bytes);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(transitions)");
+        e = cudaMemcpy(t, g->trans.data(), bytes, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(t);
+            return cuda_fail(e, "cudaMemcpy(transitions)");
+        }
+        g->trans_dev[dev] = t;
+    }
     *out = g->dev[dev];
     *dev_out = dev;
     configure_pool(dev);
@@ -174,7 +187,8 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
     uint32_t nl = 0;
     e = timed("k_simulate", s, [&](uint32_t* tl) {
         cudaError_t e2 = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1,
-                                              sm_count_of(dev), s, &nl, g->dg.n_prof);
+                                              sm_count_of(dev), s, &nl, g->dg.n_prof, g->trans_dev[dev],
+                                              g->n_q);
         if (tl) *tl = nl;
         return e2;
     });
@@ -200,6 +214,7 @@ mig_geometry::~mig_geometry() {
             cudaGetDevice(&cur);
             cudaSetDevice(d);
             cudaFree(dev[d]);
+            if (trans_dev[d]) cudaFree(trans_dev[d]);
             cudaSetDevice(cur);
         }
 }

@@ -50,6 +50,56 @@ uint64_t count_maximal(const Tables& T, uint32_t s, uint32_t free_left, uint32_t
     return n;
 }
 
+// Slot-level transition table (mig_geometry::trans): breadth-first over states (occ, SM) from the empty GPU.
+// Placing q = (profile, start) destroys the instances whose slots it overlaps (the instances are the runs of
+// occupied slots cut at instance starts) and creates q. Left empty (n_q = 0) if the table would not fit 24-bit
+// state ids or 64 placements.
+void build_transitions(mig_geometry* g) {
+    const DevGeom& d = g->dg;
+    std::vector<uint32_t> qs;  // start | mask << 8, in (profile, k) order
+    for (uint32_t p = 0; p < d.n_prof; ++p)
+        for (uint32_t k = 0; k < d.n_place[p]; ++k) qs.push_back(d.place[p][k]);
+    g->trans.clear();
+    g->n_q = g->n_trans_states = 0;
+    if (qs.size() > 64) return;
+    const uint32_t nq = (uint32_t)qs.size();
+    std::vector<uint32_t> keys{0};  // occ | SM << 8
+    std::vector<int32_t> id(1u << 16, -1);
+    id[0] = 0;
+    std::vector<uint32_t> tab;
+    for (size_t i = 0; i < keys.size(); ++i) {
+        const uint32_t occ = keys[i] & 0xFFu, SM = keys[i] >> 8;
+        uint32_t EM = 0;  // last slot of every instance
+        for (uint32_t s = 0; s < d.n_slots; ++s) {
+            if (!((SM >> s) & 1u)) continue;
+            uint32_t e = s;
+            while (e + 1 < d.n_slots && ((occ >> (e + 1)) & 1u) && !((SM >> (e + 1)) & 1u)) ++e;
+            EM |= 1u << e;
+        }
+        for (uint32_t q = 0; q < nq; ++q) {
+            const uint32_t lo = qs[q] & 0xFFu, qm = qs[q] >> 8;
+            const uint32_t hi = 31u - (uint32_t)__builtin_clz(qm);
+            uint32_t a = lo, b = hi;
+            if ((occ >> lo) & 1u) a = 31u - (uint32_t)__builtin_clz(SM & ((2u << lo) - 1u));
+            if ((occ >> hi) & 1u) b = (uint32_t)__builtin_ctz(EM & ~((1u << hi) - 1u));
+            const uint32_t rm = occ & ((2u << b) - 1u) & ~((1u << a) - 1u);
+            const uint32_t nocc = (occ & ~rm) | qm, nSM = (SM & ~rm) | (1u << lo);
+            const uint32_t nd = (uint32_t)__builtin_popcount(SM & rm);
+            const uint32_t key = nocc | (nSM << 8);
+            if (id[key] < 0) {
+                id[key] = (int32_t)keys.size();
+                keys.push_back(key);
+            }
+            tab.push_back(((uint32_t)d.fcr[nocc] << 16) | ((15u - nd) << 8) | lo);
+            tab.push_back(rm | ((uint32_t)id[key] << 8));
+        }
+        if (keys.size() >= (1u << 24)) return;
+    }
+    g->trans.swap(tab);
+    g->n_q = nq;
+    g->n_trans_states = (uint32_t)keys.size();
+}
+
 // All sets of non-overlapping placements inside free_left (|S| when started from the empty GPU).
 uint64_t count_all(const Tables& T, uint32_t s, uint32_t free_left) {
     while (s < T.n_slots && !((free_left >> s) & 1u)) ++s;
@@ -278,6 +328,7 @@ mig_status load_geometry(const std::string& text, mig_geometry* g) {
             for (size_t k = 0; k < v.size(); ++k) d.alay[lvl][k] = v[k].first | (v[k].second << 8);
         }
     }
+    build_transitions(g);
     mig_geometry_info& in = g->info;
     snprintf(in.gpu_name, sizeof(in.gpu_name), "%s", g->name.c_str());
     in.n_slots = d.n_slots;

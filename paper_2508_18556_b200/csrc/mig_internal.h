@@ -45,8 +45,15 @@ struct mig_geometry {
     std::vector<std::string> prof_names;
     mig::DevGeom dg;
     uint32_t sms_per_slice = 0, warps_per_sm = 0;
-    std::mutex mu;                     // guards dev[]
+    // Slot-level partition states (occupancy, instance starts) reachable by placements, and for every state and
+    // placement q (index = sum of earlier profiles' starts + k): {fcr(result) << 16 | (15 - #destroyed) << 8 |
+    // start, destroyed-slot mask | next state << 8}, where placing q destroys the instances it overlaps (Alg. 2
+    // when nothing overlaps; fusion / fission R8 otherwise). Used by the lane kernel's FUSION_FISSION path.
+    std::vector<uint32_t> trans;       // [n_trans_states][n_q][2]
+    uint32_t n_trans_states = 0, n_q = 0;
+    std::mutex mu;                     // guards dev[] and trans_dev[]
     mig::DevGeom* dev[64] = {};        // per-device copy, uploaded on first use
+    uint32_t* trans_dev[64] = {};
     ~mig_geometry();
 };
 

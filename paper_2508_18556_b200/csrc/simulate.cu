@@ -940,7 +940,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
-                                 cudaStream_t stream);
+                                 const uint32_t* trans, uint32_t n_q, cudaStream_t stream);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
 // (8 or 32 lanes per trace).
@@ -958,7 +958,8 @@ bool simulate_use_lane() {
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof) {
+                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint32_t* trans,
+                            uint32_t n_q) {
     SimParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -985,14 +986,15 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     PA.counter = counter + 1;
     cudaError_t e = cudaSuccess;
     *launches = 0;
-    if (P.n_pol && simulate_use_lane() && n_prof <= 8) {  // the lane kernel packs idle masks per profile in a u64
+    // the lane kernel packs idle masks per profile in a u64 and takes fusion / fission from the transition table
+    if (P.n_pol && simulate_use_lane() && n_prof <= 8 && trans) {
         const uint64_t blocks = simulate_lane_grid(tr.n_traces, sm_count);
         uint16_t* ring = nullptr;
         e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * tr.max_jobs * sizeof(uint16_t), stream);
         if (e != cudaSuccess) return e;
         for (uint32_t k = 0; k < P.n_pol && e == cudaSuccess; ++k) {
             e = launch_simulate_lane(Gdev, tr, P.pol[k], P.pol_idx[k], n_pol, est, out, totals, counter + 2 + k,
-                                     est_err, ring, blocks, stream);
+                                     est_err, ring, blocks, trans, n_q, stream);
             ++*launches;
         }
         cudaFreeAsync(ring, stream);

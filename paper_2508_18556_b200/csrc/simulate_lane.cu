@@ -11,15 +11,17 @@
 //                                    reachability "can be precomputed offline"), so a decision is one LDS
 //   reuse (R7) ....... idle instance starts & a per-profile "tightly fits" mask over the per-slot
 //                                    profile nibbles (<= 7 idle instances, highest start first)
-//   fusion / fission (R8) .......... the instance boundary masks SM/EM, evaluated only when Alg. 2 fails
-//   next event (R28) ............... min over eight end-tick registers; ties by (kind, job) from shared memory
+//   fusion / fission (R8) .......... only when Alg. 2 fails: the candidates touching no busy slot (a table by busy
+//                                    mask) scored from the slot-level state's transition row (host-built, global
+//                                    memory, L1-resident): fcr(result), #destroyed, destroyed slots, next state
+//   next event (R28) ............... min over the eight per-slot end ticks; ties by (kind, job) (shared memory)
 // The loop is a flat state machine (PASS: one head evaluation; EVT: one event; FIN: write the unit's result and take
 // the next unit), so the 32 lanes of a warp stay in one loop even though their traces are at different points:
 // the cost of an iteration is the sum of the branches present in the warp, not the slowest trace. Units are taken
 // from an atomic counter one ahead (lane-level work stealing); per-policy totals are per-lane shared-memory partials
 // reduced once per CTA.
 //
-// Per-lane state: occupancy occ, instance starts SM / ends EM, busy starts BS / busy slots BM (u8 masks), profile
+// Per-lane state: occupancy occ, instance starts SM, slot-level state id sid, busy starts BS / busy slots BM, profile
 // nibble per start slot (prof4), end tick and job|kind per start slot (shared memory, [slot][lane]),
 // the head job's record (prefetched when the queue advances), a requeue FIFO in global scratch (rare: OOM /
 // preempt restarts, R13), packed 16-bit counters, FNV-1a-64 hash halves, four u64 accumulators.
@@ -44,6 +46,8 @@ struct LaneParams {
     unsigned long long* counter;
     const unsigned long long* est_err;  // error word of k_estimate (merged into this policy's totals)
     uint16_t* ring;                     // [grid threads][ring_cap] requeue FIFOs: job | need << 10 (15 = none)
+    const uint2* trans;                 // mig_geometry::trans, [state][n_q] (FUSION_FISSION)
+    uint32_t n_q;
     uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
     mig_policy pol;
 };
@@ -62,7 +66,8 @@ __constant__ const uint8_t kF64[kT64] = {12, 15, 16, 17, 18, 19};
 
 struct LaneShared {
     DevGeom G;
-    uint8_t alloc[256 * 8];   // Alg. 2 result by (occupancy, profile): start, or 0xFF = FAIL
+    uint8_t alloc[256 * 8];   // Alg. 2 result by (occupancy, profile): placement index k, or 0xFF = FAIL
+    uint8_t qbase[8];         // transition-table column of placement 0 of profile p
     uint8_t nobusy[256 * 8];  // FF: placements k of profile p (bit k) that touch no busy slot, by busy-slot mask
     unsigned long long reuse_sel[16];  // FF: byte q = 0xFF if an idle instance of profile q tightly fits profile p
                                        // (same memory, compute >=; R7), selecting from the idle-by-profile masks
@@ -110,18 +115,11 @@ __device__ __forceinline__ uint32_t lane_wave_ticks(const DevGeom& G, uint32_t t
     return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
 }
 
-__device__ __forceinline__ uint32_t lane_overlap_extent(uint32_t occ, uint32_t SM, uint32_t EM, uint32_t lo,
-                                                        uint32_t hi) {
-    const uint32_t a = ((occ >> lo) & 1u) ? 31u - __clz(SM & ((2u << lo) - 1u)) : lo;
-    const uint32_t b = ((occ >> hi) & 1u) ? (uint32_t)__ffs(EM & ~((1u << hi) - 1u)) - 1u : hi;
-    return occ & ((2u << b) - 1u) & ~((1u << a) - 1u);
-}
-
 template <int KIND>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) LaneShared S;
-    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    const uint32_t tid = threadIdx.x;
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
         uint32_t* dst = reinterpret_cast<uint32_t*>(&S.G);
@@ -136,15 +134,18 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         const DevGeom& G = S.G;
         for (uint32_t i = tid; i < 256 * 8; i += blockDim.x) {  // Alg. 2 for every (occupancy, profile)
             const uint32_t occ = i >> 3, p = i & 7u;
-            uint32_t best = 0;
+            uint32_t best = 0, bk = 0xFFu;
             if (p < G.n_prof && occ < (1u << G.n_slots)) {
                 for (uint32_t k = 0; k < G.n_place[p]; ++k) {
                     const uint32_t pl = G.place[p][k], qm = pl >> 8;
                     const uint32_t score = (pl && !(occ & qm)) ? ((uint32_t)G.fcr[occ | qm] << 8) | (pl & 0xFFu) : 0u;
-                    best = max(best, score);
+                    if (score > best) {
+                        best = score;
+                        bk = k;
+                    }
                 }
             }
-            S.alloc[i] = best ? (uint8_t)(best & 0xFFu) : (uint8_t)0xFFu;
+            S.alloc[i] = (uint8_t)bk;
             uint32_t nb = 0;  // here occ plays the busy-slot mask BM
             if (p < G.n_prof)
                 for (uint32_t k = 0; k < G.n_place[p]; ++k) nb |= ((G.place[p][k] >> 8) & occ) ? 0u : 1u << k;
@@ -165,6 +166,13 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 if ((ok >> q) & 1u) sel |= 0xFFull << (8 * q);
             S.reuse_sel[tid] = sel;
             S.scand[tid] = (uint8_t)sc;
+        }
+        if (tid == 0) {
+            uint32_t qb = 0;
+            for (uint32_t p = 0; p < 8; ++p) {
+                S.qbase[p] = (uint8_t)qb;
+                qb += p < G.n_prof ? G.n_place[p] : 0u;
+            }
         }
         if (tid < 8) {
             uint32_t f = 0xFFu;
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     unsigned long long tr_next = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
     uint64_t j0 = 0;
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
-    uint32_t occ = 0, SM = 0, EM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0;
+    uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0, sid = 0;
     uint64_t IPM = 0;  // FF: idle instances by profile, byte p bit s = an idle instance of profile p starts at s
     uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
     uint64_t a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         }
         t = qh = rh = rn = evm = 0;
         BS = BM = 0;
-        occ = SM = EM = prof4 = 0;
+        occ = SM = prof4 = sid = 0;
         IPM = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) et[k * kLaneThreads] = kNoEnd;
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             // warp reconverged between phases: every decision path then shares one copy of the common code.
             if (mode == 0 && hj == kNoJob) mode = 1;
             const bool pass = mode == 0;
-            uint32_t j = 0, need = 0, s = 0, kd = 0, nd = 0, pr = 0, lo = 0, cm = 0;
+            uint32_t j = 0, need = 0, s = 0, kd = 0, nd = 0, pr = 0, lo = 0, qk = 0;
             if (pass) {
                 j = hj;
                 need = head_need();
@@ -410,73 +418,46 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         }
                     }
                     if (!kd) {
-                        const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2
+                        const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2: placement k
                         if (a != 0xFFu) {
-                            s = a;
+                            s = G.place[need][a] & 0xFFu;
+                            qk = a;
                             kd = K_ALLOC;
                         } else {
                             // fusion / fission candidates: placements touching no busy slot (none: WAIT)
-                            if (KIND == MIG_FUSION_FISSION && (SM & ~BS)) cm = S.nobusy[(BM << 3) | need];
-                            if (!cm) {  // sleep() until a running job finishes
+                            const uint32_t cm =
+                                (KIND == MIG_FUSION_FISSION && (SM & ~BS)) ? S.nobusy[(BM << 3) | need] : 0u;
+                            if (KIND == MIG_FUSION_FISSION && cm) {
+                                // A7 (R8): placement k destroys the idle instances it overlaps;
+                                // best (fcr(result), -#destroyed, start), read from the state's transition row
+                                const uint2* row = P.trans + (size_t)sid * P.n_q + S.qbase[need];
+                                uint32_t best = 0, by = 0;
+                                for (uint32_t m = cm; m; m &= m - 1u) {
+                                    const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                                    if ((G.place[need][k] >> 8) & occ) {
+                                        const uint2 e = __ldg(row + k);
+                                        if (e.x > best) {
+                                            best = e.x;
+                                            by = e.y;
+                                        }
+                                    }
+                                }
+                                if (best) {
+                                    s = best & 0xFFu;
+                                    nd = 15u - ((best >> 8) & 0xFFu);
+                                    const uint32_t rm = by & 0xFFu;
+                                    IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
+                                    occ &= ~rm;
+                                    SM &= ~rm;
+                                    sid = by >> 8;
+                                    kd = K_RECONF;
+                                }
+                            }
+                            if (!kd) {  // sleep() until a running job finishes
                                 kd = K_WAIT;
                                 lo = jsh | (K_WAIT << 12) | 0xF00u | (need << 4);
                             }
                         }
-                    }
-                }
-            }
-            if (KIND == MIG_FUSION_FISSION) {
-                // ---- A7: fusion / fission (R8), warp-cooperative: each requesting lane's
-                // candidate placements are scored by eight lanes: destroy the idle instances placement k overlaps
-                // (none busy, >= 1); best (fcr(result), -#destroyed, start) ----
-                __syncwarp();
-                uint32_t a7m = __ballot_sync(FULL, cm != 0), a7rm = 0;
-                while (a7m) {  // up to four requests per round: lanes 8r..8r+7 score request r's placements
-                    const uint32_t r = lane >> 3, k = lane & 7u;
-                    const uint32_t m1 = a7m & (a7m - 1u), m2 = m1 & (m1 - 1u), m3 = m2 & (m2 - 1u);
-                    const uint32_t mr = r == 0 ? a7m : r == 1 ? m1 : r == 2 ? m2 : m3;
-                    const uint32_t src = mr ? (uint32_t)__ffs(mr) - 1u : 0u;
-                    const uint32_t o = __shfl_sync(FULL, occ, src), sm = __shfl_sync(FULL, SM, src),
-                                   em = __shfl_sync(FULL, EM, src), nn = __shfl_sync(FULL, need, src),
-                                   c = __shfl_sync(FULL, cm, src);
-                    uint32_t sc = 0, rm = 0;
-                    if (mr && ((c >> k) & 1u)) {
-                        const uint32_t pl = G.place[nn][k], qm = pl >> 8;
-                        if (qm & o) {
-                            const uint32_t ql = pl & 0xFFu, nlen = (G.pinfo[nn] >> 16) & 0xFu;
-                            rm = lane_overlap_extent(o, sm, em, ql, ql + nlen - 1u);
-                            // (fcr(result), -#destroyed, start); the scoring lane k rides in the low bits
-                            sc = ((uint32_t)G.fcr[(o & ~rm) | qm] << 16) | ((15u - __popc(sm & rm)) << 8) | (ql << 3) |
-                                 k;
-                        }
-                    }
-                    sc = max(sc, __shfl_xor_sync(FULL, sc, 1));
-                    sc = max(sc, __shfl_xor_sync(FULL, sc, 2));
-                    sc = max(sc, __shfl_xor_sync(FULL, sc, 4));
-                    // requester of round slot rr (its rank among the round's requests) reads lane 8 * rr
-                    const uint32_t rr = __popc(a7m & ((1u << lane) - 1u));
-                    const uint32_t best = __shfl_sync(FULL, sc, (rr & 3u) * 8u);
-                    const uint32_t brm = __shfl_sync(FULL, rm, (rr & 3u) * 8u + (best & 7u));
-                    if (((a7m >> lane) & 1u) && rr < 4) {
-                        cm = best | 0x80000000u;
-                        a7rm = brm;
-                    }
-                    a7m = m3 & (m3 - 1u);
-                }
-                if (cm) {
-                    const uint32_t bs = cm & 0x7FFFFFFFu;
-                    if (bs) {
-                        s = (bs >> 3) & 0x1Fu;
-                        nd = 15u - ((bs >> 8) & 0xFFu);
-                        const uint32_t rm = a7rm;
-                        IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
-                        occ &= ~rm;
-                        SM &= ~rm;
-                        EM &= ~rm;
-                        kd = K_RECONF;
-                    } else {
-                        kd = K_WAIT;
-                        lo = (j << 16) | (K_WAIT << 12) | 0xF00u | (need << 4);
                     }
                 }
             }
@@ -486,11 +467,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 const bool created = kd == K_ALLOC || kd == K_RECONF;
                 const bool place = kd != K_WAIT && kd != K_REJECT;
                 if (created) {
-                    const uint32_t pn = G.pinfo[need];
-                    occ |= ((pn >> 8) & 0xFFu) << s;
+                    occ |= ((G.pinfo[need] >> 8) & 0xFFu) << s;
                     if (KIND == MIG_FUSION_FISSION) {
                         SM |= 1u << s;
-                        EM |= 1u << (s + ((pn >> 16) & 0xFu) - 1u);
+                        if (kd == K_ALLOC) sid = __ldg(P.trans + (size_t)sid * P.n_q + S.qbase[need] + qk).y >> 8;
                     }
                     prof4 = (prof4 & ~(0xFu << (4 * s))) | (need << (4 * s));
                 }
@@ -686,7 +666,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
-                                 cudaStream_t stream) {
+                                 const uint32_t* trans, uint32_t n_q, cudaStream_t stream) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -705,6 +685,8 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     P.n_pol_all = n_pol_all;
     P.pol_idx = pol_idx;
     P.pol = pol;
+    P.trans = reinterpret_cast<const uint2*>(trans);
+    P.n_q = n_q;
     const dim3 grid((unsigned)blocks), block(kLaneThreads);
     switch (pol.kind) {
         case MIG_BASELINE: k_simulate_lane<MIG_BASELINE><<<grid, block, 0, stream>>>(Gdev, P); break;
