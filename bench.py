@@ -339,14 +339,26 @@ def run_mine(args):
     peaks, peak_src = measured_peaks()
     f_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 4 * 32 * f_mhz * 1e6  # lane-ops/s: 4 SMSPs x 1 warp-instruction/cycle x 32 lanes per SM
-    ops_sim = (OPS_PER_DECISION * dec_step + OPS_PER_EVENT * events_step + OPS_PER_JOB_STAGE * jobs_step * n_pol) / world
-    achieved = ops_sim / (sim_ms * 1e-3)
+    # Roofline of the dominant launch (the longest per-policy simulation launch, timed by CUDA events on the
+    # launching stream through mig_timing_enable): algorithmic lane-ops of that policy's decisions and events
+    # (DESIGN.md ops model) / its average launch duration, against the issue peak.
+    launch_ms = {k: v[0] / args.steps for k, v in ktimes.items() if k.startswith("sim_")}
+    dom = max(launch_ms, key=launch_ms.get) if launch_ms else "k_simulate"
+    dom_ms = launch_ms.get(dom, sim_ms)
+    kind_of = {"sim_baseline": 0, "sim_static": 1, "sim_dynamic": 2, "sim_ff": 3}
+    dom_pols = [i for i, (k, f) in enumerate(wl["policies"]) if k == kind_of.get(dom, -1)] or list(range(n_pol))
+    dom_dec = sum(int(totals[i]["placements"]) + int(totals[i]["waits"]) + int(totals[i]["rejected"]) for i in dom_pols)
+    dom_ev = sum(int(totals[i]["placements"]) for i in dom_pols)
+    dom_launches = max(1, ktimes.get(dom, (0, args.steps))[1] // args.steps) if dom in ktimes else 1
+    ops_dom = (OPS_PER_DECISION * dom_dec + OPS_PER_EVENT * dom_ev +
+               OPS_PER_JOB_STAGE * jobs_step * len(dom_pols)) / world / dom_launches
+    achieved = ops_dom / (dom_ms / dom_launches * 1e-3)
     traffic, ncu = None, {}
     prof = os.path.join(ROOT, "profiles", f"ncu_config{cfg}.json")
     if os.path.exists(prof) and n_per == wl["traces"]:
         with open(prof) as f:
             ncu = json.load(f)
-        traffic = ncu.get("k_simulate_dram_bytes_per_launch")
+        traffic = ncu.get(f"{dom}_dram_bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": "decisions/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -358,23 +370,24 @@ def run_mine(args):
                    "decisions_per_step": dec_step, "parallelism": f"trace-sharded x{world}",
                    "l2": f"inputs ({tr.n_jobs * 16 / 1e9:.2f} GB/GPU) larger than L2; no flush"},
         "kernels": {"k_estimate_ms": est_ms, "k_simulate_ms": sim_ms,
-                    "k_simulate_share": sim_ms / ms_per_step},
-        "roofline": {"bound": "alu", "kernel": "k_simulate", "achieved": achieved, "peak": alu_peak,
+                    "k_simulate_share": sim_ms / ms_per_step, "launch_ms": launch_ms,
+                    "dominant_share": dom_ms / ms_per_step},
+        "roofline": {"bound": "alu", "kernel": f"k_simulate_lane ({dom})", "achieved": achieved, "peak": alu_peak,
                      "unit": "int lane-ops/s", "frac": achieved / alu_peak, "traffic": traffic,
                      "peak_source": f"148 SMs x 4 SMSP x 32 lanes x {f_mhz:.0f} MHz ({peak_src} sm_max_mhz)",
                      "ops_model": f"{OPS_PER_DECISION}/decision + {OPS_PER_EVENT}/event + "
                                   f"{OPS_PER_JOB_STAGE}/job/policy (DESIGN.md)",
-                     "ncu_issue_slot_util": ncu.get("k_simulate_issue_slot_util"),
-                     "ncu_active_lanes_per_instr": ncu.get("k_simulate_active_lanes_per_instr"),
+                     "ncu_issue_slot_util": ncu.get(f"{dom}_issue_slot_util"),
+                     "ncu_active_lanes_per_instr": ncu.get(f"{dom}_active_lanes_per_instr"),
                      "ncu_source": ncu.get("source")},
-        "hbm": {"algorithmic_bytes_per_launch": tr.n_jobs * 16 + n_per * n_pol * 96,
-                "peak_gbs": peaks.get("hbm_gbs")},
+        # secondary roofline: a launch reads every job record once and writes one 96 B result per trace
+        "hbm": {"algorithmic_bytes_per_launch": tr.n_jobs * 16 + n_per * 96, "peak_gbs": peaks.get("hbm_gbs")},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
     }
-    line["hbm"]["achieved_gbs"] = line["hbm"]["algorithmic_bytes_per_launch"] / (sim_ms * 1e-3) / 1e9
+    line["hbm"]["achieved_gbs"] = line["hbm"]["algorithmic_bytes_per_launch"] / (dom_ms / dom_launches * 1e-3) / 1e9
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

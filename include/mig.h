@@ -227,9 +227,11 @@ mig_status mig_workspace_bytes(const char* cublas_workspace_config, uint32_t n_l
 uint32_t mig_last_launch_count(void);
 
 /* Kernel timing (bench accounting). While enabled on a thread, every device call of that thread brackets its
- * kernel launches with CUDA events on the call's stream, grouped as "k_estimate" (the estimation kernel) and
- * "k_simulate" (all simulation kernels of the call). mig_timing_query synchronises the recorded events, writes up
- * to cap entries {name, total milliseconds, launch count} and clears the record. Enabling or disabling clears it. */
+ * kernel launches with CUDA events on the call's stream, grouped as "k_estimate" (the estimation kernel),
+ * "k_simulate" (all simulation kernels of the call) and, inside it, one group per lane-kernel policy launch
+ * ("sim_baseline", "sim_static", "sim_dynamic", "sim_ff"). mig_timing_query synchronises the recorded events,
+ * writes up to cap entries {name, total milliseconds, launch count} and clears the record. Enabling or disabling
+ * clears it. */
 typedef struct {
     char name[16];
     double ms;

@@ -256,6 +256,14 @@ mig_status mig_workspace_bytes(const char* cfg, uint32_t n_layers, uint64_t* byt
 
 uint32_t mig_last_launch_count(void) { return t_launches; }
 
+}  // extern "C"
+
+int mig_timed(const char* name, mig_stream_t stream, const std::function<int(uint32_t*)>& f) {
+    return (int)timed(name, (cudaStream_t)stream, [&](uint32_t* nl) { return (cudaError_t)f(nl); });
+}
+
+extern "C" {
+
 void mig_timing_enable(int on) {
     clear_recs();
     t_timing = on != 0;

@@ -60,3 +60,9 @@ struct mig_geometry {
 // error helpers (capi.cu)
 mig_status mig_set_error(mig_status s, const std::string& msg);
 void mig_note_launches(uint32_t n);
+
+// mig_timing_enable support (capi.cu): when timing is on for this thread, records events on `stream` around the
+// launches issued by f (f returns a cudaError_t and the number of launches through its argument) under `name`.
+#include <functional>
+typedef struct CUstream_st* mig_stream_t;
+int mig_timed(const char* name, mig_stream_t stream, const std::function<int(uint32_t*)>& f);

@@ -992,9 +992,13 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
         uint16_t* ring = nullptr;
         e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * tr.max_jobs * sizeof(uint16_t), stream);
         if (e != cudaSuccess) return e;
+        static const char* kNames[4] = {"sim_baseline", "sim_static", "sim_dynamic", "sim_ff"};
         for (uint32_t k = 0; k < P.n_pol && e == cudaSuccess; ++k) {
-            e = launch_simulate_lane(Gdev, tr, P.pol[k], P.pol_idx[k], n_pol, est, out, totals, counter + 2 + k,
-                                     est_err, ring, blocks, trans, n_q, stream);
+            e = (cudaError_t)mig_timed(kNames[P.pol[k].kind & 3u], stream, [&](uint32_t* nl) {
+                if (nl) *nl = 1;
+                return (int)launch_simulate_lane(Gdev, tr, P.pol[k], P.pol_idx[k], n_pol, est, out, totals,
+                                                 counter + 2 + k, est_err, ring, blocks, trans, n_q, stream);
+            });
             ++*launches;
         }
         cudaFreeAsync(ring, stream);
