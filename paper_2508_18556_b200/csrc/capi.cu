@@ -16,7 +16,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
                             cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint32_t* trans,
-                            uint32_t n_q);
+                            uint32_t n_q, const uint32_t* a7, uint32_t n_a7);
 }  // namespace mig
 
 namespace {
@@ -118,6 +118,18 @@ mig_status device_geometry(const mig_geometry* gc, mig::DevGeom** out, int* dev_
         }
         g->trans_dev[dev] = t;
     }
+    if (!g->a7_dev[dev] && !g->a7.empty()) {
+        uint32_t* t = nullptr;
+        const size_t bytes = g->a7.size() * sizeof(uint32_t);
+        e = cudaMalloc(&t, bytes);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(fusion/fission table)");
+        e = cudaMemcpy(t, g->a7.data(), bytes, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(t);
+            return cuda_fail(e, "cudaMemcpy(fusion/fission table)");
+        }
+        g->a7_dev[dev] = t;
+    }
     *out = g->dev[dev];
     *dev_out = dev;
     configure_pool(dev);
@@ -188,7 +200,7 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
     e = timed("k_simulate", s, [&](uint32_t* tl) {
         cudaError_t e2 = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1,
                                               sm_count_of(dev), s, &nl, g->dg.n_prof, g->trans_dev[dev],
-                                              g->n_q);
+                                              g->n_q, g->a7_dev[dev], g->n_a7);
         if (tl) *tl = nl;
         return e2;
     });
@@ -215,6 +227,7 @@ mig_geometry::~mig_geometry() {
             cudaSetDevice(d);
             cudaFree(dev[d]);
             if (trans_dev[d]) cudaFree(trans_dev[d]);
+            if (a7_dev[d]) cudaFree(a7_dev[d]);
             cudaSetDevice(cur);
         }
 }

@@ -60,7 +60,8 @@ void build_transitions(mig_geometry* g) {
     for (uint32_t p = 0; p < d.n_prof; ++p)
         for (uint32_t k = 0; k < d.n_place[p]; ++k) qs.push_back(d.place[p][k]);
     g->trans.clear();
-    g->n_q = g->n_trans_states = 0;
+    g->a7.clear();
+    g->n_q = g->n_a7 = g->n_trans_states = 0;
     if (qs.size() > 64) return;
     const uint32_t nq = (uint32_t)qs.size();
     std::vector<uint32_t> keys{0};  // occ | SM << 8
@@ -95,8 +96,36 @@ void build_transitions(mig_geometry* g) {
         }
         if (keys.size() >= (1u << 24)) return;
     }
+    // fusion / fission answers per (state, profile, candidate mask)
+    uint32_t na7 = 0;
+    for (uint32_t p = 0; p < d.n_prof; ++p) na7 += 1u << d.n_place[p];
+    std::vector<uint32_t> a7((size_t)keys.size() * na7 * 2, 0u);
+    for (size_t i = 0; i < keys.size(); ++i) {
+        const uint32_t occ = keys[i] & 0xFFu;
+        uint32_t base = 0, qb = 0;
+        for (uint32_t p = 0; p < d.n_prof; ++p) {
+            const uint32_t np = d.n_place[p];
+            for (uint32_t c = 0; c < (1u << np); ++c) {
+                uint32_t bx = 0, by = 0;
+                for (uint32_t k = 0; k < np; ++k) {
+                    if (!((c >> k) & 1u) || !((d.place[p][k] >> 8) & occ)) continue;
+                    const uint32_t* e = &tab[(i * nq + qb + k) * 2];
+                    if (e[0] > bx) {
+                        bx = e[0];
+                        by = e[1];
+                    }
+                }
+                a7[(i * na7 + base + c) * 2] = bx;
+                a7[(i * na7 + base + c) * 2 + 1] = by;
+            }
+            base += 1u << np;
+            qb += np;
+        }
+    }
     g->trans.swap(tab);
+    g->a7.swap(a7);
     g->n_q = nq;
+    g->n_a7 = na7;
     g->n_trans_states = (uint32_t)keys.size();
 }
 

@@ -940,7 +940,8 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
-                                 const uint32_t* trans, uint32_t n_q, cudaStream_t stream);
+                                 const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
+                                 cudaStream_t stream);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
 // (8 or 32 lanes per trace).
@@ -959,7 +960,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
                             cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint32_t* trans,
-                            uint32_t n_q) {
+                            uint32_t n_q, const uint32_t* a7, uint32_t n_a7) {
     SimParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -987,7 +988,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     cudaError_t e = cudaSuccess;
     *launches = 0;
     // the lane kernel packs idle masks per profile in a u64 and takes fusion / fission from the transition table
-    if (P.n_pol && simulate_use_lane() && n_prof <= 8 && trans) {
+    if (P.n_pol && simulate_use_lane() && n_prof <= 8 && trans && a7) {
         const uint64_t blocks = simulate_lane_grid(tr.n_traces, sm_count);
         uint16_t* ring = nullptr;
         e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * tr.max_jobs * sizeof(uint16_t), stream);
@@ -997,7 +998,8 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
             e = (cudaError_t)mig_timed(kNames[P.pol[k].kind & 3u], stream, [&](uint32_t* nl) {
                 if (nl) *nl = 1;
                 return (int)launch_simulate_lane(Gdev, tr, P.pol[k], P.pol_idx[k], n_pol, est, out, totals,
-                                                 counter + 2 + k, est_err, ring, blocks, trans, n_q, stream);
+                                                 counter + 2 + k, est_err, ring, blocks, trans, n_q, a7, n_a7,
+                                                 stream);
             });
             ++*launches;
         }

@@ -47,7 +47,8 @@ struct LaneParams {
     const unsigned long long* est_err;  // error word of k_estimate (merged into this policy's totals)
     uint16_t* ring;                     // [grid threads][ring_cap] requeue FIFOs: job | need << 10 (15 = none)
     const uint2* trans;                 // mig_geometry::trans, [state][n_q] (FUSION_FISSION)
-    uint32_t n_q;
+    const uint2* a7;                    // mig_geometry::a7, [state][n_a7] (FUSION_FISSION)
+    uint32_t n_q, n_a7;
     uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
     mig_policy pol;
 };
@@ -68,6 +69,7 @@ struct LaneShared {
     DevGeom G;
     uint8_t alloc[256 * 8];   // Alg. 2 result by (occupancy, profile): placement index k, or 0xFF = FAIL
     uint8_t qbase[8];         // transition-table column of placement 0 of profile p
+    uint16_t cbase[8];        // fusion/fission-table column of candidate mask 0 of profile p
     uint8_t nobusy[256 * 8];  // FF: placements k of profile p (bit k) that touch no busy slot, by busy-slot mask
     unsigned long long reuse_sel[16];  // FF: byte q = 0xFF if an idle instance of profile q tightly fits profile p
                                        // (same memory, compute >=; R7), selecting from the idle-by-profile masks
@@ -168,10 +170,12 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             S.scand[tid] = (uint8_t)sc;
         }
         if (tid == 0) {
-            uint32_t qb = 0;
+            uint32_t qb = 0, cb = 0;
             for (uint32_t p = 0; p < 8; ++p) {
                 S.qbase[p] = (uint8_t)qb;
+                S.cbase[p] = (uint16_t)cb;
                 qb += p < G.n_prof ? G.n_place[p] : 0u;
+                cb += p < G.n_prof ? 1u << G.n_place[p] : 0u;
             }
         }
         if (tid < 8) {
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             }
         } else {
             // ---- PASS: evaluate the head of the queue (Alg. 4, one decision) ----
-            // P1 (local decision) | A7 (fusion/fission, warp-cooperative) | P2 (record, run start, pop), with the
+            // P1 (local decision, incl. fusion/fission A7) | P2 (record, run start, pop), with the
             // warp reconverged between phases: every decision path then shares one copy of the common code.
             if (mode == 0 && hj == kNoJob) mode = 1;
             const bool pass = mode == 0;
@@ -429,19 +433,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                                 (KIND == MIG_FUSION_FISSION && (SM & ~BS)) ? S.nobusy[(BM << 3) | need] : 0u;
                             if (KIND == MIG_FUSION_FISSION && cm) {
                                 // A7 (R8): placement k destroys the idle instances it overlaps;
-                                // best (fcr(result), -#destroyed, start), read from the state's transition row
-                                const uint2* row = P.trans + (size_t)sid * P.n_q + S.qbase[need];
-                                uint32_t best = 0, by = 0;
-                                for (uint32_t m = cm; m; m &= m - 1u) {
-                                    const uint32_t k = (uint32_t)__ffs(m) - 1u;
-                                    if ((G.place[need][k] >> 8) & occ) {
-                                        const uint2 e = __ldg(row + k);
-                                        if (e.x > best) {
-                                            best = e.x;
-                                            by = e.y;
-                                        }
-                                    }
-                                }
+                                // best (fcr(result), -#destroyed, start) over the candidates c, one table entry
+                                // per (slot-level state, profile, c) (host-built, mig_geometry::a7)
+                                const uint2 e = __ldg(P.a7 + (size_t)sid * P.n_a7 + S.cbase[need] + cm);
+                                const uint32_t best = e.x, by = e.y;
                                 if (best) {
                                     s = best & 0xFFu;
                                     nd = 15u - ((best >> 8) & 0xFFu);
@@ -666,7 +661,8 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
-                                 const uint32_t* trans, uint32_t n_q, cudaStream_t stream) {
+                                 const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
+                                 cudaStream_t stream) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -687,6 +683,8 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     P.pol = pol;
     P.trans = reinterpret_cast<const uint2*>(trans);
     P.n_q = n_q;
+    P.a7 = reinterpret_cast<const uint2*>(a7);
+    P.n_a7 = n_a7;
     const dim3 grid((unsigned)blocks), block(kLaneThreads);
     switch (pol.kind) {
         case MIG_BASELINE: k_simulate_lane<MIG_BASELINE><<<grid, block, 0, stream>>>(Gdev, P); break;
