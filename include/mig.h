@@ -99,6 +99,14 @@ mig_status mig_geometry_fcr(const mig_geometry* g, uint32_t occ_mask, uint32_t* 
  * `profile` maximising fcr (equal fcr: highest start), or -1 = FAIL. Host-only test hook. */
 mig_status mig_geometry_place(const mig_geometry* g, uint32_t occ_mask, uint32_t profile, int32_t* start);
 
+/* Fusion / fission (reading R8) on the partition with occupancy occ_mask and instance starts
+ * start_mask (bit i = an instance starts at memory slot i), busy_mask = the slots of busy instances: among the
+ * placements of `profile` that overlap at least one instance and no busy slot, the one maximising (fcr of the
+ * result, -#destroyed instances, start). *start = its start (-1 = none), *destroyed = the slots of the destroyed
+ * instances. Answered from the slot-level tables the simulation kernel uses. Host-only test hook. */
+mig_status mig_geometry_fusion(const mig_geometry* g, uint32_t occ_mask, uint32_t start_mask, uint32_t busy_mask,
+                               uint32_t profile, int32_t* start, uint32_t* destroyed);
+
 /* ------------------------------------------------------------------------------------------------------------------
  * Traces (job queues). All jobs of a trace arrive at t = 0 (batch).
  * Record format (tracegen/tracegen.h documents the same layout):

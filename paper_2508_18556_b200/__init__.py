@@ -76,6 +76,8 @@ _lib.mig_geometry_profile.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint
                                       C.POINTER(C.c_uint32), C.c_char_p]
 _lib.mig_geometry_fcr.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]
 _lib.mig_geometry_place.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_int32)]
+_lib.mig_geometry_fusion.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_uint32)]
 _lib.mig_estimate_memory.argtypes = [C.c_void_p, C.POINTER(mig_traces), C.POINTER(mig_policy), C.c_void_p,
                                      C.c_void_p]
 _lib.mig_simulate.argtypes = [C.c_void_p, C.POINTER(mig_traces), C.POINTER(mig_policy), C.c_uint32, C.c_void_p,
@@ -152,6 +154,13 @@ def mig_geometry_place(g: Geometry, occ: int, profile: int) -> int:
     out = C.c_int32()
     _check(_lib.mig_geometry_place(g.h, occ, profile, C.byref(out)))
     return out.value
+
+
+def mig_geometry_fusion(g: Geometry, occ: int, starts: int, busy: int, profile: int):
+    """Fusion/fission test hook (include/mig.h): (start or -1, destroyed-slot mask)."""
+    st, dm = C.c_int32(), C.c_uint32()
+    _check(_lib.mig_geometry_fusion(g.h, occ, starts, busy, profile, C.byref(st), C.byref(dm)))
+    return st.value, dm.value
 
 
 def policy(g: Geometry | None = None, kind=MIG_FUSION_FISSION, flags=0, ctx_mib=512, reconfig_ticks=500,

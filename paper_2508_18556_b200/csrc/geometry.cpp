@@ -124,6 +124,7 @@ void build_transitions(mig_geometry* g) {
     }
     g->trans.swap(tab);
     g->a7.swap(a7);
+    g->trans_id.swap(id);
     g->n_q = nq;
     g->n_a7 = na7;
     g->n_trans_states = (uint32_t)keys.size();
@@ -443,6 +444,25 @@ mig_status mig_geometry_place(const mig_geometry* g, uint32_t occ, uint32_t prof
         if (score > best) best = score;
     }
     *start = best ? (int32_t)(best & 0xFF) : -1;
+    return MIG_OK;
+}
+
+mig_status mig_geometry_fusion(const mig_geometry* g, uint32_t occ, uint32_t sm, uint32_t busy, uint32_t profile,
+                               int32_t* start, uint32_t* destroyed) {
+    if (!g || !start || !destroyed) return mig_set_error(MIG_E_INVALID_ARG, "mig_geometry_fusion: null argument");
+    const DevGeom& d = g->dg;
+    if (profile >= d.n_prof) return mig_set_error(MIG_E_INVALID_ARG, "profile index out of range");
+    if (g->a7.empty()) return mig_set_error(MIG_E_UNSUPPORTED, "no slot-level tables for this geometry");
+    const uint32_t key = (occ & 0xFFu) | ((sm & 0xFFu) << 8);
+    if (occ > 0xFFu || sm > 0xFFu || g->trans_id[key] < 0)
+        return mig_set_error(MIG_E_INVALID_ARG, "(occupancy, starts) is not a reachable partition state");
+    uint32_t cm = 0, cbase = 0;
+    for (uint32_t p = 0; p < profile; ++p) cbase += 1u << d.n_place[p];
+    for (uint32_t k = 0; k < d.n_place[profile]; ++k)
+        if (!((d.place[profile][k] >> 8) & busy)) cm |= 1u << k;
+    const uint32_t* e = &g->a7[((size_t)g->trans_id[key] * g->n_a7 + cbase + cm) * 2];
+    *start = e[0] ? (int32_t)(e[0] & 0xFFu) : -1;
+    *destroyed = e[0] ? (e[1] & 0xFFu) : 0u;
     return MIG_OK;
 }
 

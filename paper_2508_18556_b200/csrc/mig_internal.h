@@ -50,6 +50,7 @@ struct mig_geometry {
     // start, destroyed-slot mask | next state << 8}, where placing q destroys the instances it overlaps (Alg. 2
     // when nothing overlaps; fusion / fission R8 otherwise). Used by the lane kernel's FUSION_FISSION path.
     std::vector<uint32_t> trans;       // [n_trans_states][n_q][2]
+    std::vector<int32_t> trans_id;     // state id by occ | start mask << 8 (-1 = not a reachable state)
     uint32_t n_trans_states = 0, n_q = 0;
     // Fusion / fission answers (R8) by (state, profile p, candidate mask c over p's placements): the entry of the
     // best placement k in c that overlaps an instance ({0, 0} if none). Row = n_a7 entries, profile p's block

@@ -95,3 +95,46 @@ def test_timing_hook_without_launches():
     mig.mig_timing_enable(True)
     assert mig.mig_timing_query() == {}
     mig.mig_timing_enable(False)
+
+
+@pytest.mark.parametrize("name", ["a30-24gb", "a100-40gb", "a100-40gb-1g10", "b200-180gb"])
+def test_fusion_table_matches_literal_r8(name):
+    """The slot-level fusion/fission answers the lane kernel reads (mig_geometry_fusion) against reading R8 evaluated
+    literally on instance sets: for every valid state of the oracle's Alg. 1 enumeration, every
+    set of busy instances (all subsets up to 5 instances, 24 seeded ones beyond) and every profile, the placements
+    that overlap >= 1 instance and only idle ones; destroy the overlapped, create the placement; best by
+    (fcr(result) from the oracle, -#destroyed, start)."""
+    import numpy as np
+
+    g = mig.mig_geometry_load(f"builtin:{name}")
+    og = orc.Geometry(geom_path(name))
+    spec = json.load(open(geom_path(name)))
+    lens = [p["memory_slots"] for p in spec["profiles"]]
+    starts = [p["starts"] for p in spec["profiles"]]
+    rng = np.random.default_rng(11)
+    n_checked = n_found = 0
+    for inst, _, _ in og.states():
+        masks = [((1 << lens[p]) - 1) << s for p, s in inst]
+        occ = sum(masks)
+        sm = sum(1 << s for _, s in inst)
+        k = len(inst)
+        subsets = range(1 << k) if k <= 5 else [int(x) for x in rng.integers(0, 1 << k, 24)]
+        for bs in subsets:
+            busy = sum(masks[i] for i in range(k) if (bs >> i) & 1)
+            for p in range(len(lens)):
+                best = None
+                for s in starts[p]:
+                    qm = ((1 << lens[p]) - 1) << s
+                    over = [i for i in range(k) if masks[i] & qm]
+                    if not over or any((bs >> i) & 1 for i in over):
+                        continue
+                    rest = [inst[i] for i in range(k) if i not in over] + [(p, s)]
+                    key = (og.fcr(rest), -len(over), s)
+                    if best is None or key > best[0]:
+                        best = (key, sum(masks[i] for i in over))
+                got = mig.mig_geometry_fusion(g, occ, sm, busy, p)
+                want = (-1, 0) if best is None else (best[0][2], best[1])
+                assert got == want, (inst, bs, p, got, want)
+                n_checked += 1
+                n_found += best is not None
+    assert n_found > 0 and n_checked > 100
