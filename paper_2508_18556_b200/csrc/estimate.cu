@@ -251,6 +251,25 @@ __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstP
         const uint64_t gend = P.off[t0 + nb] - j_base;
         const uint64_t gbeg = __shfl_sync(FULL, my_off, 0);
         for (uint64_t c = gbeg; c < gend; c += 32) {
+            if (P.dyn_only && c + 128 <= gend) {
+                // mig_simulate's estimate: only DYNAMIC jobs need work; look 4 chunks ahead (4 loads in flight per
+                // lane) and skip them when none is DYNAMIC, checking the records on the way
+                uint4 r4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) r4[u] = __ldg(P.jobs + c + 32 * u + lane);
+                bool dyn = false, bad = false;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t cl = (r4[u].z >> 16) & 0xFFu;
+                    dyn |= cl == kClassDynamic;
+                    bad |= cl > 2 || (r4[u].z & 0xFFFFu) > 4096 || (r4[u].z >> 24) != 0;
+                }
+                if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
+                if (!__any_sync(FULL, dyn)) {
+                    c += 96;
+                    continue;
+                }
+            }
             const uint64_t g = c + lane;
             const bool valid = g < gend;
             uint4 r = make_uint4(0, 0, 0, 0), e = make_uint4(0, 0, 0, 0);

@@ -75,6 +75,7 @@ struct LaneShared {
                                        // (same memory, compute >=; R7), selecting from the idle-by-profile masks
     uint8_t scand[16];        // STATIC: layout starts whose slice can hold profile p
     uint8_t lvl_first[8];     // first profile of each memory level ([n_levels] = 0xFF)
+    uint32_t lmem[8];         // level memories, padded with 0xFFFFFFFF beyond n_levels
     uint32_t jk[8][kLaneThreads];  // per lane and start slot: job | end kind << 16 of the running job
     uint32_t et[8][kLaneThreads];  // per lane and start slot: end tick of the running job (kNoEnd = idle)
     // per-lane partial totals (no atomics: 64-bit shared atomics are CAS loops), reduced once per CTA
@@ -97,7 +98,7 @@ __device__ __forceinline__ uint32_t lane_tight_fit(const LaneShared& S, uint32_t
     if (!fold || warps == 0) {
         uint32_t L = 0;
 #pragma unroll
-        for (int l = 0; l < kMaxLevels; ++l) L += ((uint32_t)l < G.n_levels && G.level_mem[l] < req) ? 1u : 0u;
+        for (int l = 0; l < kMaxLevels; ++l) L += S.lmem[l] < req ? 1u : 0u;  // padded with 0xFFFFFFFF
         return S.lvl_first[L];
     }
     const uint32_t cf = G.wave_cap[G.full_prof];
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             for (uint32_t p = G.n_prof; p-- > 0;)
                 if (G.level[p] == tid) f = p;
             S.lvl_first[tid] = (uint8_t)(tid < G.n_levels ? f : 0xFFu);
+            S.lmem[tid] = tid < G.n_levels ? G.level_mem[tid] : 0xFFFFFFFFu;
         }
     }
     __syncthreads();
@@ -280,8 +282,9 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         uint32_t ticks = hr.w;
         const bool dyn = ((hr.z >> 16) & 0xFFu) == kClassDynamic;
         uint32_t fe, pred = 0, conv = 0, phys = 0;
-        const mig_job_estimate* ej = P.est + j0 + j;
+        const mig_job_estimate* ej = nullptr;
         if (__builtin_expect(dyn, 0)) {
+            ej = P.est + j0 + j;
             const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(ej));
             pred = e0.y;
             conv = e0.z & 0xFFFFu;
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                                 // A7 (R8): placement k destroys the idle instances it overlaps;
                                 // best (fcr(result), -#destroyed, start) over the candidates c, one table entry
                                 // per (slot-level state, profile, c) (host-built, mig_geometry::a7)
-                                const uint2 e = __ldg(P.a7 + (size_t)sid * P.n_a7 + S.cbase[need] + cm);
+                                const uint2 e = __ldg(P.a7 + (sid * P.n_a7 + S.cbase[need] + cm));
                                 const uint32_t best = e.x, by = e.y;
                                 if (best) {
                                     s = best & 0xFFu;
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     occ |= ((G.pinfo[need] >> 8) & 0xFFu) << s;
                     if (KIND == MIG_FUSION_FISSION) {
                         SM |= 1u << s;
-                        if (kd == K_ALLOC) sid = __ldg(P.trans + (size_t)sid * P.n_q + S.qbase[need] + qk).y >> 8;
+                        if (kd == K_ALLOC) sid = __ldg(P.trans + (sid * P.n_q + S.qbase[need] + qk)).y >> 8;
                     }
                     prof4 = (prof4 & ~(0xFu << (4 * s))) | (need << (4 * s));
                 }
