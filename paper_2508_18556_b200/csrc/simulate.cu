@@ -987,25 +987,28 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     PA.counter = counter + 1;
     cudaError_t e = cudaSuccess;
     *launches = 0;
-    // the lane kernel packs idle masks per profile in a u64 and takes fusion / fission from the transition table
-    if (P.n_pol && simulate_use_lane() && n_prof <= 8 && trans && a7) {
+    // the lane kernel packs idle masks per profile in a u64 and takes fusion / fission from the host tables
+    const bool lane = simulate_use_lane() && n_prof <= 8 && trans && a7;
+    if (lane) {  // every policy, Scheme A included: one lane-kernel launch each
         const uint64_t blocks = simulate_lane_grid(tr.n_traces, sm_count);
+        const uint64_t stride = (uint64_t)tr.max_jobs * (PA.n_pol ? kMaxLevels : 1);  // Scheme A: group lists
         uint16_t* ring = nullptr;
-        e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * tr.max_jobs * sizeof(uint16_t), stream);
+        e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * stride * sizeof(uint16_t), stream);
         if (e != cudaSuccess) return e;
-        static const char* kNames[4] = {"sim_baseline", "sim_static", "sim_dynamic", "sim_ff"};
-        for (uint32_t k = 0; k < P.n_pol && e == cudaSuccess; ++k) {
-            e = (cudaError_t)mig_timed(kNames[P.pol[k].kind & 3u], stream, [&](uint32_t* nl) {
+        static const char* kNames[5] = {"sim_baseline", "sim_static", "sim_dynamic", "sim_ff", "sim_scheme_a"};
+        for (uint32_t i = 0; i < n_pol && e == cudaSuccess; ++i) {
+            e = (cudaError_t)mig_timed(kNames[pols[i].kind], stream, [&](uint32_t* nl) {
                 if (nl) *nl = 1;
-                return (int)launch_simulate_lane(Gdev, tr, P.pol[k], P.pol_idx[k], n_pol, est, out, totals,
-                                                 counter + 2 + k, est_err, ring, blocks, trans, n_q, a7, n_a7,
+                return (int)launch_simulate_lane(Gdev, tr, pols[i], i, n_pol, est, out, totals, counter + 2 + i,
+                                                 est_err, ring, blocks, trans, n_q, a7, n_a7,
                                                  stream);
             });
             ++*launches;
         }
         cudaFreeAsync(ring, stream);
-        if (e != cudaSuccess) return e;
-    } else if (P.n_pol) {
+        return e;
+    }
+    if (P.n_pol) {
         e = launch_variant<false>(Gdev, P, tr, sm_count, stream);
         if (e != cudaSuccess) return e;
         ++*launches;

@@ -58,7 +58,8 @@ constexpr int kLaneMinBlocks = 6;
 constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
 constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
 
-// mig_policy_totals fields accumulated per lane: 32-bit counts (index -> totals field) and 64-bit sums. completed,
+// mig_policy_totals fields accumulated per CTA: 32-bit counts (index -> totals field; shared atomics, at most
+// 2^32 / MIG_MAX_JOBS_PER_TRACE units per CTA) and 64-bit sums (per-lane partials). completed,
 // restarts and energy are linear in these (n - rejected - failed; ooms - failed + preempts; idle_w * makespan +
 // w_per_slice * busy) and are derived once per CTA.
 constexpr int kT32 = 12, kT64 = 6;
@@ -79,7 +80,7 @@ struct LaneShared {
     uint32_t jk[8][kLaneThreads];  // per lane and start slot: job | end kind << 16 of the running job
     uint32_t et[8][kLaneThreads];  // per lane and start slot: end tick of the running job (kNoEnd = idle)
     // per-lane partial totals (no atomics: 64-bit shared atomics are CAS loops), reduced once per CTA
-    uint32_t c32[kT32][kLaneThreads];
+    uint32_t c32[kT32];            // per-CTA 32-bit counts (shared atomics)
     unsigned long long c64[kT64][kLaneThreads];
 };
 
@@ -127,8 +128,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
         uint32_t* dst = reinterpret_cast<uint32_t*>(&S.G);
         for (uint32_t i = tid; i < sizeof(DevGeom) / 4; i += blockDim.x) dst[i] = __ldg(src + i);
-#pragma unroll
-        for (int f = 0; f < kT32; ++f) S.c32[f][tid] = 0;
+        if (tid < kT32) S.c32[tid] = 0;
 #pragma unroll
         for (int f = 0; f < kT64; ++f) S.c64[f][tid] = 0;
     }
@@ -196,7 +196,13 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     const bool wave = (pol.flags & MIG_WAVE_TIME) != 0;
     const uint32_t reconfig = pol.reconfig_ticks, full_mem = G.full_mem;
     const uint64_t jbase = P.off[0];
-    uint16_t* ring = P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap;
+    // Scheme B: requeue FIFO (ring_cap entries); Scheme A: group lists, [memory level][ring_cap]
+    uint16_t* ring = P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap * (KIND == MIG_SCHEME_A ? kMaxLevels : 1);
+    // Scheme A: [0..7] group lengths by memory level, [8..15] next group-list index of the slice at slot s
+    __shared__ uint16_t s_sa[KIND == MIG_SCHEME_A ? 16 : 1][kLaneThreads];
+    uint16_t* glen = &s_sa[0][tid];
+    uint16_t* nx = &s_sa[KIND == MIG_SCHEME_A ? 8 : 0][tid];
+    uint32_t cur = 0xFFu, ns = 0, PM = 0, ready = 0;  // Scheme A: current group, its slices, pending-slice mask
     uint32_t* jk = &S.jk[0][tid];
     uint32_t* et = &S.et[0][tid];
     const uint32_t fp = G.full_prof;
@@ -256,6 +262,12 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 occ |= G.lenmask[p] << s;
             }
         }
+        if (KIND == MIG_SCHEME_A) {
+            cur = 0xFFu;
+            ns = PM = ready = 0;
+#pragma unroll
+            for (int l = 0; l < 8; ++l) glen[l * kLaneThreads] = 0;
+        }
         K0 = K1 = K2 = K3 = 0;
         a_turn = a_busy = a_mem = a_waste = 0;
         hl = (uint32_t)kFnvOffset;
@@ -263,6 +275,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         bbusy = false;
         mode = 0;
         fetch_head();
+        if (KIND == MIG_SCHEME_A && hj != kNoJob) mode = 4;  // the grouping pass first
     };
     auto pop = [&]() {
         if (qh < n) {
@@ -377,6 +390,132 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         a_turn += t;
                     }
                     bbusy = false;
+                }
+            }
+        } else if constexpr (KIND == MIG_SCHEME_A) {
+            // ---- Scheme A, schedule_by_group (reading R38) ----
+            if (mode == 4) {  // sorted_by_mig_group at t = 0, one job per iteration; REJECTs in queue order
+                const uint32_t j = hj, need = head_need();
+                if (need == kNoNeed) {
+                    lrec(hl, hh, 0u, (j << 16) | (K_REJECT << 12) | 0xFF0u);
+                    K2 += 1u;
+                } else {
+                    const uint32_t lv = G.level[need], c = glen[lv * kLaneThreads];
+                    ring[lv * P.ring_cap + c] = (uint16_t)j;
+                    glen[lv * kLaneThreads] = (uint16_t)(c + 1u);
+                }
+                pop();
+                if (hj == kNoJob) mode = 0;
+            }
+            __syncwarp();
+            if (mode == 0) {
+                const uint32_t cand = PM & ~BS;
+                if (cand) {  // the lowest idle slice with pending jobs takes its next one
+                    const uint32_t s = (uint32_t)__ffs(cand) - 1u;
+                    const uint32_t k = nx[s * kLaneThreads];
+                    const uint32_t j = ring[cur * P.ring_cap + k];
+                    const uint32_t pr = (prof4 >> (4 * s)) & 0xFu;
+                    hr = __ldg(P.jobs + j0 + j);
+                    he = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
+                    lrec(hl, hh, t, (j << 16) | (K_PLACE_GROUP << 12) | (s << 8) | (pr << 4));
+                    K0 += 1u;
+                    uint32_t end, ek;
+                    start_run(j, s, pr, t < ready ? t + reconfig : t, end, ek);  // a new slice: reconfig first
+                    et[s * kLaneThreads] = end;
+                    jk[s * kLaneThreads] = j | (ek << 16);
+                    BS |= 1u << s;
+                    BM |= ((G.pinfo[pr] >> 8) & 0xFFu) << s;
+                    nx[s * kLaneThreads] = (uint16_t)(k + ns);
+                    if (k + ns >= glen[cur * kLaneThreads]) PM &= ~(1u << s);
+                } else if (BS == 0) {  // drained: set_homogeneous_slices(next non-empty group)
+                    uint32_t l = cur == 0xFFu ? 0u : cur + 1u;
+                    while (l < G.n_levels && glen[l * kLaneThreads] == 0) ++l;
+                    if (l < G.n_levels) {
+                        const uint32_t nd = __popc(SM);
+                        lrec(hl, hh, t, (0xFFFFu << 16) | (K_LAYOUT << 12) | (l << 4) | nd);
+                        K1 += nd;
+                        ns = G.n_alay[l];
+                        const uint32_t len = glen[l * kLaneThreads];
+                        SM = prof4 = PM = 0;
+                        for (uint32_t k = 0; k < ns; ++k) {
+                            const uint32_t e = G.alay[l][k], st = e & 0xFFu;
+                            SM |= 1u << st;
+                            prof4 |= (e >> 8) << (4 * st);
+                            nx[st * kLaneThreads] = (uint16_t)k;
+                            if (k < len) PM |= 1u << st;
+                        }
+                        K0 += ns << 16;
+                        ready = t + reconfig;
+                        cur = l;
+                    } else {
+                        mode = 1;  // nothing left: EVT finds no running job and finishes the unit
+                    }
+                } else {
+                    mode = 1;
+                }
+            }
+            __syncwarp();
+            if (mode == 1) {  // the events of the next tick (R28), then dispatch again
+                if (!evm) {
+                    uint32_t e8[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) e8[k] = et[k * kLaneThreads];
+                    uint32_t tn = e8[0];
+#pragma unroll
+                    for (int k = 1; k < 8; ++k) tn = min(tn, e8[k]);
+                    if (tn == kNoEnd) {
+                        mode = 2;
+                    } else {
+                        t = tn;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) evm |= (e8[k] == tn ? 1u : 0u) << k;
+                    }
+                }
+                if (evm) {
+                    uint32_t es = (uint32_t)__ffs(evm) - 1u;
+                    uint32_t v = jk[es * kLaneThreads];
+                    for (uint32_t m = evm & (evm - 1u); m; m &= m - 1u) {
+                        const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                        const uint32_t w = jk[k * kLaneThreads];
+                        if (w < v) {
+                            v = w;
+                            es = k;
+                        }
+                    }
+                    evm &= ~(1u << es);
+                    const uint32_t job = v & 0xFFFFu, ek = v >> 16;
+                    const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = G.pinfo[epr];
+                    const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
+                    lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));
+                    a_turn += ek == 0 ? t : 0u;
+                    K2 += ek == 1 ? 1u << 16 : 0u;
+                    K3 += ek == 2 ? 1u : 0u;
+                    uint32_t req = 0;
+                    if (ek == 1) {
+                        req = G.level_next[si & 0xFu];
+                        if (req == 0) {
+                            lrec(hl, hh, t, elo | (K_FAILED << 12));
+                            K3 += 1u << 16;
+                        }
+                    } else if (ek == 2) {
+                        req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
+                    }
+                    if (req) {  // the tail of the job's new (larger) group
+                        const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
+                        const uint32_t nn = lane_tight_fit(S, req, w, fold);
+                        if (nn == kNoNeed) {
+                            lrec(hl, hh, t, (job << 16) | (K_REJECT << 12) | 0xFF0u);
+                            K2 += 1u;
+                        } else {
+                            const uint32_t lv = G.level[nn], c = glen[lv * kLaneThreads];
+                            ring[lv * P.ring_cap + c] = (uint16_t)job;
+                            glen[lv * kLaneThreads] = (uint16_t)(c + 1u);
+                        }
+                    }
+                    et[es * kLaneThreads] = kNoEnd;
+                    BS &= ~(1u << es);
+                    BM &= ~(((si >> 8) & 0xFFu) << es);
+                    if (!evm) mode = 0;
                 }
             }
         } else {
@@ -581,20 +720,20 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 o[5] = make_uint4((uint32_t)a_mem, (uint32_t)(a_mem >> 32), (uint32_t)a_waste,
                                   (uint32_t)(a_waste >> 32));
             }
-            {  // a12: per-lane partial totals (slots of this lane only)
-                uint32_t* c = &S.c32[0][tid];
-                c[0 * kLaneThreads] += 1u;
-                c[1 * kLaneThreads] += n;
-                c[2 * kLaneThreads] += rejected;
-                c[3 * kLaneThreads] += failed;
-                c[4 * kLaneThreads] += ooms;
-                c[5 * kLaneThreads] += preempts;
-                c[6 * kLaneThreads] += placements;
-                c[7 * kLaneThreads] += waits;
-                c[8 * kLaneThreads] += creates;
-                c[9 * kLaneThreads] += destroys;
-                c[10 * kLaneThreads] = max(c[10 * kLaneThreads], makespan);
-                c[11 * kLaneThreads] |= err;
+            {  // a12: 32-bit counts by shared atomics, 64-bit sums in this lane's partial slots
+                uint32_t* c = S.c32;
+                atomicAdd(c + 0, 1u);
+                atomicAdd(c + 1, n);
+                if (rejected) atomicAdd(c + 2, rejected);
+                if (failed) atomicAdd(c + 3, failed);
+                if (ooms) atomicAdd(c + 4, ooms);
+                if (preempts) atomicAdd(c + 5, preempts);
+                atomicAdd(c + 6, placements);
+                if (waits) atomicAdd(c + 7, waits);
+                if (creates) atomicAdd(c + 8, creates);
+                if (destroys) atomicAdd(c + 9, destroys);
+                atomicMax(c + 10, makespan);
+                if (err) atomicOr(c + 11, err);
                 unsigned long long* d = &S.c64[0][tid];
                 d[0 * kLaneThreads] += makespan;
                 d[1 * kLaneThreads] += a_turn;
@@ -621,10 +760,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         if (tid < kT32 + kT64) {  // one thread per field reduces the CTA's lanes
             unsigned long long v = 0;
             if (tid < kT32) {
-                for (int k = 0; k < kLaneThreads; ++k) {
-                    const uint32_t x = S.c32[tid][k];
-                    v = tid == 10 ? max(v, (unsigned long long)x) : tid == 11 ? (v | x) : v + x;
-                }
+                v = S.c32[tid];
             } else {
                 for (int k = 0; k < kLaneThreads; ++k) v += S.c64[tid - kT32][k];
             }
@@ -694,6 +830,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
         case MIG_STATIC: k_simulate_lane<MIG_STATIC><<<grid, block, 0, stream>>>(Gdev, P); break;
         case MIG_DYNAMIC: k_simulate_lane<MIG_DYNAMIC><<<grid, block, 0, stream>>>(Gdev, P); break;
         case MIG_FUSION_FISSION: k_simulate_lane<MIG_FUSION_FISSION><<<grid, block, 0, stream>>>(Gdev, P); break;
+        case MIG_SCHEME_A: k_simulate_lane<MIG_SCHEME_A><<<grid, block, 0, stream>>>(Gdev, P); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
