@@ -55,7 +55,7 @@ struct OrGeomDesc {
 
 struct OrPolicy {
     uint32_t kind;   // 0 BASELINE, 1 STATIC, 2 DYNAMIC, 3 FUSION_FISSION, 4 SCHEME_A
-    uint32_t flags;  // 1 EARLY_RESTART, 2 WARP_FOLD, 4 EWMA_REUSE, 8 WAVE_TIME
+    uint32_t flags;  // 1 EARLY_RESTART, 2 WARP_FOLD, 4 EWMA_REUSE, 8 WAVE_TIME, 16 PCIE_CONTENTION
     uint32_t ctx_mib, reconfig_ticks, idle_w, w_per_slice;
     double z;
     uint32_t eps_num, eps_den, conv_k, min_n;
@@ -80,7 +80,7 @@ static_assert(sizeof(OrEstimate) == 80, "estimate layout");
 static_assert(sizeof(OrResult) == 96, "result layout");
 
 enum { BASELINE = 0, STATIC = 1, DYNAMIC = 2, FUSION_FISSION = 3, SCHEME_A = 4 };
-enum { F_EARLY_RESTART = 1, F_WARP_FOLD = 2, F_EWMA = 4, F_WAVE_TIME = 8 };
+enum { F_EARLY_RESTART = 1, F_WARP_FOLD = 2, F_EWMA = 4, F_WAVE_TIME = 8, F_PCIE = 16 };
 enum { K_REUSE = 1, K_ALLOC, K_RECONF, K_WAIT, K_REJECT, K_COMPLETE, K_OOM, K_PREEMPT, K_FAILED, K_PLACE_STATIC,
        K_PLACE_BASELINE, K_LAYOUT, K_PLACE_GROUP };
 
@@ -228,6 +228,12 @@ struct Instance {
     bool busy;
     int job;
     uint32_t run_start;
+    // PCIe contention (flag F_PCIE, reading R39): the run in progress is re-timed whenever the number of
+    // transferring runs changes. D = nominal duration (ticks), W = remaining work in 2^-16 nominal ticks since tk.
+    bool started = false;
+    uint32_t D = 0, end = 0, tk = 0, kind_order = 0, iters_run = 0;
+    int64_t W = 0;
+    uint64_t memsum = 0;  // physical MiB summed over the iterations the run executes (nominal)
 };
 
 std::vector<int> state_key(const Geometry& g, const std::vector<Instance>& inst) {
@@ -369,6 +375,7 @@ void peak_memory_prediction(const std::vector<uint32_t>& y, const std::vector<ui
 // ---------------------------------------------------------------------------------------------------------------
 struct Job {
     uint32_t cls, iters, ticks, est, tru, ws, warps;
+    uint32_t xfer;               // PCIe transfer fraction of an iteration, in 1/256 (record bits 24-31, R39)
     uint32_t b, q0, slope_q8, sigma, qslope;
     std::vector<uint32_t> y, q;  // DYNAMIC samples i = 1..T
     OrEstimate e;
@@ -414,6 +421,7 @@ Job load_job(const Geometry& g, const uint32_t* rec, const uint32_t* ext, uint64
     Job j;
     j.cls = (rec[2] >> 16) & 0xFF;
     j.iters = rec[2] & 0xFFFF;
+    j.xfer = rec[2] >> 24;
     j.ticks = rec[3];
     j.ws = ext ? ext[0] : 0;
     j.warps = ext ? ext[1] : 0;
@@ -583,12 +591,107 @@ struct Sim {
         }
         ev.tick = end;
         uint32_t comp = pol.kind == BASELINE ? g.d.n_compute : g.d.prof_compute[in.prof];
-        r.busy_slice_ticks += (uint64_t)comp * (end - s);
         // memory held while running: iterations 1..k at `ticks` each (k = OOM / preempt / last iteration)
         uint32_t iters_run = ev.kind_order == 1 ? i_oom : ev.kind_order == 2 ? i_pre : T;
+        if (pol.flags & F_PCIE) {  // R39: the end is known only as the run progresses (retime, run_pcie)
+            in.started = false;
+            in.D = end - s;
+            in.kind_order = ev.kind_order;
+            in.iters_run = iters_run;
+            in.memsum = memory_sum(j, iters_run, pol);
+            return;
+        }
+        r.busy_slice_ticks += (uint64_t)comp * (end - s);
         r.mem_mib_ticks += memory_sum(j, iters_run, pol) * ticks;
         if (ev.kind_order != 0) r.wasted_ticks += end - s;
         events.push(ev);
+    }
+
+    // ---- PCIe contention ("PCIe bandwidth remains a shared resource, being equally divided among
+    // multiple MIG instances"; reading R39) ----
+    // A run of a job with transfer fraction F/256 > 0 shares PCIe with the other transferring runs in progress
+    // (c of them): its transfer time is multiplied by c, its kernel time is not, so it advances at
+    // 2^24 / (256 - F + F c) units of 2^-16 nominal ticks per tick (floor). Runs with F = 0 are unaffected.
+    uint32_t c_eff = 0;  // transferring runs in progress since the last retime
+
+    static int64_t rate(uint32_t F, uint32_t c) {
+        return F == 0 ? 65536 : (int64_t)((1u << 24) / (256u - F + F * c));
+    }
+
+    // Every run in progress advances from its last retime tick to t at the concurrency in effect (c_eff).
+    void advance(uint32_t tt) {
+        for (Instance& in : inst)
+            if (in.busy && in.started) {
+                in.W -= (int64_t)(tt - in.tk) * rate(jobs[in.job].xfer, c_eff);
+                in.tk = tt;
+            }
+    }
+
+    // At tick t, after the events and the scheduler pass: runs due to start now begin (full nominal work), the
+    // concurrency is recounted and every run in progress gets its end for the new rate.
+    void retime() {
+        uint32_t c = 0;
+        for (Instance& in : inst) {
+            if (!in.busy) continue;
+            if (!in.started && in.run_start == t) {
+                in.started = true;
+                in.tk = t;
+                in.W = (int64_t)in.D << 16;
+            }
+            if (in.started && jobs[in.job].xfer > 0) ++c;
+        }
+        for (Instance& in : inst)
+            if (in.busy && in.started) {
+                const int64_t rho = rate(jobs[in.job].xfer, c);
+                in.end = t + (uint32_t)((in.W + rho - 1) / rho);
+            }
+        c_eff = c;
+    }
+
+    // A run ends at t: its actual duration counts for power, memory and waste (R26, R39).
+    void end_run(int k) {
+        Instance& in = inst[k];
+        const Job& j = jobs[in.job];
+        const uint32_t actual = t - in.run_start;
+        const uint32_t comp = pol.kind == BASELINE ? g.d.n_compute : g.d.prof_compute[in.prof];
+        r.busy_slice_ticks += (uint64_t)comp * actual;
+        // memory: a constant footprint for the whole run; a DYNAMIC job's iterations stretched uniformly
+        r.mem_mib_ticks += j.cls == TG_CLASS_DYNAMIC ? (in.iters_run ? in.memsum * actual / in.iters_run : 0)
+                                                     : physical(j, 1, pol) * actual;
+        if (in.kind_order != 0) r.wasted_ticks += actual;
+        Event ev;
+        ev.tick = t;
+        ev.kind_order = in.kind_order;
+        ev.job = (uint32_t)in.job;
+        apply(ev);
+    }
+
+    // The event loop with re-timing: the next tick is the earliest end or pending start; ends are applied in R28
+    // order and followed by one scheduler pass; a tick with only starts has no pass (nothing finished).
+    void run_pcie(bool scheme_a) {
+        retime();
+        for (;;) {
+            uint32_t tn = 0xFFFFFFFFu;
+            for (const Instance& in : inst)
+                if (in.busy) tn = std::min(tn, in.started ? in.end : in.run_start);
+            if (tn == 0xFFFFFFFFu) break;
+            advance(tn);
+            t = tn;
+            std::vector<std::pair<uint64_t, int>> ends;  // (kind order, job) -> instance
+            for (size_t k = 0; k < inst.size(); ++k)
+                if (inst[k].busy && inst[k].started && inst[k].end == t)
+                    ends.push_back({((uint64_t)inst[k].kind_order << 32) | (uint32_t)inst[k].job, inst[k].start});
+            std::sort(ends.begin(), ends.end());
+            for (auto& e : ends) end_run(find_instance(e.second));
+            if (!ends.empty()) {
+                r.makespan = t;
+                if (scheme_a) a_step();
+                else scheduler_pass();
+            }
+            retime();
+            check_invariants();
+            if (!err.empty()) return;
+        }
     }
 
     // One scheduler pass at tick t (Alg. 4; wake on every event, R9).
@@ -878,6 +981,7 @@ struct Sim {
         t = 0;
         for (size_t i = 0; i < jobs.size(); ++i) a_enqueue((int)i);  // REJECTs at t = 0, in queue order
         a_step();
+        if (pol.flags & F_PCIE) run_pcie(true);
         while (!events.empty()) {
             t = events.top().tick;
             while (!events.empty() && events.top().tick == t) {
@@ -908,6 +1012,7 @@ struct Sim {
         for (size_t i = 0; i < jobs.size(); ++i) queue.push_back((int)i);
         t = 0;
         scheduler_pass();
+        if (pol.flags & F_PCIE) run_pcie(false);
         while (!events.empty()) {
             t = events.top().tick;
             while (!events.empty() && events.top().tick == t) {

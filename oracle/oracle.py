@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 BASELINE, STATIC, DYNAMIC, FUSION_FISSION, SCHEME_A = 0, 1, 2, 3, 4
-EARLY_RESTART, WARP_FOLD, EWMA_REUSE, WAVE_TIME = 1, 2, 4, 8
+EARLY_RESTART, WARP_FOLD, EWMA_REUSE, WAVE_TIME, PCIE = 1, 2, 4, 8, 16
 
 KIND_NAMES = {1: "REUSE", 2: "ALLOC", 3: "RECONF", 4: "WAIT", 5: "REJECT", 6: "COMPLETE", 7: "OOM", 8: "PREEMPT",
               9: "FAILED", 10: "PLACE_STATIC", 11: "PLACE_BASELINE", 12: "LAYOUT", 13: "PLACE_GROUP"}

@@ -289,3 +289,69 @@ def test_memory_utilisation_and_wasted_time():
     # memory integral of the dynamic run: sum over iterations of (1000 + 100 i) x 10 ticks
     assert int(b["mem_mib_ticks"]) == 10 * (sum(1000 + 100 * i for i in range(1, 7)) +
                                             sum(1000 + 100 * i for i in range(1, 51)))
+
+
+# ---- PCIe contention (reading R39) ----
+
+def _pcie_run(geo, jobs_list, kind, flags=orc.PCIE, reconfig=0):
+    jobs, ext, off = tg.pack_traces([jobs_list])
+    g = orc.Geometry(geom_path(geo))
+    return orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, flags=flags, ctx_mib=0, reconfig_ticks=reconfig))[0, 0]
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3, 4])
+def test_pcie_zero_fraction_changes_nothing(kind):
+    """"transfer_fraction 0 for all -> no slowdown regardless of concurrency": with F = 0 the re-timed
+    event loop reproduces the plain one field for field (decision hash included), on generated config-5 traces."""
+    jobs, ext, off = tg.generate_host(5, 40)
+    g = orc.Geometry(geom_path("a100-40gb"))
+    a = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind))
+    b = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, flags=orc.PCIE))
+    for f in orc.RESULT_DTYPE.names:
+        assert np.array_equal(a[f], b[f]), f
+
+
+def test_pcie_seven_transfer_jobs_closed_form():
+    """7 identical 5 GB jobs with transfer fraction F/256 on the seven 1g.5gb slices run concurrently, each
+    advancing at 2^24 / (256 + 6F) units of 2^-16 ticks per tick: the per-job runtime ratio is (1 - f) + 7f
+    (S:381), here F = 51 (f ~ 0.2): ratio 2.2, batch throughput vs one-at-a-time 7 / 2.2 ~ 3.18 (the
+    mechanism behind the paper's 1.92x instead of 7x for Needleman-Wunsch)."""
+    D, F = 1000, 51
+    job = tg.pack_job(4096, 4096, 10, 0, D // 10, xfer=F)
+    rho = (1 << 24) // (256 - F + F * 7)
+    end = -(-D * 65536 // rho)
+    r = _pcie_run("a100-40gb", [job] * 7, kind=3)
+    assert r["makespan"] == end == 2196
+    assert r["busy_slice_ticks"] == 7 * end and r["completed"] == 7
+    base = _pcie_run("a100-40gb", [job] * 7, kind=0)
+    assert base["makespan"] == 7 * D  # one run at a time: c = 1, no slowdown (S:380)
+    assert abs(base["makespan"] / r["makespan"] - 3.19) < 0.01
+
+
+def test_pcie_single_transfer_run_and_mixed_fractions():
+    """c counts only transferring runs: a job with F > 0 next to F = 0 jobs runs at full speed; two F = 128 jobs
+    share: 2^24 / 384 = 43690 per tick, 1000 ticks of work end at ceil(65536000 / 43690) = 1501."""
+    a = tg.pack_job(4096, 4096, 10, 0, 100, xfer=128)
+    b = tg.pack_job(4096, 4096, 10, 0, 300, xfer=0)
+    r = _pcie_run("a100-40gb", [a, b], kind=3)
+    assert r["makespan"] == 3000 and r["busy_slice_ticks"] == 1000 + 3000
+    r = _pcie_run("a100-40gb", [a, a], kind=3)
+    assert r["makespan"] == 1501 and r["busy_slice_ticks"] == 2 * 1501
+
+
+def test_pcie_retime_when_a_transfer_run_starts_late():
+    """Re-timing at a start (STATIC layout 4g@0, 2g@4, 1g@6 of A100-40GB): A (4 GB, F = 128, 1000 ticks) runs on
+    1g@6 from 0; C (8 GB, F = 0) on 2g@4 and D (15 GB, F = 0) on 4g@0 run 400 ticks; B (8 GB, F = 128, 1000 ticks)
+    waits and starts at 400 on 2g@4. A: 400 ticks alone, then 65536000 - 400*65536 = 39321600 units at
+    2^24/384 = 43690 per tick -> ends at 400 + ceil(900.01) = 1301. B: 901 ticks shared leave
+    65536000 - 901*43690 = 26171310 units, alone again at 65536 per tick -> ends at 1301 + 400 = 1701."""
+    A = tg.pack_job(4096, 4096, 10, 0, 100, xfer=128)
+    C = tg.pack_job(8192, 8192, 4, 0, 100)
+    D = tg.pack_job(15360, 15360, 4, 0, 100)
+    B = tg.pack_job(8192, 8192, 10, 0, 100, xfer=128)
+    r = _pcie_run("a100-40gb", [A, C, D, B], kind=1)
+    assert r["completed"] == 4 and r["makespan"] == 1701
+    assert r["busy_slice_ticks"] == 1 * 1301 + 2 * 400 + 4 * 400 + 2 * (1701 - 400)
+    assert r["turnaround_sum"] == 1301 + 400 + 400 + 1701
+    plain = _pcie_run("a100-40gb", [A, C, D, B], kind=1, flags=0)
+    assert plain["makespan"] == 1400

@@ -108,9 +108,10 @@ def dyn_samples(seed: int, trace_id: int, job_idx: int, job, ext, T: int):
     return y, q
 
 
-def pack_job(x, y, iters, cls, ticks, ws=0, warps=0, slope_q8=0, sigma=0, qslope=0):
-    """One job record + ext record in the tracegen.h format (for hand-written fixtures)."""
-    return ([x, y, (iters & 0xFFFF) | (cls << 16), ticks],
+def pack_job(x, y, iters, cls, ticks, ws=0, warps=0, slope_q8=0, sigma=0, qslope=0, xfer=0):
+    """One job record + ext record in the tracegen.h format (for hand-written fixtures). xfer: PCIe transfer
+    fraction of an iteration in 1/256 (record bits 24-31, reading R39)."""
+    return ([x, y, (iters & 0xFFFF) | (cls << 16) | ((xfer & 0xFF) << 24), ticks],
             [ws, warps, slope_q8, (sigma & 0xFFFF) | (qslope << 16)])
 
 
