@@ -113,7 +113,8 @@ mig_status mig_geometry_fusion(const mig_geometry* g, uint32_t occ_mask, uint32_
  *   jobs[j]     = {x, y, z, w} u32:
  *                 STATIC/MODEL: x = est_mib (compile-time / model-size estimate), y = true_mib (footprint)
  *                 DYNAMIC:      x = b_mib (intercept), y = q0_q16 (inverse reuse ratio at t=0, Q16)
- *                 z = iters (bits 0-15) | class (bits 16-23: 0 STATIC, 1 MODEL, 2 DYNAMIC) | 0 (bits 24-31)
+ *                 z = iters (bits 0-15) | class (bits 16-23: 0 STATIC, 1 MODEL, 2 DYNAMIC)
+ *                     | PCIe transfer fraction F of an iteration in 1/256 (bits 24-31; MIG_PCIE_CONTENTION)
  *                 w = iter_ticks
  *   jobs_ext[j] = {ws_mib, warps, slope_q8, sigma_mib | qslope_q16 << 16} or NULL (all zero).
  *   DYNAMIC jobs report per-iteration samples (requested MiB, inverse reuse Q16) drawn in-kernel from the
@@ -156,8 +157,13 @@ enum {
     MIG_EARLY_RESTART = 1, /* preempt when the converged forecast exceeds the slice   */
     MIG_WARP_FOLD = 2,     /* tight fit keeps the full-GPU wave count                        */
     MIG_EWMA_REUSE = 4,    /* EWMA of the inverse reuse ratio instead of its trend (north_star; not in paper) */
-    MIG_WAVE_TIME = 8      /* iter_ticks are full-GPU times; on profile p an iteration of a job with W warps takes
+    MIG_WAVE_TIME = 8,     /* iter_ticks are full-GPU times; on profile p an iteration of a job with W warps takes
                               ceil(ticks * waves(W,p) / waves(W,full)) ticks (R31 variant)  */
+    MIG_PCIE_CONTENTION = 16 /* PCIe bandwidth is divided equally among the runs that transfer (PAPER.md:696-701,
+                              reading R39): a run of a job with transfer fraction F/256 (record bits 24-31) > 0
+                              advances at 2^24 / (256 - F + F*c) units of 2^-16 nominal ticks per tick while c
+                              transferring runs are in progress, re-timed whenever c changes; power, memory
+                              integral and waste use actual durations. Lane kernel only (MIG_E_CUDA otherwise). */
 };
 
 typedef struct {

@@ -21,7 +21,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 MIG_BASELINE, MIG_STATIC, MIG_DYNAMIC, MIG_FUSION_FISSION, MIG_SCHEME_A = 0, 1, 2, 3, 4
-MIG_EARLY_RESTART, MIG_WARP_FOLD, MIG_EWMA_REUSE, MIG_WAVE_TIME = 1, 2, 4, 8
+MIG_EARLY_RESTART, MIG_WARP_FOLD, MIG_EWMA_REUSE, MIG_WAVE_TIME, MIG_PCIE_CONTENTION = 1, 2, 4, 8, 16
 MIG_MAX_JOBS_PER_TRACE = 768
 MIG_NEVER = 0xFFFF
 STATUS = {0: "MIG_OK", 1: "MIG_E_INVALID_ARG", 2: "MIG_E_IO", 3: "MIG_E_PARSE", 4: "MIG_E_VALIDATION",

@@ -151,7 +151,7 @@ mig_status check_traces(const mig_traces* tr) {
 
 mig_status check_policy(const mig_policy& p) {
     if (p.kind > MIG_SCHEME_A) return mig_set_error(MIG_E_INVALID_ARG, "policy.kind out of range");
-    if (p.flags & ~15u) return mig_set_error(MIG_E_INVALID_ARG, "unknown policy flag");
+    if (p.flags & ~31u) return mig_set_error(MIG_E_INVALID_ARG, "unknown policy flag");
     if (p.min_n < 3) return mig_set_error(MIG_E_INVALID_ARG, "policy.min_n must be >= 3");
     if (p.conv_k < 1 || p.conv_k > 32) return mig_set_error(MIG_E_INVALID_ARG, "policy.conv_k must be 1..32");
     if (p.eps_den == 0) return mig_set_error(MIG_E_INVALID_ARG, "policy.eps_den must be > 0");

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstP
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t cl = (r4[u].z >> 16) & 0xFFu;
                     dyn |= cl == kClassDynamic;
-                    bad |= cl > 2 || (r4[u].z & 0xFFFFu) > 4096 || (r4[u].z >> 24) != 0;
+                    bad |= cl > 2 || (r4[u].z & 0xFFFFu) > 4096;
                 }
                 if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
                 if (!__any_sync(FULL, dyn)) {
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstP
                 if (P.ext) e = __ldg(P.ext + g);
             }
             const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
-            if (__any_sync(FULL, valid && (cls > 2 || T > 4096 || (r.z >> 24) != 0)) && lane == 0)
+            if (__any_sync(FULL, valid && (cls > 2 || T > 4096)) && lane == 0)
                 atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
             if (valid && cls != kClassDynamic && !P.dyn_only) {
                 const uint64_t phys = (uint64_t)r.y + e.x + P.ctx;

@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(WARPS * 32, 32 / WARPS) k_simulate(const DevGe
             const uint4 r = __ldg(P.jobs + j0 + j);
             const uint4 e = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
             const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
-            if (cls > 2 || T > 4096 || (r.z >> 24) != 0) err |= (uint32_t)MIG_ERR_BAD_RECORD;
+            if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
             uint4 A, Bv;
             A.x = T | (cls << 16);
             A.y = r.w;
@@ -941,7 +941,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
-                                 cudaStream_t stream);
+                                 uint4* pc, cudaStream_t stream);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
 // (8 or 32 lanes per trace).
@@ -995,19 +995,31 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
         uint16_t* ring = nullptr;
         e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * stride * sizeof(uint16_t), stream);
         if (e != cudaSuccess) return e;
+        bool any_pc = false;  // PCIe contention (R39): per lane and slot run state
+        for (uint32_t i = 0; i < n_pol; ++i) any_pc |= (pols[i].flags & MIG_PCIE_CONTENTION) != 0;
+        uint4* pc = nullptr;
+        if (any_pc) {
+            e = cudaMallocAsync(&pc, blocks * simulate_lane_threads() * 8 * 2 * sizeof(uint4), stream);
+            if (e != cudaSuccess) {
+                cudaFreeAsync(ring, stream);
+                return e;
+            }
+        }
         static const char* kNames[5] = {"sim_baseline", "sim_static", "sim_dynamic", "sim_ff", "sim_scheme_a"};
         for (uint32_t i = 0; i < n_pol && e == cudaSuccess; ++i) {
             e = (cudaError_t)mig_timed(kNames[pols[i].kind], stream, [&](uint32_t* nl) {
                 if (nl) *nl = 1;
                 return (int)launch_simulate_lane(Gdev, tr, pols[i], i, n_pol, est, out, totals, counter + 2 + i,
-                                                 est_err, ring, blocks, trans, n_q, a7, n_a7,
-                                                 stream);
+                                                 est_err, ring, blocks, trans, n_q, a7, n_a7, pc, stream);
             });
             ++*launches;
         }
         cudaFreeAsync(ring, stream);
+        if (pc) cudaFreeAsync(pc, stream);
         return e;
     }
+    for (uint32_t i = 0; i < n_pol; ++i)  // the group kernel has no contention model
+        if (pols[i].flags & MIG_PCIE_CONTENTION) return cudaErrorNotSupported;
     if (P.n_pol) {
         e = launch_variant<false>(Gdev, P, tr, sm_count, stream);
         if (e != cudaSuccess) return e;

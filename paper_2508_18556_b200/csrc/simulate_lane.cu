@@ -48,6 +48,7 @@ struct LaneParams {
     uint16_t* ring;                     // [grid threads][ring_cap] requeue FIFOs: job | need << 10 (15 = none)
     const uint2* trans;                 // mig_geometry::trans, [state][n_q] (FUSION_FISSION)
     const uint2* a7;                    // mig_geometry::a7, [state][n_a7] (FUSION_FISSION)
+    uint4* pc;                          // PCIe contention: per lane and start slot, 2 x uint4 of run state (R39)
     uint32_t n_q, n_a7;
     uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
     mig_policy pol;
@@ -119,7 +120,7 @@ __device__ __forceinline__ uint32_t lane_wave_ticks(const DevGeom& G, uint32_t t
     return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
 }
 
-template <int KIND>
+template <int KIND, bool PC>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) LaneShared S;
@@ -203,6 +204,12 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     uint16_t* glen = &s_sa[0][tid];
     uint16_t* nx = &s_sa[KIND == MIG_SCHEME_A ? 8 : 0][tid];
     uint32_t cur = 0xFFu, ns = 0, PM = 0, ready = 0;  // Scheme A: current group, its slices, pending-slice mask
+    // PCIe contention (R39): slot s run state at pcs[2s] = {W lo, W hi, tk, rs}, pcs[2s+1] = {D, mem, iters,
+    // F | started << 8 | dynamic << 9}; c_eff = transferring runs since the last retime; tick_end = an end event
+    // was applied at the current tick (a tick with only starts has no scheduler pass)
+    uint4* pcs = PC ? P.pc + (size_t)(blockIdx.x * kLaneThreads + tid) * 16u : nullptr;
+    uint32_t c_eff = 0;
+    bool tick_end = false;
     uint32_t* jk = &S.jk[0][tid];
     uint32_t* et = &S.et[0][tid];
     const uint32_t fp = G.full_prof;
@@ -262,6 +269,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 occ |= G.lenmask[p] << s;
             }
         }
+        c_eff = 0;
         if (KIND == MIG_SCHEME_A) {
             cur = 0xFFu;
             ns = PM = ready = 0;
@@ -322,6 +330,15 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             end = rs + T * ticks;
         }
         const uint32_t dur = end - rs;
+        if constexpr (PC) {  // R39: the run's end follows its progress; power, memory and waste at its end
+            const uint32_t it = ek == 1 ? fe : ek == 2 ? i_pre : T;
+            const uint32_t mem =
+                dyn ? __ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) : phys;
+            pcs[2 * s] = make_uint4(0u, 0u, rs, rs);
+            pcs[2 * s + 1] = make_uint4(dur, mem, it, (hr.z >> 24) | (dyn ? 0x200u : 0u));
+            end = rs;  // the slot's next event: the run's start
+            return;
+        }
         a_busy += (uint64_t)comp * dur;
         if (__builtin_expect(dyn, 0)) {
             const uint32_t* m = reinterpret_cast<const uint32_t*>(ej) + 12;  // mem_fe[5], mem_conv, mem_T
@@ -331,10 +348,67 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         }
         if (ek) a_waste += dur;
     };
+    // PCIe contention (reading R39): a transferring run (F > 0) advances at
+    // 2^24 / (256 - F + F c) units of 2^-16 nominal ticks per tick, c = transferring runs in progress.
+    auto pc_rate = [](uint32_t F, uint32_t c) -> uint64_t { return F ? (1u << 24) / (256u - F + F * c) : 65536u; };
+    auto pc_advance = [&](uint32_t tn) {  // every run in progress advances to tn at the rate in effect
+        for (uint32_t m = BS; m; m &= m - 1u) {
+            const uint32_t s = (uint32_t)__ffs(m) - 1u;
+            uint4 a = pcs[2 * s];
+            const uint32_t misc = pcs[2 * s + 1].w;
+            if (!((misc >> 8) & 1u)) continue;
+            const uint64_t W = ((uint64_t)a.y << 32 | a.x) - (uint64_t)(tn - a.z) * pc_rate(misc & 0xFFu, c_eff);
+            a.x = (uint32_t)W;
+            a.y = (uint32_t)(W >> 32);
+            a.z = tn;
+            pcs[2 * s] = a;
+        }
+    };
+    auto pc_retime = [&]() {  // runs due now start; recount c; every run in progress gets its end for the new rate
+        uint32_t c = 0;
+        for (uint32_t m = BS; m; m &= m - 1u) {
+            const uint32_t s = (uint32_t)__ffs(m) - 1u;
+            uint4 b = pcs[2 * s + 1];
+            if (!((b.w >> 8) & 1u) && pcs[2 * s].w == t) {
+                const uint64_t W = (uint64_t)b.x << 16;
+                pcs[2 * s] = make_uint4((uint32_t)W, (uint32_t)(W >> 32), t, t);
+                b.w |= 0x100u;
+                pcs[2 * s + 1] = b;
+            }
+            c += ((b.w >> 8) & 1u) && (b.w & 0xFFu) ? 1u : 0u;
+        }
+        for (uint32_t m = BS; m; m &= m - 1u) {
+            const uint32_t s = (uint32_t)__ffs(m) - 1u;
+            const uint32_t misc = pcs[2 * s + 1].w;
+            if (!((misc >> 8) & 1u)) continue;
+            const uint4 a = pcs[2 * s];
+            const uint64_t W = (uint64_t)a.y << 32 | a.x, rho = pc_rate(misc & 0xFFu, c);
+            et[s * kLaneThreads] = t + (uint32_t)((W + rho - 1u) / rho);
+        }
+        c_eff = c;
+    };
+    // Slot es's event at t under contention: a start (no record; returns true) or an end whose actual duration
+    // is accounted here (power R26, memory integral, waste).
+    auto pc_event = [&](uint32_t es, uint32_t ek, uint32_t comp) -> bool {
+        uint4 b = pcs[2 * es + 1];
+        if (!((b.w >> 8) & 1u)) {
+            const uint64_t W = (uint64_t)b.x << 16;
+            pcs[2 * es] = make_uint4((uint32_t)W, (uint32_t)(W >> 32), t, t);
+            b.w |= 0x100u;
+            pcs[2 * es + 1] = b;
+            return true;
+        }
+        const uint32_t actual = t - pcs[2 * es].w;
+        a_busy += (uint64_t)comp * actual;
+        a_mem += (b.w & 0x200u) ? (b.z ? (uint64_t)b.y * actual / b.z : 0ull) : (uint64_t)b.y * actual;
+        if (ek) a_waste += actual;
+        tick_end = true;
+        return false;
+    };
     auto head_need = [&]() {  // first evaluation of an initial queue entry: tight fit of req0 + record checks
         if (hneed == kUnk) {
             const uint32_t cls = (hr.z >> 16) & 0xFFu, T = hr.z & 0xFFFFu;
-            if (cls > 2 || T > 4096 || (hr.z >> 24) != 0) err |= (uint32_t)MIG_ERR_BAD_RECORD;
+            if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
             const uint32_t req0 = cls == kClassDynamic ? G.mem[0] : hr.x + he.x + P.ctx;  // R16 / est + ws + ctx
             hneed = lane_tight_fit(S, req0, he.y, fold);
         }
@@ -457,6 +531,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             __syncwarp();
             if (mode == 1) {  // the events of the next tick (R28), then dispatch again
                 if (!evm) {
+                    if constexpr (PC) pc_retime();
                     uint32_t e8[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) e8[k] = et[k * kLaneThreads];
@@ -467,6 +542,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         mode = 2;
                     } else {
                         t = tn;
+                        if constexpr (PC) {
+                            pc_advance(tn);  // the runs in progress reach tn at the rate in effect
+                            tick_end = false;
+                        }
 #pragma unroll
                         for (int k = 0; k < 8; ++k) evm |= (e8[k] == tn ? 1u : 0u) << k;
                     }
@@ -485,37 +564,40 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     evm &= ~(1u << es);
                     const uint32_t job = v & 0xFFFFu, ek = v >> 16;
                     const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = G.pinfo[epr];
-                    const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
-                    lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));
-                    a_turn += ek == 0 ? t : 0u;
-                    K2 += ek == 1 ? 1u << 16 : 0u;
-                    K3 += ek == 2 ? 1u : 0u;
-                    uint32_t req = 0;
-                    if (ek == 1) {
-                        req = G.level_next[si & 0xFu];
-                        if (req == 0) {
-                            lrec(hl, hh, t, elo | (K_FAILED << 12));
-                            K3 += 1u << 16;
+                    const bool pc_start = PC && pc_event(es, ek, (si >> 4) & 0xFu);  // R39: a start, no record
+                    if (!pc_start) {
+                        const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
+                        lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));
+                        a_turn += ek == 0 ? t : 0u;
+                        K2 += ek == 1 ? 1u << 16 : 0u;
+                        K3 += ek == 2 ? 1u : 0u;
+                        uint32_t req = 0;
+                        if (ek == 1) {
+                            req = G.level_next[si & 0xFu];
+                            if (req == 0) {
+                                lrec(hl, hh, t, elo | (K_FAILED << 12));
+                                K3 += 1u << 16;
+                            }
+                        } else if (ek == 2) {
+                            req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
                         }
-                    } else if (ek == 2) {
-                        req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
-                    }
-                    if (req) {  // the tail of the job's new (larger) group
-                        const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
-                        const uint32_t nn = lane_tight_fit(S, req, w, fold);
-                        if (nn == kNoNeed) {
-                            lrec(hl, hh, t, (job << 16) | (K_REJECT << 12) | 0xFF0u);
-                            K2 += 1u;
-                        } else {
-                            const uint32_t lv = G.level[nn], c = glen[lv * kLaneThreads];
-                            ring[lv * P.ring_cap + c] = (uint16_t)job;
-                            glen[lv * kLaneThreads] = (uint16_t)(c + 1u);
+                        if (req) {  // the tail of the job's new (larger) group
+                            const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
+                            const uint32_t nn = lane_tight_fit(S, req, w, fold);
+                            if (nn == kNoNeed) {
+                                lrec(hl, hh, t, (job << 16) | (K_REJECT << 12) | 0xFF0u);
+                                K2 += 1u;
+                            } else {
+                                const uint32_t lv = G.level[nn], c = glen[lv * kLaneThreads];
+                                ring[lv * P.ring_cap + c] = (uint16_t)job;
+                                glen[lv * kLaneThreads] = (uint16_t)(c + 1u);
+                            }
                         }
+                        et[es * kLaneThreads] = kNoEnd;
+                        BS &= ~(1u << es);
+                        BM &= ~(((si >> 8) & 0xFFu) << es);
                     }
-                    et[es * kLaneThreads] = kNoEnd;
-                    BS &= ~(1u << es);
-                    BM &= ~(((si >> 8) & 0xFFu) << es);
-                    if (!evm) mode = 0;
+                    if (!evm) mode = (PC && !tick_end) ? 1u : 0u;  // a tick with only starts has no pass
                 }
             }
         } else {
@@ -632,6 +714,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             // ---- EVT: apply one event (min end tick; ties COMPLETE < OOM < PREEMPT, then job id, R28) ----
             if (mode == 1) {
                 if (!evm) {
+                    if constexpr (PC) pc_retime();
                     uint32_t e8[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) e8[k] = et[k * kLaneThreads];
@@ -642,6 +725,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         mode = 2;
                     } else {
                         t = tn;
+                        if constexpr (PC) {
+                            pc_advance(tn);  // the runs in progress reach tn at the rate in effect
+                            tick_end = false;
+                        }
 #pragma unroll
                         for (int k = 0; k < 8; ++k) evm |= (e8[k] == tn ? 1u : 0u) << k;
                     }
@@ -664,40 +751,43 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     evm &= ~(1u << es);
                     const uint32_t job = v & 0xFFFFu, ek = v >> 16;
                     const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = G.pinfo[epr];
-                    const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
-                    lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7 / PREEMPT 8
-                    a_turn += ek == 0 ? t : 0u;
-                    K2 += ek == 1 ? 1u << 16 : 0u;
-                    K3 += ek == 2 ? 1u : 0u;
-                    uint32_t req = 0;
-                    if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
-                        req = G.level_next[si & 0xFu];
-                        if (req == 0) {
-                            lrec(hl, hh, t, elo | (K_FAILED << 12));
-                            K3 += 1u << 16;
+                    const bool pc_start = PC && pc_event(es, ek, (si >> 4) & 0xFu);  // R39: a start, no record
+                    if (!pc_start) {
+                        const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
+                        lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7 / PREEMPT 8
+                        a_turn += ek == 0 ? t : 0u;
+                        K2 += ek == 1 ? 1u << 16 : 0u;
+                        K3 += ek == 2 ? 1u : 0u;
+                        uint32_t req = 0;
+                        if (ek == 1) {  // OOM: next larger slice (R14) or FAILED on the whole GPU
+                            req = G.level_next[si & 0xFu];
+                            if (req == 0) {
+                                lrec(hl, hh, t, elo | (K_FAILED << 12));
+                                K3 += 1u << 16;
+                            }
+                        } else if (ek == 2) {  // PREEMPT: restart on the slice meeting the forecast (R25)
+                            req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
                         }
-                    } else if (ek == 2) {  // PREEMPT: restart on the slice meeting the forecast (R25)
-                        req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
+                        if (req) {  // back to the queue tail (R13) with the new tight fit
+                            const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
+                            const uint32_t nn = lane_tight_fit(S, req, w, fold);
+                            uint32_t pos = rh + rn;
+                            if (pos >= P.ring_cap) pos -= P.ring_cap;
+                            ring[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
+                            ++rn;
+                            if (hj == kNoJob) fetch_head();
+                        }
+                        et[es * kLaneThreads] = kNoEnd;
+                        const uint32_t ext = ((si >> 8) & 0xFFu) << es;
+                        BS &= ~(1u << es);
+                        BM &= ~ext;
+                        if (KIND == MIG_DYNAMIC) {  // free on completion (R10)
+                            occ &= ~ext;
+                            K1 += 1u;
+                        }
+                        if (KIND == MIG_FUSION_FISSION) IPM |= 1ull << (8 * epr + es);  // the instance is idle
                     }
-                    if (req) {  // back to the queue tail (R13) with the new tight fit
-                        const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
-                        const uint32_t nn = lane_tight_fit(S, req, w, fold);
-                        uint32_t pos = rh + rn;
-                        if (pos >= P.ring_cap) pos -= P.ring_cap;
-                        ring[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
-                        ++rn;
-                        if (hj == kNoJob) fetch_head();
-                    }
-                    et[es * kLaneThreads] = kNoEnd;
-                    const uint32_t ext = ((si >> 8) & 0xFFu) << es;
-                    BS &= ~(1u << es);
-                    BM &= ~ext;
-                    if (KIND == MIG_DYNAMIC) {  // free on completion (R10)
-                        occ &= ~ext;
-                        K1 += 1u;
-                    }
-                    if (KIND == MIG_FUSION_FISSION) IPM |= 1ull << (8 * epr + es);  // the instance is idle
-                    if (!evm) mode = 0;
+                    if (!evm) mode = (PC && !tick_end) ? 1u : 0u;  // a tick with only starts has no pass
                 }
             }
         }
@@ -785,7 +875,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
 // Grid: resident CTAs per SM x SMs (persistent; units are taken from the counter), capped by the unit count.
 uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate_lane<MIG_FUSION_FISSION>, kLaneThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate_lane<MIG_FUSION_FISSION, false>, kLaneThreads, 0);
     if (per_sm < 1) per_sm = 1;
     uint64_t blocks = (uint64_t)per_sm * sm_count;
     const uint64_t want = (n_traces + kLaneThreads - 1) / kLaneThreads;
@@ -801,7 +891,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
-                                 cudaStream_t stream) {
+                                 uint4* pc, cudaStream_t stream) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -824,13 +914,28 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     P.n_q = n_q;
     P.a7 = reinterpret_cast<const uint2*>(a7);
     P.n_a7 = n_a7;
+    P.pc = pc;
     const dim3 grid((unsigned)blocks), block(kLaneThreads);
+    const bool con = (pol.flags & MIG_PCIE_CONTENTION) != 0;  // BASELINE runs one job at a time: never contended
+    if (con && !P.pc) return cudaErrorInvalidValue;
     switch (pol.kind) {
-        case MIG_BASELINE: k_simulate_lane<MIG_BASELINE><<<grid, block, 0, stream>>>(Gdev, P); break;
-        case MIG_STATIC: k_simulate_lane<MIG_STATIC><<<grid, block, 0, stream>>>(Gdev, P); break;
-        case MIG_DYNAMIC: k_simulate_lane<MIG_DYNAMIC><<<grid, block, 0, stream>>>(Gdev, P); break;
-        case MIG_FUSION_FISSION: k_simulate_lane<MIG_FUSION_FISSION><<<grid, block, 0, stream>>>(Gdev, P); break;
-        case MIG_SCHEME_A: k_simulate_lane<MIG_SCHEME_A><<<grid, block, 0, stream>>>(Gdev, P); break;
+        case MIG_BASELINE: k_simulate_lane<MIG_BASELINE, false><<<grid, block, 0, stream>>>(Gdev, P); break;
+        case MIG_STATIC:
+            if (con) k_simulate_lane<MIG_STATIC, true><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_STATIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            break;
+        case MIG_DYNAMIC:
+            if (con) k_simulate_lane<MIG_DYNAMIC, true><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_DYNAMIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            break;
+        case MIG_FUSION_FISSION:
+            if (con) k_simulate_lane<MIG_FUSION_FISSION, true><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_FUSION_FISSION, false><<<grid, block, 0, stream>>>(Gdev, P);
+            break;
+        case MIG_SCHEME_A:
+            if (con) k_simulate_lane<MIG_SCHEME_A, true><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
+            break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

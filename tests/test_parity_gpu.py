@@ -101,7 +101,7 @@ def test_estimates_match_oracle(cfg, n):
     assert dyn.any() and (est["conv_iter"][dyn] > 0).any()
 
 
-def random_tiny_traces(rng, geo_spec, n_traces, max_len, dyn_frac=0.3):
+def random_tiny_traces(rng, geo_spec, n_traces, max_len, dyn_frac=0.3, xfer=False):
     slot = geo_spec["slot_mib"]
     full = geo_spec["total_memory_slots"] * slot
     traces = []
@@ -113,13 +113,15 @@ def random_tiny_traces(rng, geo_spec, n_traces, max_len, dyn_frac=0.3):
                 T = int(rng.integers(1, 300))
                 tr.append(tg.pack_job(b, 65536, T, 2, int(rng.integers(1, 50)), ws=int(rng.integers(0, 64)),
                                       slope_q8=int(rng.integers(0, 200 * 256)), sigma=int(rng.integers(0, 200)),
-                                      qslope=int(rng.integers(0, 100))))
+                                      qslope=int(rng.integers(0, 100)),
+                                      xfer=int(rng.integers(0, 256)) if xfer and rng.random() < 0.6 else 0))
             else:
                 est = int(rng.integers(1, full + 4000))
                 tru = est if rng.random() < 0.6 else int(rng.integers(1, full + 4000))
                 tr.append(tg.pack_job(est, tru, int(rng.integers(0, 6)), int(rng.integers(0, 2)),
                                       int(rng.integers(1, 2000)), ws=int(rng.integers(0, 100)),
-                                      warps=int(rng.integers(0, 20000))))
+                                      warps=int(rng.integers(0, 20000)),
+                                      xfer=int(rng.integers(0, 256)) if xfer and rng.random() < 0.6 else 0))
         traces.append(tr)
     return tg.pack_traces(traces)
 
@@ -261,3 +263,35 @@ def test_recorded_samples_parity(cfg, n, monkeypatch):
     monkeypatch.setenv("MIG_HOST_CHUNK_JOBS", "3000")
     hres, _ = mig.mig_simulate_host(g, jobs, ext, off, pols, seed=wrong_seed, samples=smp, sample_off=soff)
     assert_same(hres, want)
+
+
+@pytest.mark.parametrize("geo", ["a30-24gb", "a100-40gb", "b200-180gb"])
+def test_pcie_contention_parity(geo):
+    """MIG_PCIE_CONTENTION (R39): re-timed runs, start events, actual-duration power / memory / waste, on random
+    ragged traces with random transfer fractions, every policy (Scheme A and early restart included), with and
+    without creation delays."""
+    spec = json.load(open(geom_path(geo)))
+    rng = np.random.default_rng(17)
+    jobs, ext, off = random_tiny_traces(rng, spec, 600, 30, xfer=True)
+    specs = [dict(kind=k, flags=16) for k in range(5)] + [dict(kind=3, flags=17), dict(kind=4, flags=17),
+                                                          dict(kind=2, flags=16 | 8)]
+    for common in [dict(ctx_mib=0, reconfig_ticks=0), dict(ctx_mib=512, reconfig_ticks=500)]:
+        got, want, tot = run_pair(geo, jobs, ext, off, specs, seed=23, common=common)
+        assert_same(got, want)
+        check_totals(got, tot)
+
+
+def test_pcie_contention_generated_config5():
+    """Config-5 traces (five policies) with transfer fractions added to the records, against the oracle."""
+    jobs, ext, off = tg.generate_host(5, 300)
+    rng = np.random.default_rng(29)
+    jobs = jobs.copy()
+    jobs[:, 2] |= (rng.integers(0, 128, len(jobs)).astype(np.uint32) << 24)
+    specs = [dict(kind=k, flags=16) for k in range(5)] + [dict(kind=3, flags=17)]
+    got, want, tot = run_pair(tg.CONFIG_GEOMETRY[5], jobs, ext, off, specs, seed=tg.seed_of(5))
+    assert_same(got, want)
+    check_totals(got, tot)
+    plain = orc.simulate(orc.Geometry(geom_path(tg.CONFIG_GEOMETRY[5])), jobs, ext, off,
+                         [orc.policy(**{**sp, "flags": sp["flags"] & ~16}) for sp in specs], seed=tg.seed_of(5))
+    assert (plain["makespan"][:, 3] < want["makespan"][:, 3]).mean() > 0.5  # contention slows FF down
+    assert np.array_equal(plain["makespan"][:, 0], want["makespan"][:, 0])  # one run at a time: never contended
