@@ -376,6 +376,7 @@ void peak_memory_prediction(const std::vector<uint32_t>& y, const std::vector<ui
 struct Job {
     uint32_t cls, iters, ticks, est, tru, ws, warps;
     uint32_t xfer;               // PCIe transfer fraction of an iteration, in 1/256 (record bits 24-31, R39)
+    uint32_t arrival = 0;        // arrival tick (R40; 0 = batch)
     uint32_t b, q0, slope_q8, sigma, qslope;
     std::vector<uint32_t> y, q;  // DYNAMIC samples i = 1..T
     OrEstimate e;
@@ -503,6 +504,7 @@ struct Sim {
     std::priority_queue<Event, std::vector<Event>, std::greater<Event>> events;
     OrResult r;
     uint32_t t = 0;
+    size_t next_arrival = 0;  // R40: jobs [0, next_arrival) have arrived (arrival ticks are non-decreasing)
     std::vector<uint64_t>* rec_out;
     std::string err;
 
@@ -671,7 +673,7 @@ struct Sim {
     void run_pcie(bool scheme_a) {
         retime();
         for (;;) {
-            uint32_t tn = 0xFFFFFFFFu;
+            uint32_t tn = next_arrival_tick();
             for (const Instance& in : inst)
                 if (in.busy) tn = std::min(tn, in.started ? in.end : in.run_start);
             if (tn == 0xFFFFFFFFu) break;
@@ -683,8 +685,9 @@ struct Sim {
                     ends.push_back({((uint64_t)inst[k].kind_order << 32) | (uint32_t)inst[k].job, inst[k].start});
             std::sort(ends.begin(), ends.end());
             for (auto& e : ends) end_run(find_instance(e.second));
-            if (!ends.empty()) {
-                r.makespan = t;
+            const bool arrived = !scheme_a && admit_arrivals();
+            if (!ends.empty()) r.makespan = t;
+            if (!ends.empty() || arrived) {
                 if (scheme_a) a_step();
                 else scheduler_pass();
             }
@@ -833,6 +836,20 @@ struct Sim {
         }
     }
 
+    // Arrival streams (reading R40): every job whose arrival tick is <= t joins the queue tail, in queue order,
+    // after the requeues of the events at t. Returns whether any arrived.
+    bool admit_arrivals() {
+        bool any = false;
+        while (next_arrival < jobs.size() && jobs[next_arrival].arrival <= t) {
+            queue.push_back((int)next_arrival++);
+            any = true;
+        }
+        return any;
+    }
+    uint32_t next_arrival_tick() const {
+        return next_arrival < jobs.size() ? jobs[next_arrival].arrival : 0xFFFFFFFFu;
+    }
+
     // Next-larger slice after an OOM (R14): smallest profile memory strictly above cap.
     bool next_larger(uint32_t cap, uint32_t* out) {
         for (uint32_t p = 0; p < g.d.n_prof; ++p)
@@ -864,7 +881,7 @@ struct Sim {
         if (ev.kind_order == 0) {
             record(t, ev.job, K_COMPLETE, in.start, in.prof, 0);
             r.completed++;
-            r.turnaround_sum += t;  // all jobs arrive at t = 0 (batch, R34)
+            r.turnaround_sum += t - j.arrival;  // completion - arrival (R34: batch, all 0; R40: streams)
         } else if (ev.kind_order == 1) {
             record(t, ev.job, K_OOM, in.start, in.prof, 0);
             r.ooms++;
@@ -980,6 +997,7 @@ struct Sim {
         gs.lists.assign(levels(g).size(), {});
         t = 0;
         for (size_t i = 0; i < jobs.size(); ++i) a_enqueue((int)i);  // REJECTs at t = 0, in queue order
+        next_arrival = jobs.size();                                   // the whole queue is grouped at t = 0
         a_step();
         if (pol.flags & F_PCIE) run_pcie(true);
         while (!events.empty()) {
@@ -1009,18 +1027,22 @@ struct Sim {
             for (uint32_t i = 0; i < g.d.n_layout; ++i)
                 inst.push_back({(int)g.d.layout_prof[i], (int)g.d.layout_start[i], false, -1, 0});
         }
-        for (size_t i = 0; i < jobs.size(); ++i) queue.push_back((int)i);
         t = 0;
+        admit_arrivals();
         scheduler_pass();
         if (pol.flags & F_PCIE) run_pcie(false);
-        while (!events.empty()) {
-            t = events.top().tick;
+        // the next tick: the earliest run end or job arrival (R9, R40)
+        while (!events.empty() || next_arrival < jobs.size()) {
+            t = std::min(events.empty() ? 0xFFFFFFFFu : events.top().tick, next_arrival_tick());
+            bool ended = false;
             while (!events.empty() && events.top().tick == t) {
                 Event ev = events.top();
                 events.pop();
                 apply(ev);
+                ended = true;
             }
-            r.makespan = t;
+            if (ended) r.makespan = t;
+            admit_arrivals();
             scheduler_pass();
             check_invariants();
             if (!err.empty()) return;
@@ -1143,7 +1165,7 @@ int or_estimate(void* gp, const uint32_t* jobs, const uint32_t* ext, const uint6
 int or_simulate(void* gp, const uint32_t* jobs, const uint32_t* ext, const uint64_t* trace_off, uint64_t t0,
                 uint64_t t1, uint64_t trace_id0, uint64_t seed, const OrPolicy* pols, uint32_t n_pol, OrResult* out,
                 uint64_t* rec, uint64_t rec_cap, uint64_t* rec_n, const uint32_t* samples,
-                const uint64_t* sample_off) {
+                const uint64_t* sample_off, const uint32_t* arrival) {
     Geometry* g = (Geometry*)gp;
     g_err.clear();
     for (uint64_t t = t0; t < t1; ++t) {
@@ -1154,9 +1176,21 @@ int or_simulate(void* gp, const uint32_t* jobs, const uint32_t* ext, const uint6
         }
         for (uint32_t p = 0; p < n_pol; ++p) {
             std::vector<Job> js;
-            for (uint64_t j = trace_off[t]; j < trace_off[t + 1]; ++j)
+            for (uint64_t j = trace_off[t]; j < trace_off[t + 1]; ++j) {
                 js.push_back(load_job(*g, jobs + 4 * j, ext ? ext + 4 * j : nullptr, seed, trace_id0 + t,
                                       (uint32_t)(j - trace_off[t]), pols[p], recorded(samples, sample_off, j)));
+                if (arrival) {  // R40: non-decreasing within a trace
+                    js.back().arrival = arrival[j];
+                    if (js.size() > 1 && arrival[j] < js[js.size() - 2].arrival) {
+                        g_err = "trace " + std::to_string(t) + ": arrival ticks decrease";
+                        return -1;
+                    }
+                }
+            }
+            if (arrival && pols[p].kind == SCHEME_A) {
+                g_err = "Scheme A groups the whole queue at t = 0: no arrival streams";
+                return -1;
+            }
             std::vector<uint64_t> recs;
             Sim sim(*g, pols[p], js, rec ? &recs : nullptr);
             sim.run();

@@ -84,7 +84,7 @@ def lib():
                                   C.c_uint64, C.POINTER(OrPolicy), C.c_void_p, C.c_void_p, C.c_void_p]
         L.or_simulate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
                                   C.c_uint64, C.c_uint64, C.POINTER(OrPolicy), C.c_uint32, C.c_void_p, C.c_void_p,
-                                  C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p]
+                                  C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -217,8 +217,9 @@ def estimate(geom: Geometry, jobs, ext, trace_off, pol, seed=0, trace_id0=0, sam
 
 
 def simulate(geom: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, t0=0, t1=None, records=False,
-             samples=None, sample_off=None):
-    """Run the oracle on traces [t0, t1). Returns results[(t1-t0), n_pol] (and the record list if records)."""
+             samples=None, sample_off=None, arrival=None):
+    """Run the oracle on traces [t0, t1). Returns results[(t1-t0), n_pol] (and the record list if records).
+    arrival: per-job arrival ticks (reading R40) or None (batch: all at t = 0)."""
     if not isinstance(pols, (list, tuple)):
         pols = [pols]
     n_traces = len(trace_off) - 1
@@ -236,7 +237,7 @@ def simulate(geom: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, t0
     smp, soff = _samples(samples, sample_off)
     rc = lib().or_simulate(geom.h, _ptr(jobs), _ptr(ext), _ptr(off), t0, t1, trace_id0, seed, parr, len(pols),
                            _ptr(out), _ptr(rec), 0 if rec is None else len(rec), C.byref(rec_n), _ptr(smp),
-                           _ptr(soff))
+                           _ptr(soff), _ptr(None if arrival is None else np.ascontiguousarray(arrival, np.uint32)))
     if rc != 0:
         raise RuntimeError(lib().or_last_error().decode())
     if records:

@@ -355,3 +355,70 @@ def test_pcie_retime_when_a_transfer_run_starts_late():
     assert r["turnaround_sum"] == 1301 + 400 + 400 + 1701
     plain = _pcie_run("a100-40gb", [A, C, D, B], kind=1, flags=0)
     assert plain["makespan"] == 1400
+
+
+# ---- arrival streams (reading R40; R34's batch arrival is the paper's setting) ----
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+@pytest.mark.parametrize("flags", [0, 1, 16])
+def test_arrivals_at_zero_equal_batch(kind, flags):
+    """Every job arriving at t = 0 is the batch setting: identical results, decision hash included."""
+    jobs, ext, off = tg.generate_host(5, 30)
+    g = orc.Geometry(geom_path("a100-40gb"))
+    a = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, flags=flags))
+    b = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, flags=flags), arrival=np.zeros(len(jobs), np.uint32))
+    for f in orc.RESULT_DTYPE.names:
+        assert np.array_equal(a[f], b[f]), f
+
+
+def test_arrival_waits_then_fuses():
+    """A (5 GB, 100 ticks) arrives at 0, B (40 GB, 50 ticks) at 10. FUSION_FISSION, ctx = reconfig = 0:
+    t=0 A ALLOC 1g@6; t=10 B's arrival wakes the scheduler: B WAIT (the whole GPU overlaps busy A); t=100 A
+    COMPLETE, B RECONF 7g@0 destroying A's idle slice; t=150 B COMPLETE. Turnaround 100 + 140; energy
+    30*150 + 25*(1*100 + 7*50) = 15750 W*ticks."""
+    A = tg.pack_job(4096, 4096, 10, 0, 10)
+    B = tg.pack_job(40960, 40960, 5, 0, 10)
+    jobs, ext, off = tg.pack_traces([[A, B]])
+    g = orc.Geometry(geom_path("a100-40gb"))
+    r, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=3, ctx_mib=0, reconfig_ticks=0), records=True,
+                           arrival=np.array([0, 10], np.uint32))
+    r = r[0, 0]
+    got = [(x["tick"], x["job"], x["kind"], x["start"], x["n_destroyed"]) for x in recs]
+    assert got == [(0, 0, "ALLOC", 6, 0), (10, 1, "WAIT", 15, 0), (100, 0, "COMPLETE", 6, 0),
+                   (100, 1, "RECONF", 0, 1), (150, 1, "COMPLETE", 0, 0)]
+    assert r["makespan"] == 150 and r["turnaround_sum"] == 100 + 140 and r["energy_wticks"] == 15750
+    assert r["placements"] == 2 and r["waits"] == 1 and r["creates"] == 2 and r["destroys"] == 1
+
+
+def test_arrival_gap_idles_the_gpu():
+    """A (10 ticks) at 0, B (10 ticks) at 1000: the GPU idles in between; makespan 1010, turnaround 10 + 10,
+    energy 30*1010 + 25*(10 + 10)."""
+    A = tg.pack_job(4096, 4096, 1, 0, 10)
+    jobs, ext, off = tg.pack_traces([[A, A]])
+    g = orc.Geometry(geom_path("a100-40gb"))
+    for kind in (0, 2, 3):
+        r = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, ctx_mib=0, reconfig_ticks=0),
+                         arrival=np.array([0, 1000], np.uint32))[0, 0]
+        comp = 7 if kind == 0 else 1
+        assert r["makespan"] == 1010 and r["turnaround_sum"] == 20
+        assert r["energy_wticks"] == 30 * 1010 + 25 * comp * 20
+
+
+def test_arrivals_spaced_beyond_durations_run_alone():
+    """Arrival gaps longer than every job: each runs alone from its arrival; makespan = last arrival + its run;
+    turnaround = sum of the runs (S:386 'turnaround = mean(completion - arrival)')."""
+    rng = np.random.default_rng(3)
+    js, arr, t = [], [], 0
+    for _ in range(12):
+        it, ticks = int(rng.integers(1, 6)), int(rng.integers(1, 100))
+        js.append(tg.pack_job(4096, 4096, it, 0, ticks))
+        arr.append(t)
+        last = it * ticks
+        t += 600
+    jobs, ext, off = tg.pack_traces([js])
+    g = orc.Geometry(geom_path("a100-40gb"))
+    durs = [int(j[0][2] & 0xFFFF) * int(j[0][3]) for j in js]
+    for kind in (0, 1, 2, 3):
+        r = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, ctx_mib=0, reconfig_ticks=0),
+                         arrival=np.array(arr, np.uint32))[0, 0]
+        assert r["makespan"] == arr[-1] + durs[-1] and r["turnaround_sum"] == sum(durs) and r["waits"] == 0
