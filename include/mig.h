@@ -137,6 +137,13 @@ typedef struct {
      * with the job records (jobs[k] <-> sample_off[k]). */
     const void* samples;        /* 8 B per sample (uint2)                                                */
     const uint64_t* sample_off; /* n_jobs + 1, or NULL when samples is NULL                              */
+    /* Arrival streams (reading R40; the paper's setting is batch, all at t = 0): arrival
+     * tick of every job, aligned with the job records (points at the tick of job trace_off[0]), non-decreasing
+     * within a trace (a decrease is flagged MIG_ERR_BAD_RECORD), or NULL = batch. A job joins the queue tail at
+     * its arrival, after the requeues of that tick's events; every arrival wakes the scheduler (R9);
+     * turnaround = completion - arrival; makespan = the last tick with an end or an arrival. Not with MIG_SCHEME_A
+ * (MIG_E_INVALID_ARG). */
+    const uint32_t* arrival;
 } mig_traces;
 
 #define MIG_MAX_JOBS_PER_TRACE 768 /* on-chip (shared-memory) staging limit of one trace */

@@ -686,7 +686,7 @@ struct Sim {
             std::sort(ends.begin(), ends.end());
             for (auto& e : ends) end_run(find_instance(e.second));
             const bool arrived = !scheme_a && admit_arrivals();
-            if (!ends.empty()) r.makespan = t;
+            if (!ends.empty() || arrived) r.makespan = t;
             if (!ends.empty() || arrived) {
                 if (scheme_a) a_step();
                 else scheduler_pass();
@@ -1034,14 +1034,12 @@ struct Sim {
         // the next tick: the earliest run end or job arrival (R9, R40)
         while (!events.empty() || next_arrival < jobs.size()) {
             t = std::min(events.empty() ? 0xFFFFFFFFu : events.top().tick, next_arrival_tick());
-            bool ended = false;
             while (!events.empty() && events.top().tick == t) {
                 Event ev = events.top();
                 events.pop();
                 apply(ev);
-                ended = true;
             }
-            if (ended) r.makespan = t;
+            r.makespan = t;  // the last tick with an end or an arrival (R40: a late arrival may only be rejected)
             admit_arrivals();
             scheduler_pass();
             check_invariants();

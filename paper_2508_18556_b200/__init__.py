@@ -57,7 +57,8 @@ class mig_geometry_info(C.Structure):
 class mig_traces(C.Structure):
     _fields_ = [("jobs", C.c_void_p), ("jobs_ext", C.c_void_p), ("trace_off", C.c_void_p), ("n_traces", C.c_uint64),
                 ("trace_id0", C.c_uint64), ("seed", C.c_uint64), ("n_jobs", C.c_uint64), ("max_jobs", C.c_uint32),
-                ("reserved", C.c_uint32), ("samples", C.c_void_p), ("sample_off", C.c_void_p)]
+                ("reserved", C.c_uint32), ("samples", C.c_void_p), ("sample_off", C.c_void_p),
+                ("arrival", C.c_void_p)]
 
 
 class mig_policy(C.Structure):
@@ -178,8 +179,9 @@ class Traces:
     """Device-resident traces: keeps the tensors alive and carries the mig_traces descriptor."""
 
     def __init__(self, jobs, ext, trace_off, n_traces, seed=0, trace_id0=0, max_jobs=None, n_jobs=None,
-                 samples=None, sample_off=None):
+                 samples=None, sample_off=None, arrival=None):
         self.jobs, self.ext, self.trace_off = jobs, ext, trace_off
+        self.arrival = arrival
         self.samples, self.sample_off = samples, sample_off
         self.n_traces = int(n_traces)
         self.n_jobs = int(jobs.shape[0]) if n_jobs is None else int(n_jobs)
@@ -192,11 +194,12 @@ class Traces:
                                ext.data_ptr() if ext is not None else None, trace_off.data_ptr(), self.n_traces,
                                trace_id0, seed, self.n_jobs, self.max_jobs, 0,
                                None if samples is None else samples.data_ptr(),
-                               None if sample_off is None else sample_off.data_ptr())
+                               None if sample_off is None else sample_off.data_ptr(),
+                               None if arrival is None else arrival.data_ptr())
 
 
 def traces_from_numpy(jobs, ext, trace_off, seed=0, trace_id0=0, device=None, max_jobs=None, samples=None,
-                      sample_off=None) -> Traces:
+                      sample_off=None, arrival=None) -> Traces:
     import torch
 
     dev = device or torch.device("cuda", torch.cuda.current_device())
@@ -210,7 +213,10 @@ def traces_from_numpy(jobs, ext, trace_off, seed=0, trace_id0=0, device=None, ma
     if samples is not None:
         smp = torch.from_numpy(np.ascontiguousarray(samples, np.uint32).view(np.int32).reshape(-1, 2)).to(dev)
         soff = torch.from_numpy(np.ascontiguousarray(sample_off, np.uint64).view(np.int64)).to(dev)
-    return Traces(j, e, o, len(trace_off) - 1, seed, trace_id0, max_jobs, samples=smp, sample_off=soff)
+    arr = None
+    if arrival is not None:
+        arr = torch.from_numpy(np.ascontiguousarray(arrival, np.uint32).view(np.int32)).to(dev)
+    return Traces(j, e, o, len(trace_off) - 1, seed, trace_id0, max_jobs, samples=smp, sample_off=soff, arrival=arr)
 
 
 def _stream_ptr(stream):
@@ -256,7 +262,7 @@ def mig_simulate(g: Geometry, tr: Traces, pols, est=None, out=None, totals=None,
 
 
 def mig_simulate_host(g: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, max_jobs=None, out=None,
-                      totals=None, samples=None, sample_off=None):
+                      totals=None, samples=None, sample_off=None, arrival=None):
     """HOST buffers in, HOST results out (page-locked numpy views recommended). Returns (results [n_traces, n_pol]
     RESULT_DTYPE, totals [n_pol] TOTALS_DTYPE)."""
     parr, n = _policies(pols)
@@ -271,10 +277,13 @@ def mig_simulate_host(g: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0
     if samples is not None:
         samples = np.ascontiguousarray(samples, np.uint32)
         sample_off = np.ascontiguousarray(sample_off, np.uint64)
+    if arrival is not None:
+        arrival = np.ascontiguousarray(arrival, np.uint32)
     desc = mig_traces(jobs.ctypes.data if len(jobs) else None, None if ext is None else ext.ctypes.data,
                       trace_off.ctypes.data, n_traces, trace_id0, seed, int(trace_off[-1] - trace_off[0]), max_jobs, 0,
                       None if samples is None else samples.ctypes.data,
-                      None if sample_off is None else sample_off.ctypes.data)
+                      None if sample_off is None else sample_off.ctypes.data,
+                      None if arrival is None else arrival.ctypes.data)
     _check(_lib.mig_simulate_host(g.h, C.byref(desc), parr, n, out.ctypes.data, totals.ctypes.data))
     return out, totals
 

@@ -159,12 +159,14 @@ mig_status check_policy(const mig_policy& p) {
     return MIG_OK;
 }
 
-mig_status check_policies(const mig_geometry* g, const mig_policy* pols, uint32_t n) {
+mig_status check_policies(const mig_geometry* g, const mig_policy* pols, uint32_t n, const mig_traces* tr) {
     if (!pols || n < 1 || n > (uint32_t)mig::kMaxPolicies)
         return mig_set_error(MIG_E_INVALID_ARG, "n_policies must be 1..8");
     for (uint32_t i = 0; i < n; ++i) {
         mig_status s = check_policy(pols[i]);
         if (s != MIG_OK) return s;
+        if (tr->arrival && pols[i].kind == MIG_SCHEME_A)
+            return mig_set_error(MIG_E_INVALID_ARG, "MIG_SCHEME_A groups the whole queue at t = 0: no arrival streams");
         if (pols[i].kind == MIG_STATIC && g->dg.n_layout == 0)
             return mig_set_error(MIG_E_INVALID_ARG, "MIG_STATIC needs a geometry with a static_layout");
         if (pols[i].kind == MIG_SCHEME_A && !g->info.scheme_a)
@@ -348,7 +350,7 @@ mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const m
     if (!g) return mig_set_error(MIG_E_INVALID_ARG, "mig_simulate: geometry is NULL");
     mig_status st = check_traces(traces);
     if (st != MIG_OK) return st;
-    st = check_policies(g, policies, n_policies);
+    st = check_policies(g, policies, n_policies, traces);
     if (st != MIG_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     mig::DevGeom* Gdev;
@@ -379,7 +381,7 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
     if (!g) return mig_set_error(MIG_E_INVALID_ARG, "mig_simulate_host: geometry is NULL");
     mig_status st = check_traces(traces);
     if (st != MIG_OK) return st;
-    st = check_policies(g, policies, n_policies);
+    st = check_policies(g, policies, n_policies, traces);
     if (st != MIG_OK) return st;
     mig::DevGeom* Gdev;
     int dev;
@@ -398,7 +400,8 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
     const size_t jb = al(chunk_jobs_cap * 16), eb = T.jobs_ext ? al(chunk_jobs_cap * 16) : 0,
                  ob = al((chunk_traces + 1) * 8), esb = al(chunk_jobs_cap * sizeof(mig_job_estimate)),
                  rb = al(chunk_traces * n_policies * sizeof(mig_trace_result));
-    const size_t per = jb + eb + ob + esb + rb + kCounterBytes;
+    const size_t ab = T.arrival ? al(chunk_jobs_cap * 4) : 0;  // arrival ticks (R40)
+    const size_t per = jb + eb + ob + esb + rb + ab + kCounterBytes;
     cudaStream_t ss[2];
     uint8_t* buf[2] = {nullptr, nullptr};
     std::vector<mig_policy_totals> host_tot(n_chunks * n_policies);
@@ -429,12 +432,15 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         mig_job_estimate* d_est = reinterpret_cast<mig_job_estimate*>(b + jb + eb + ob);
         mig_trace_result* d_out = reinterpret_cast<mig_trace_result*>(b + jb + eb + ob + esb);
         mig_policy_totals* d_tot = d_tot_all + c * n_policies;
-        unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(b + jb + eb + ob + esb + rb);
+        uint32_t* d_arr = reinterpret_cast<uint32_t*>(b + jb + eb + ob + esb + rb);
+        unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(b + jb + eb + ob + esb + rb + ab);
         e = cudaMemcpyAsync(d_jobs, (const uint8_t*)T.jobs + jlo * 16, nj * 16, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess && T.jobs_ext)
             e = cudaMemcpyAsync(d_ext, (const uint8_t*)T.jobs_ext + jlo * 16, nj * 16, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(d_off, off + t0, (nt + 1) * 8, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && T.arrival)
+            e = cudaMemcpyAsync(d_arr, T.arrival + jlo, nj * 4, cudaMemcpyHostToDevice, s);
         uint8_t* d_smp = nullptr;
         uint64_t* d_soff = nullptr;
         if (e == cudaSuccess && T.samples) {  // recorded samples of this chunk's jobs (stream-ordered scratch)
@@ -461,6 +467,7 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         ct.n_jobs = nj;
         ct.samples = d_smp;
         ct.sample_off = d_soff;
+        ct.arrival = T.arrival ? d_arr : nullptr;
         st = simulate_device(g, Gdev, dev, ct, policies, n_policies, nullptr, d_est, d_out, d_tot, d_cnt, s);
         if (d_smp) cudaFreeAsync(d_smp, s);
         if (d_soff) cudaFreeAsync(d_soff, s);

@@ -1018,8 +1018,8 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
         if (pc) cudaFreeAsync(pc, stream);
         return e;
     }
-    for (uint32_t i = 0; i < n_pol; ++i)  // the group kernel has no contention model
-        if (pols[i].flags & MIG_PCIE_CONTENTION) return cudaErrorNotSupported;
+    for (uint32_t i = 0; i < n_pol; ++i)  // the group kernel has no contention model and no arrival streams
+        if ((pols[i].flags & MIG_PCIE_CONTENTION) || tr.arrival) return cudaErrorNotSupported;
     if (P.n_pol) {
         e = launch_variant<false>(Gdev, P, tr, sm_count, stream);
         if (e != cudaSuccess) return e;

@@ -49,6 +49,7 @@ struct LaneParams {
     const uint2* trans;                 // mig_geometry::trans, [state][n_q] (FUSION_FISSION)
     const uint2* a7;                    // mig_geometry::a7, [state][n_a7] (FUSION_FISSION)
     uint4* pc;                          // PCIe contention: per lane and start slot, 2 x uint4 of run state (R39)
+    const uint32_t* arr;                // arrival ticks aligned with jobs (R40), or NULL (batch)
     uint32_t n_q, n_a7;
     uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
     mig_policy pol;
@@ -120,7 +121,7 @@ __device__ __forceinline__ uint32_t lane_wave_ticks(const DevGeom& G, uint32_t t
     return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
 }
 
-template <int KIND, bool PC>
+template <int KIND, bool EXT>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) LaneShared S;
@@ -207,7 +208,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     // PCIe contention (R39): slot s run state at pcs[2s] = {W lo, W hi, tk, rs}, pcs[2s+1] = {D, mem, iters,
     // F | started << 8 | dynamic << 9}; c_eff = transferring runs since the last retime; tick_end = an end event
     // was applied at the current tick (a tick with only starts has no scheduler pass)
-    uint4* pcs = PC ? P.pc + (size_t)(blockIdx.x * kLaneThreads + tid) * 16u : nullptr;
+    // EXT instantiations: PCIe contention and / or arrival streams (runtime flags, uniform per launch)
+    const bool pcie = EXT && (pol.flags & MIG_PCIE_CONTENTION) != 0 && KIND != MIG_BASELINE;
+    const bool arr = EXT && P.arr != nullptr;
+    uint4* pcs = pcie ? P.pc + (size_t)(blockIdx.x * kLaneThreads + tid) * 16u : nullptr;
     uint32_t c_eff = 0;
     bool tick_end = false;
     uint32_t* jk = &S.jk[0][tid];
@@ -228,22 +232,43 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     // BASELINE only: the running job (one at a time on the whole GPU)
     uint32_t bjob = 0, bend = 0;
     bool bbusy = false, boom = false;
+    uint32_t na = 0, alast = 0;  // arrival streams (R40): next job to arrive, last arrival tick seen
 
     auto fetch_head = [&]() {  // queue = jobs[qh..n) ++ requeue FIFO
         if (qh < n) {
             hj = qh;
             hneed = kUnk;
-        } else if (KIND != MIG_BASELINE && rn) {
+        } else if ((KIND != MIG_BASELINE || EXT) && rn) {
             const uint32_t v = ring[rh];
             hj = v & 0x3FFu;
             hneed = v >> 10;
             if (hneed == 15u) hneed = kNoNeed;
+            else if (hneed == 14u) hneed = kUnk;  // an arrival (R40): tight fit at its first evaluation
         } else {
             hj = kNoJob;
             return;
         }
         hr = __ldg(P.jobs + j0 + hj);
         he = P.ext ? __ldg(P.ext + j0 + hj) : make_uint4(0, 0, 0, 0);
+    };
+    // Arrival streams (reading R40): jobs whose arrival tick is <= t join the queue tail in queue order (after the
+    // requeues of the tick's events); their tight fit is computed when they first reach the head.
+    auto admit = [&]() -> bool {
+        bool any = false;
+        while (na < n) {
+            const uint32_t a = __ldg(P.arr + j0 + na);
+            if (a > t) break;
+            if (a < alast) err |= (uint32_t)MIG_ERR_BAD_RECORD;  // arrival ticks must not decrease
+            alast = max(alast, a);
+            uint32_t pos = rh + rn;
+            if (pos >= P.ring_cap) pos -= P.ring_cap;
+            ring[pos] = (uint16_t)(na | (14u << 10));
+            ++rn;
+            ++na;
+            if (hj == kNoJob) fetch_head();
+            any = true;
+        }
+        return any;
     };
     auto init_unit = [&]() {
         const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
@@ -282,6 +307,13 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
         hh = (uint32_t)(kFnvOffset >> 32);
         bbusy = false;
         mode = 0;
+        if (KIND == MIG_BASELINE && EXT) prof4 = fp;  // the generic loop's whole-GPU "instance" at slot 0
+        if (arr) {  // R40: the queue starts with the jobs arriving at t = 0
+            qh = n;
+            na = alast = 0;
+            hj = kNoJob;
+            admit();
+        }
         fetch_head();
         if (KIND == MIG_SCHEME_A && hj != kNoJob) mode = 4;  // the grouping pass first
     };
@@ -330,7 +362,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             end = rs + T * ticks;
         }
         const uint32_t dur = end - rs;
-        if constexpr (PC) {  // R39: the run's end follows its progress; power, memory and waste at its end
+        if (EXT && pcie) {  // R39: the run's end follows its progress; power, memory and waste at its end
             const uint32_t it = ek == 1 ? fe : ek == 2 ? i_pre : T;
             const uint32_t mem =
                 dyn ? __ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) : phys;
@@ -422,7 +454,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     // the phases keep the warp converged (without them the compiler's reconvergence points are too coarse and the
     // divergent paths of an iteration ran one after another: 4.5 active lanes per instruction).
     while (__any_sync(FULL, active)) {
-        if constexpr (KIND == MIG_BASELINE) {
+        if constexpr (KIND == MIG_BASELINE && !EXT) {
             // ---- BASELINE: one job at a time on the whole GPU, queue order ----
             if (mode == 0) {
                 bool ev = false;
@@ -531,7 +563,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             __syncwarp();
             if (mode == 1) {  // the events of the next tick (R28), then dispatch again
                 if (!evm) {
-                    if constexpr (PC) pc_retime();
+                    if (EXT && pcie) pc_retime();
                     uint32_t e8[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) e8[k] = et[k * kLaneThreads];
@@ -542,10 +574,8 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         mode = 2;
                     } else {
                         t = tn;
-                        if constexpr (PC) {
-                            pc_advance(tn);  // the runs in progress reach tn at the rate in effect
-                            tick_end = false;
-                        }
+                        if (EXT && pcie) pc_advance(tn);  // the runs in progress reach tn at the rate in effect
+                        tick_end = false;
 #pragma unroll
                         for (int k = 0; k < 8; ++k) evm |= (e8[k] == tn ? 1u : 0u) << k;
                     }
@@ -564,7 +594,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     evm &= ~(1u << es);
                     const uint32_t job = v & 0xFFFFu, ek = v >> 16;
                     const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = G.pinfo[epr];
-                    const bool pc_start = PC && pc_event(es, ek, (si >> 4) & 0xFu);  // R39: a start, no record
+                    const bool pc_start = EXT && pcie && pc_event(es, ek, (si >> 4) & 0xFu);  // R39: start
                     if (!pc_start) {
                         const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
                         lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));
@@ -597,7 +627,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         BS &= ~(1u << es);
                         BM &= ~(((si >> 8) & 0xFFu) << es);
                     }
-                    if (!evm) mode = (PC && !tick_end) ? 1u : 0u;  // a tick with only starts has no pass
+                    if (!evm) mode = (pcie && !tick_end) ? 1u : 0u;  // a tick with only starts has no pass
                 }
             }
         } else {
@@ -615,6 +645,15 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                 if (need == kNoNeed) {  // no profile can ever hold the job: REJECT
                     lo = jsh | (K_REJECT << 12) | 0xFF0u;
                     kd = K_REJECT;
+                } else if (KIND == MIG_BASELINE) {  // one job at a time on the whole GPU
+                    if (BS) {
+                        kd = K_WAIT;
+                        lo = jsh | (K_WAIT << 12) | 0xF00u | (need << 4);
+                    } else {
+                        s = 0;
+                        pr = fp;
+                        kd = K_PLACE_BASELINE;
+                    }
                 } else if (KIND == MIG_STATIC) {  // smallest idle fitting layout slice, tie -> highest start (R11)
                     const uint32_t cand = S.scand[need];
                     uint32_t m = cand & ~BS, bk = 0;
@@ -714,23 +753,26 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
             // ---- EVT: apply one event (min end tick; ties COMPLETE < OOM < PREEMPT, then job id, R28) ----
             if (mode == 1) {
                 if (!evm) {
-                    if constexpr (PC) pc_retime();
+                    if (EXT && pcie) pc_retime();
                     uint32_t e8[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) e8[k] = et[k * kLaneThreads];
                     uint32_t tn = e8[0];
 #pragma unroll
                     for (int k = 1; k < 8; ++k) tn = min(tn, e8[k]);
+                    if (arr && na < n) tn = min(tn, __ldg(P.arr + j0 + na));  // the next arrival (R40)
                     if (tn == kNoEnd) {
                         mode = 2;
                     } else {
                         t = tn;
-                        if constexpr (PC) {
-                            pc_advance(tn);  // the runs in progress reach tn at the rate in effect
-                            tick_end = false;
-                        }
+                        if (EXT && pcie) pc_advance(tn);  // the runs in progress reach tn at the rate in effect
+                        tick_end = false;
 #pragma unroll
                         for (int k = 0; k < 8; ++k) evm |= (e8[k] == tn ? 1u : 0u) << k;
+                        if (!evm) {  // an arrival-only tick: admit, then one scheduler pass (R9, R40)
+                            admit();
+                            mode = 0;
+                        }
                     }
                 }
                 if (evm) {
@@ -751,11 +793,11 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                     evm &= ~(1u << es);
                     const uint32_t job = v & 0xFFFFu, ek = v >> 16;
                     const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = G.pinfo[epr];
-                    const bool pc_start = PC && pc_event(es, ek, (si >> 4) & 0xFu);  // R39: a start, no record
+                    const bool pc_start = EXT && pcie && pc_event(es, ek, (si >> 4) & 0xFu);  // R39: start
                     if (!pc_start) {
                         const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
                         lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7 / PREEMPT 8
-                        a_turn += ek == 0 ? t : 0u;
+                        a_turn += ek == 0 ? t - (arr ? __ldg(P.arr + j0 + job) : 0u) : 0u;  // completion - arrival
                         K2 += ek == 1 ? 1u << 16 : 0u;
                         K3 += ek == 2 ? 1u : 0u;
                         uint32_t req = 0;
@@ -787,7 +829,10 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
                         }
                         if (KIND == MIG_FUSION_FISSION) IPM |= 1ull << (8 * epr + es);  // the instance is idle
                     }
-                    if (!evm) mode = (PC && !tick_end) ? 1u : 0u;  // a tick with only starts has no pass
+                    if (!evm) {  // the tick is over: its arrivals join the queue (R40); a tick with only starts has no pass
+                        const bool arrived = arr && admit();
+                        mode = (pcie && !tick_end && !arrived) ? 1u : 0u;
+                    }
                 }
             }
         }
@@ -915,25 +960,31 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     P.a7 = reinterpret_cast<const uint2*>(a7);
     P.n_a7 = n_a7;
     P.pc = pc;
+    P.arr = tr.arrival;
     const dim3 grid((unsigned)blocks), block(kLaneThreads);
-    const bool con = (pol.flags & MIG_PCIE_CONTENTION) != 0;  // BASELINE runs one job at a time: never contended
+    const bool con = (pol.flags & MIG_PCIE_CONTENTION) != 0 && pol.kind != MIG_BASELINE;  // BASELINE: c <= 1
     if (con && !P.pc) return cudaErrorInvalidValue;
+    const bool ext = con || P.arr;  // the EXT instantiation: contention and / or arrival streams
     switch (pol.kind) {
-        case MIG_BASELINE: k_simulate_lane<MIG_BASELINE, false><<<grid, block, 0, stream>>>(Gdev, P); break;
+        case MIG_BASELINE:
+            if (ext) k_simulate_lane<MIG_BASELINE, true><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_BASELINE, false><<<grid, block, 0, stream>>>(Gdev, P);
+            break;
         case MIG_STATIC:
-            if (con) k_simulate_lane<MIG_STATIC, true><<<grid, block, 0, stream>>>(Gdev, P);
+            if (ext) k_simulate_lane<MIG_STATIC, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_STATIC, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_DYNAMIC:
-            if (con) k_simulate_lane<MIG_DYNAMIC, true><<<grid, block, 0, stream>>>(Gdev, P);
+            if (ext) k_simulate_lane<MIG_DYNAMIC, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_DYNAMIC, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_FUSION_FISSION:
-            if (con) k_simulate_lane<MIG_FUSION_FISSION, true><<<grid, block, 0, stream>>>(Gdev, P);
+            if (ext) k_simulate_lane<MIG_FUSION_FISSION, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_FUSION_FISSION, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_SCHEME_A:
-            if (con) k_simulate_lane<MIG_SCHEME_A, true><<<grid, block, 0, stream>>>(Gdev, P);
+            if (P.arr) return cudaErrorInvalidValue;  // Scheme A groups the whole queue at t = 0
+            if (ext) k_simulate_lane<MIG_SCHEME_A, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         default: return cudaErrorInvalidValue;

@@ -3,6 +3,8 @@ tables (Alg. 1 fcr by occupancy mask, Alg. 2 placement) agree with the oracle's 
 geometry validation names the offending field, and device calls fail loudly (no CPU fallback)."""
 import ctypes as C
 import json
+
+import numpy as np
 import os
 import re
 
@@ -138,3 +140,13 @@ def test_fusion_table_matches_literal_r8(name):
                 n_checked += 1
                 n_found += best is not None
     assert n_found > 0 and n_checked > 100
+
+
+def test_scheme_a_rejects_arrival_streams():
+    """Scheme A groups the whole queue at t = 0 (R38): with arrival ticks (R40) the call is an argument error."""
+    from tracegen import tracegen as tg
+
+    jobs, ext, off = tg.pack_traces([[tg.pack_job(4096, 4096, 1, 0, 10)]])
+    g = mig.mig_geometry_load("builtin:a100-40gb")
+    with pytest.raises(mig.MigError, match="INVALID_ARG"):
+        mig.mig_simulate_host(g, jobs, ext, off, [mig.policy(g, kind=4)], arrival=np.zeros(1, np.uint32))

@@ -422,3 +422,18 @@ def test_arrivals_spaced_beyond_durations_run_alone():
         r = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, ctx_mib=0, reconfig_ticks=0),
                          arrival=np.array(arr, np.uint32))[0, 0]
         assert r["makespan"] == arr[-1] + durs[-1] and r["turnaround_sum"] == sum(durs) and r["waits"] == 0
+
+
+def test_arrival_rejected_after_last_completion_extends_makespan():
+    """R40: makespan is the last tick with an end or an arrival. A job no slice can hold, arriving after the last
+    completion, is rejected at its arrival tick, which ends the run: A (10 ticks) at 0, B (50 GB, too large for
+    A100-40GB) at 500 -> makespan 500, one REJECT at 500."""
+    A = tg.pack_job(4096, 4096, 1, 0, 10)
+    B = tg.pack_job(51200, 51200, 1, 0, 10)
+    jobs, ext, off = tg.pack_traces([[A, B]])
+    g = orc.Geometry(geom_path("a100-40gb"))
+    for kind in (0, 1, 2, 3):
+        r, recs = orc.simulate(g, jobs, ext, off, orc.policy(kind=kind, ctx_mib=0, reconfig_ticks=0), records=True,
+                               arrival=np.array([0, 500], np.uint32))
+        assert r[0, 0]["makespan"] == 500 and r[0, 0]["rejected"] == 1 and r[0, 0]["completed"] == 1
+        assert recs[-1]["tick"] == 500 and recs[-1]["kind"] == "REJECT"

@@ -26,18 +26,28 @@ ESTIMATE_FIELDS = ["req0_mib", "pred_mib", "conv_iter", "n_levels", "fe", "phi",
                    "mem_conv", "mem_T"]
 
 
-def run_pair(geo, jobs, ext, off, specs, seed=0, common=None, max_jobs=None):
+def run_pair(geo, jobs, ext, off, specs, seed=0, common=None, max_jobs=None, arrival=None):
     common = common or {}
     g = mig.mig_geometry_load(f"builtin:{geo}")
     og = orc.Geometry(geom_path(geo))
     pols = [mig.policy(g, **s, **common) for s in specs]
     opols = [orc.policy(**s, **common) for s in specs]
-    tr = mig.traces_from_numpy(jobs, ext, off, seed=seed, max_jobs=max_jobs)
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=seed, max_jobs=max_jobs, arrival=arrival)
     res, tot = mig.mig_simulate(g, tr, pols)
     torch.cuda.synchronize()
     got = mig.results_numpy(res, len(pols))
-    want = orc.simulate(og, jobs, ext, off, opols, seed=seed)
+    want = orc.simulate(og, jobs, ext, off, opols, seed=seed, arrival=arrival)
     return got, want, mig.totals_numpy(tot)
+
+
+def random_arrivals(rng, off, spread):
+    """Non-decreasing arrival ticks per trace (R40): sorted uniform draws in [0, spread), some traces all at 0."""
+    arr = np.zeros(int(off[-1]), np.uint32)
+    for t in range(len(off) - 1):
+        a, b = int(off[t]), int(off[t + 1])
+        if b > a and rng.random() < 0.8:
+            arr[a:b] = np.sort(rng.integers(0, spread, b - a))
+    return arr
 
 
 def assert_same(got, want):
@@ -295,3 +305,34 @@ def test_pcie_contention_generated_config5():
                          [orc.policy(**{**sp, "flags": sp["flags"] & ~16}) for sp in specs], seed=tg.seed_of(5))
     assert (plain["makespan"][:, 3] < want["makespan"][:, 3]).mean() > 0.5  # contention slows FF down
     assert np.array_equal(plain["makespan"][:, 0], want["makespan"][:, 0])  # one run at a time: never contended
+
+
+@pytest.mark.parametrize("geo", ["a30-24gb", "a100-40gb", "h100-80gb"])
+def test_arrival_streams_parity(geo):
+    """Arrival streams (R40): random non-decreasing arrival ticks on random ragged traces, every Scheme B policy
+    and BASELINE, with and without PCIe contention and creation delays; per-trace results and totals."""
+    spec = json.load(open(geom_path(geo)))
+    rng = np.random.default_rng(31)
+    jobs, ext, off = random_tiny_traces(rng, spec, 600, 30, xfer=True)
+    arrival = random_arrivals(rng, off, 3000)
+    specs = [dict(kind=k) for k in range(4)] + [dict(kind=3, flags=1), dict(kind=2, flags=16),
+                                                dict(kind=3, flags=17), dict(kind=0, flags=16)]
+    for common in [dict(ctx_mib=0, reconfig_ticks=0), dict(ctx_mib=512, reconfig_ticks=500)]:
+        got, want, tot = run_pair(geo, jobs, ext, off, specs, seed=37, common=common, arrival=arrival)
+        assert_same(got, want)
+        check_totals(got, tot)
+
+
+def test_arrival_streams_host_pipeline_and_config2(monkeypatch):
+    """Config-2 traces with arrival streams through mig_simulate_host (chunked H2D of the arrival ticks) equal the
+    device call and the oracle."""
+    monkeypatch.setenv("MIG_HOST_CHUNK_JOBS", "20000")
+    jobs, ext, off = tg.generate_host(2, 400)
+    arrival = random_arrivals(np.random.default_rng(41), off, 200000)
+    specs = [dict(kind=3), dict(kind=0)]
+    got, want, tot = run_pair("a100-40gb", jobs, ext, off, specs, seed=tg.seed_of(2), arrival=arrival)
+    assert_same(got, want)
+    g = mig.mig_geometry_load("builtin:a100-40gb")
+    pols = [mig.policy(g, **sp) for sp in specs]
+    hres, htot = mig.mig_simulate_host(g, jobs, ext, off, pols, seed=tg.seed_of(2), arrival=arrival)
+    assert_same(hres, want)
