@@ -115,7 +115,6 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     uint32_t fe[5] = {kNever, kNever, kNever, kNever, kNever};
     uint32_t mfe[5] = {0u, 0u, 0u, 0u, 0u};  // physical MiB summed over iterations 1..fe[l]
     uint32_t Smem = 0, mconv = 0;            // running sum (memory integral)
-    auto lvl_thr = [&](uint32_t l) -> int64_t { return (int64_t)G.level_mem[l] - ws_ctx; };  // phys > L <=> floor > thr
     auto fe_set = [&](uint32_t l, uint32_t v, uint32_t m) {
 #pragma unroll
         for (int k = 0; k < kMaxLevels; ++k)
@@ -131,6 +130,11 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     double phi = 0.0, a = 0.0, sig = 0.0;
     bool done_pred = T < P.min_n;
     bool bad = false;
+    // generated series whose range bounds already satisfy the predictor's input limits skip the per-sample checks
+    // (y < 2^18, 0 < q < 2^26): y <= b + slope*T/256 + the largest Irwin-Hall draw + 1, q grows from q0 by qs
+    const uint64_t y_hi = (uint64_t)b + (((uint64_t)slope * T) >> 8) +
+                          (((uint64_t)131070u * ((sigma_n & 0xFFFFu) * 7094u)) >> 28) + 2u;
+    const bool check = rec_samples || y_hi >= (1u << 18) || q0 == 0 || (uint64_t)q0 + (uint64_t)qs * T >= (1u << 26);
     for (uint32_t base = 0; base < T; base += 32) {  // to T: the memory integral needs every iteration
         const uint32_t n = base + lane + 1;
         const bool valid = n <= T;
@@ -143,19 +147,18 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
             } else {
                 tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
             }
-            bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
+            if (check) bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
         }
         // physical MiB of iteration n and its running sum (R22: requested / inverse reuse, + ws + ctx)
-        const uint32_t phys = valid ? (uint32_t)((q_unit ? (uint64_t)y : ((uint64_t)y * 65536ull) / q) + ws_ctx) : 0u;
+        const uint64_t phys64 = valid ? (q_unit ? (uint64_t)y : ((uint64_t)y * 65536ull) / q) + ws_ctx : 0ull;
+        const uint32_t phys = (uint32_t)phys64;
         // running sum of the memory integral: one reduction per chunk, prefixes only where needed
         auto prefix = [&](uint32_t m) { return Smem + __reduce_add_sync(FULL, lane <= m ? phys : 0u); };
         // first-exceed iteration of every memory level (R12): phys(i) = floor(y*65536/q) + ws + ctx > L.
         // Levels ascend, so fe[l] <= fe[l+1]: only the lowest level not yet crossed needs a ballot per chunk
         // (more when one chunk crosses several levels).
         while (lnext < G.n_levels) {
-            const int64_t th = lvl_thr(lnext);
-            const bool over = valid && (th < 0 || (q_unit ? (int64_t)y > th
-                                                           : (uint64_t)y * 65536ull >= (uint64_t)(th + 1) * q));
+            const bool over = valid && phys64 > G.level_mem[lnext];
             const uint32_t m = __ballot_sync(FULL, over);
             if (!m) break;
             fe_set(lnext, base + __ffs(m), prefix((uint32_t)__ffs(m) - 1u));
@@ -168,11 +171,12 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
         // exact integer moments at n = base + lane + 1 (inclusive warp scans + carried totals)
         const int64_t yi = y, qi = q, ni = n;
-        const int64_t sy = Sy + warp_scan_i64(yi, lane);
+        const int64_t sy = Sy + (int64_t)warp_scan_u32(y, lane);  // sum y <= 4096 * 2^18 fits 32 bits
         const int64_t sty = Sty + warp_scan_i64(valid ? ni * yi : 0, lane);
         const int64_t syy = Syy + warp_scan_i64(yi * yi, lane);
-        const int64_t sq = Sq + warp_scan_i64(qi, lane);
-        const int64_t stq = Stq + warp_scan_i64(valid ? ni * qi : 0, lane);
+        // constant inverse reuse: its fit is not needed (V = 1), so its moments are not formed
+        const int64_t sq = q_unit ? 0 : Sq + warp_scan_i64(qi, lane);
+        const int64_t stq = q_unit ? 0 : Stq + warp_scan_i64(valid ? ni * qi : 0, lane);
         // EWMA of the inverse reuse ratio (R36): L_1 = q_1, L_i = L_{i-1} + ((q_i - L_{i-1}) >> 3); a sequential
         // recurrence, evaluated over the chunk's lanes in order (optional variant, never on the default path).
         int64_t myL = 0;
