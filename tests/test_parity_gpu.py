@@ -194,10 +194,12 @@ def test_device_generator_equals_host(cfg):
     assert np.array_equal(do.cpu().numpy().view(np.uint64), ho)
 
 
-@pytest.mark.parametrize("cfg,n_full,n_sample", [(2, 1_000_000, 1500), (3, 1_000_000, 1500), (4, 2_000_000, 4000)])
+@pytest.mark.parametrize("cfg,n_full,n_sample", [(2, 1_000_000, 1500), (3, 1_000_000, 1500), (4, 2_000_000, 4000),
+                                               (5, 4_000_000, 800)])
 def test_full_size_sampled_parity(cfg, n_full, n_sample):
-    """BASELINE.json sizes (C4 at 1/5 to bound memory) in the launch configuration bench.py uses: device-generated
-    traces, all policies in one call; sampled traces are regenerated on the host and run through the oracle."""
+    """BASELINE.json sizes (C4 at 1/5, C5 at 1/3 of its 8-GPU shard, to bound memory) in the launch configuration
+    bench.py uses: device-generated traces, all policies in one call; sampled traces are regenerated on the host and
+    run through the oracle."""
     geo = tg.CONFIG_GEOMETRY[cfg]
     g = mig.mig_geometry_load(f"builtin:{geo}")
     og = orc.Geometry(geom_path(geo))
