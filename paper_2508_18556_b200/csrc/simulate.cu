@@ -941,7 +941,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
-                                 uint4* pc, cudaStream_t stream);
+                                 uint4* pc, int sm_count, cudaStream_t stream);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
 // (8 or 32 lanes per trace).
@@ -1010,7 +1010,8 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
             e = (cudaError_t)mig_timed(kNames[pols[i].kind], stream, [&](uint32_t* nl) {
                 if (nl) *nl = 1;
                 return (int)launch_simulate_lane(Gdev, tr, pols[i], i, n_pol, est, out, totals, counter + 2 + i,
-                                                 est_err, ring, blocks, trans, n_q, a7, n_a7, pc, stream);
+                                                 est_err, ring, blocks, trans, n_q, a7, n_a7, pc, sm_count,
+                                                 stream);
             });
             ++*launches;
         }

@@ -31,6 +31,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "device_common.cuh"
 
 namespace mig {
@@ -56,7 +58,13 @@ struct LaneParams {
 };
 
 constexpr int kLaneThreads = 128;
-constexpr int kLaneMinBlocks = 6;
+// Resident CTAs per SM (launch bounds) and where the u64 accumulators live: the Scheme B kernels (STATIC, DYNAMIC,
+// FUSION_FISSION) keep them in shared memory and run 7 CTAs; BASELINE (record streaming, L1-bound) and Scheme A
+// keep them in registers and run 6. Measured A/B, DESIGN.md §6.
+template <int KIND>
+__host__ __device__ constexpr bool lane_acc_smem() { return KIND != MIG_BASELINE && KIND != MIG_SCHEME_A; }
+template <int KIND>
+__host__ __device__ constexpr int lane_min_blocks() { return lane_acc_smem<KIND>() ? 7 : 6; }
 constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
 constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
 
@@ -122,7 +130,7 @@ __device__ __forceinline__ uint32_t lane_wave_ticks(const DevGeom& G, uint32_t t
 }
 
 template <int KIND, bool EXT>
-__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
+__global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) LaneShared S;
     const uint32_t tid = threadIdx.x;
@@ -226,7 +234,14 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
     uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0, sid = 0;
     uint64_t IPM = 0;  // FF: idle instances by profile, byte p bit s = an idle instance of profile p starts at s
     uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
-    uint64_t a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
+    // u64 accumulators: turnaround, busy slice-ticks, MiB-ticks, wasted ticks (lane_acc_smem)
+    constexpr bool kAccSmem = lane_acc_smem<KIND>();
+    __shared__ unsigned long long s_acc[kAccSmem ? 4 : 1][kLaneThreads];
+    unsigned long long r_acc0 = 0, r_acc1 = 0, r_acc2 = 0, r_acc3 = 0;
+    unsigned long long& a_turn = kAccSmem ? s_acc[0][tid] : r_acc0;
+    unsigned long long& a_busy = kAccSmem ? s_acc[kAccSmem ? 1 : 0][tid] : r_acc1;
+    unsigned long long& a_mem = kAccSmem ? s_acc[kAccSmem ? 2 : 0][tid] : r_acc2;
+    unsigned long long& a_waste = kAccSmem ? s_acc[kAccSmem ? 3 : 0][tid] : r_acc3;
     uint32_t hj = kNoJob, hneed = kUnk;  // head job and its tight fit (kUnk: not yet computed)
     uint4 hr = make_uint4(0, 0, 0, 0), he = make_uint4(0, 0, 0, 0);
     // BASELINE only: the running job (one at a time on the whole GPU)
@@ -918,14 +933,26 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks)
 }
 
 // Grid: resident CTAs per SM x SMs (persistent; units are taken from the counter), capped by the unit count.
-uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count) {
+template <int KIND>
+static int lane_per_sm() {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate_lane<MIG_FUSION_FISSION, false>, kLaneThreads, 0);
-    if (per_sm < 1) per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate_lane<KIND, false>, kLaneThreads, 0);
+    return per_sm < 1 ? 1 : per_sm;
+}
+
+// Grid: resident CTAs per SM x SMs (persistent; units are taken from the counter), capped by the unit count.
+static uint64_t lane_blocks(int per_sm, uint64_t n_traces, int sm_count) {
     uint64_t blocks = (uint64_t)per_sm * sm_count;
     const uint64_t want = (n_traces + kLaneThreads - 1) / kLaneThreads;
     if (want < blocks) blocks = want;
     return blocks < 1 ? 1 : blocks;
+}
+
+// The largest grid of any kind (sizes the per-lane scratch shared by the launches of one call).
+uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count) {
+    const int per_sm = std::max(std::max(lane_per_sm<MIG_BASELINE>(), lane_per_sm<MIG_FUSION_FISSION>()),
+                                lane_per_sm<MIG_SCHEME_A>());
+    return lane_blocks(per_sm, n_traces, sm_count);
 }
 
 uint32_t simulate_lane_threads() { return kLaneThreads; }
@@ -936,7 +963,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
-                                 uint4* pc, cudaStream_t stream) {
+                                 uint4* pc, int sm_count, cudaStream_t stream) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -961,7 +988,11 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     P.n_a7 = n_a7;
     P.pc = pc;
     P.arr = tr.arrival;
-    const dim3 grid((unsigned)blocks), block(kLaneThreads);
+    const int per_sm = pol.kind == MIG_BASELINE   ? lane_per_sm<MIG_BASELINE>()
+                       : pol.kind == MIG_SCHEME_A ? lane_per_sm<MIG_SCHEME_A>()
+                                                  : lane_per_sm<MIG_FUSION_FISSION>();
+    const dim3 grid((unsigned)std::min<uint64_t>(blocks, lane_blocks(per_sm, tr.n_traces, sm_count))),
+        block(kLaneThreads);
     const bool con = (pol.flags & MIG_PCIE_CONTENTION) != 0 && pol.kind != MIG_BASELINE;  // BASELINE: c <= 1
     if (con && !P.pc) return cudaErrorInvalidValue;
     const bool ext = con || P.arr;  // the EXT instantiation: contention and / or arrival streams
