@@ -338,3 +338,31 @@ def test_arrival_streams_host_pipeline_and_config2(monkeypatch):
     pols = [mig.policy(g, **sp) for sp in specs]
     hres, htot = mig.mig_simulate_host(g, jobs, ext, off, pols, seed=tg.seed_of(2), arrival=arrival)
     assert_same(hres, want)
+
+
+def test_nine_profile_geometry_uses_the_group_kernel(tmp_path):
+    """A geometry with more than 8 profiles (the lane kernel packs per-profile idle masks in 64 bits) runs on the
+    group kernel: same parity bar, random ragged traces, Scheme B policies."""
+    prof = []
+    for name, c, ln, st in [("1g.a", 1, 1, list(range(7))), ("1g.b", 1, 2, [0, 2, 4, 6]), ("2g.b", 2, 2, [0, 2, 4]),
+                            ("1g.c", 1, 4, [0, 4]), ("2g.c", 2, 4, [0, 4]), ("3g.c", 3, 4, [0, 4]),
+                            ("4g.c", 4, 4, [0]), ("5g.d", 5, 8, [0]), ("7g.d", 7, 8, [0])]:
+        prof.append({"name": name, "compute_slices": c, "memory_slots": ln, "starts": st})
+    spec = {"gpu_name": "NINE", "total_memory_slots": 8, "slot_mib": 5120, "total_compute_slices": 7,
+            "sms_per_slice": 14, "warps_per_sm": 64, "idle_w": 30, "w_per_slice": 25, "profiles": prof}
+    path = tmp_path / "nine.json"
+    path.write_text(json.dumps(spec))
+    g = mig.mig_geometry_load(str(path))
+    assert g.info.n_profiles == 9
+    og = orc.Geometry(str(path))
+    rng = np.random.default_rng(43)
+    jobs, ext, off = random_tiny_traces(rng, spec, 300, 25)
+    specs = [dict(kind=0), dict(kind=2), dict(kind=3), dict(kind=3, flags=1)]
+    pols = [mig.policy(g, **s, ctx_mib=256, reconfig_ticks=100) for s in specs]
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=5)
+    res, tot = mig.mig_simulate(g, tr, pols)
+    torch.cuda.synchronize()
+    got = mig.results_numpy(res, len(pols))
+    want = orc.simulate(og, jobs, ext, off, [orc.policy(**s, ctx_mib=256, reconfig_ticks=100) for s in specs], seed=5)
+    assert_same(got, want)
+    check_totals(got, mig.totals_numpy(tot))
