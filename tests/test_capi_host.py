@@ -150,3 +150,32 @@ def test_scheme_a_rejects_arrival_streams():
     g = mig.mig_geometry_load("builtin:a100-40gb")
     with pytest.raises(mig.MigError, match="INVALID_ARG"):
         mig.mig_simulate_host(g, jobs, ext, off, [mig.policy(g, kind=4)], arrival=np.zeros(1, np.uint32))
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+
+    exe = tmp_path / "c_api_example"
+    lib_dir = os.path.dirname(mig.LIB_PATH)
+    subprocess.run(["gcc", "-std=c11", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "c_api_example.c"), "-L", lib_dir, "-lmig",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+
+
+def test_c_example_builds_against_the_header_and_library(tmp_path):
+    """examples/c_api_example.c compiles with -Wall -Werror against include/mig.h and links libmig.so; without a
+    GPU it fails loudly (MIG_E_CUDA, exit 2), never silently computing on the CPU."""
+    r = _build_c_example(tmp_path)
+    assert (r.returncode == 0 and "FUSION_FISSION" in r.stdout) or (r.returncode == 2 and "no CUDA device" in r.stderr)
+
+
+@pytest.mark.gpu
+def test_c_example_reproduces_example_w(tmp_path):
+    """The plain-C caller gets example W's hand-derived results (tests/golden/config1_w.json)."""
+    r = _build_c_example(tmp_path)
+    assert r.returncode == 0, r.stderr
+    got = {ln.split()[0]: ln.split() for ln in r.stdout.strip().splitlines()}
+    assert got["BASELINE"][2] == "450" and got["STATIC"][2] == "210"
+    assert got["DYNAMIC"][2] == "220" and got["FUSION_FISSION"][2] == "220"
+    assert got["FUSION_FISSION"][12] == "27100" and got["BASELINE"][12] == "58500"
