@@ -92,7 +92,19 @@ def oracle_rate(cfg, pols, cores, seconds, first_trace=0, pool=None, max_traces=
     ntr = sum(o[2] for o in outs)
     sample = (f"{ntr} traces of config {cfg} (ids {first_trace + 64}..{first_trace + 64 + ntr - 1}) x "
               f"{len(pols)} policies, {cores} processes x {per_core} traces")
+    oracle_rate.single = statistics.mean(o[1] / o[0] for o in outs)  # one process (one core) alone
     return decs / wall, ntr / wall, sample, wall
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -183,7 +195,7 @@ def run_reference(args):
         "config": {"workload": wl["desc"], "policies": [POLICY_NAMES[p] for p in wl["policies"]],
                    "parallelism": f"{cores} oracle processes"},
         "cpu_baseline": {"value": value, "unit": "decisions/s", "cores": cores, "kind": "oracle",
-                         "sample": f"per step: {sample}"},
+                         "sample": f"per step: {sample}", "cpu_model": cpu_model(), "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -210,7 +222,8 @@ def run_mine(args):
         cores = min(os.cpu_count() or 1, args.cpu_cores)
         r, trs, sample, wall = oracle_rate(cfg, wl["policies"], cores, args.cpu_seconds, max_traces=n_per)
         cpu = {"value": r, "unit": "decisions/s", "cores": cores, "kind": "oracle", "sample": sample,
-               "traces_per_s": trs, "wall_s": round(wall, 2)}
+               "traces_per_s": trs, "wall_s": round(wall, 2), "per_process_decisions_per_s": oracle_rate.single,
+               "cpu_model": cpu_model(), "host_cpus": os.cpu_count()}
         log(f"cpu oracle baseline: {r:.3e} decisions/s on {cores} cores")
 
     local = local % max(1, torch.cuda.device_count())  # --share-gpu testing: several ranks on one device
@@ -233,6 +246,9 @@ def run_mine(args):
     t_id0, _ = shard_range(rank, world, n_per_rank=n_per)
     jobs, ext, off = tg.generate_device(cfg, n_per, trace_id0=t_id0, seed=seed, device=dev)
     J = tg.jobs_per_trace(cfg)
+    # samples the estimator scans per step (a3 runs every DYNAMIC job to its declared T): iteration-steps (§8(d))
+    zf = jobs[:, 2].to(torch.int64)
+    dyn_samples = int(((zf & 0xFFFF) * (((zf >> 16) & 0xFF) == 2).to(torch.int64)).sum().item())
     tr = mig.Traces(jobs, ext, off, n_per, seed=seed, trace_id0=t_id0, max_jobs=J)
     res = torch.empty((n_per * n_pol, 96), dtype=torch.uint8, device=dev)
     tot = torch.empty((n_pol, 192), dtype=torch.uint8, device=dev)
@@ -343,7 +359,11 @@ def run_mine(args):
     # launching stream through mig_timing_enable): algorithmic lane-ops of that policy's decisions and events
     # (DESIGN.md ops model) / its average launch duration, against the issue peak.
     launch_ms = {k: v[0] / args.steps for k, v in ktimes.items() if k.startswith("sim_")}
-    dom = max(launch_ms, key=launch_ms.get) if launch_ms else "k_simulate"
+    # policies alternate between the caller's stream and a side stream (launch_simulate): a side launch ("~")
+    # queues for the SMs of the launch before it, so its event span is not its duration; the dominant launch is
+    # taken among the caller-stream launches, whose spans are
+    own = {k: v for k, v in launch_ms.items() if not k.endswith("~")}
+    dom = max(own, key=own.get) if own else "k_simulate"
     dom_ms = launch_ms.get(dom, sim_ms)
     kind_of = {"sim_baseline": 0, "sim_static": 1, "sim_dynamic": 2, "sim_ff": 3}
     dom_pols = [i for i, (k, f) in enumerate(wl["policies"]) if k == kind_of.get(dom, -1)] or list(range(n_pol))
@@ -353,6 +373,12 @@ def run_mine(args):
     ops_dom = (OPS_PER_DECISION * dom_dec + OPS_PER_EVENT * dom_ev +
                OPS_PER_JOB_STAGE * jobs_step * len(dom_pols)) / world / dom_launches
     achieved = ops_dom / (dom_ms / dom_launches * 1e-3)
+    ops_desc = f"{OPS_PER_DECISION}/decision + {OPS_PER_EVENT}/event + {OPS_PER_JOB_STAGE}/job/policy (DESIGN.md)"
+    kname = f"k_simulate_lane ({dom})"
+    if est_ms > dom_ms and dyn_samples:  # configs 3-4: the estimator is the dominant kernel (one launch per step)
+        dom, dom_ms, kname, dom_launches = "k_estimate", est_ms, "k_estimate", 1
+        achieved = OPS_PER_DYN_ITER * dyn_samples / (est_ms * 1e-3)
+        ops_desc = f"{OPS_PER_DYN_ITER}/DYNAMIC-job sample scanned (fits not counted; DESIGN.md)"
     traffic, ncu = None, {}
     prof = os.path.join(ROOT, "profiles", f"ncu_config{cfg}.json")
     if os.path.exists(prof) and n_per == wl["traces"]:
@@ -372,11 +398,10 @@ def run_mine(args):
         "kernels": {"k_estimate_ms": est_ms, "k_simulate_ms": sim_ms,
                     "k_simulate_share": sim_ms / ms_per_step, "launch_ms": launch_ms,
                     "dominant_share": dom_ms / ms_per_step},
-        "roofline": {"bound": "alu", "kernel": f"k_simulate_lane ({dom})", "achieved": achieved, "peak": alu_peak,
+        "roofline": {"bound": "alu", "kernel": kname, "achieved": achieved, "peak": alu_peak,
                      "unit": "int lane-ops/s", "frac": achieved / alu_peak, "traffic": traffic,
                      "peak_source": f"148 SMs x 4 SMSP x 32 lanes x {f_mhz:.0f} MHz ({peak_src} sm_max_mhz)",
-                     "ops_model": f"{OPS_PER_DECISION}/decision + {OPS_PER_EVENT}/event + "
-                                  f"{OPS_PER_JOB_STAGE}/job/policy (DESIGN.md)",
+                     "ops_model": ops_desc,
                      "ncu_issue_slot_util": ncu.get(f"{dom}_issue_slot_util"),
                      "ncu_active_lanes_per_instr": ncu.get(f"{dom}_active_lanes_per_instr"),
                      "ncu_source": ncu.get("source")},
@@ -388,6 +413,9 @@ def run_mine(args):
         "clocks": clk,
     }
     line["hbm"]["achieved_gbs"] = line["hbm"]["algorithmic_bytes_per_launch"] / (dom_ms / dom_launches * 1e-3) / 1e9
+    if dyn_samples:  # §8(d): configs 3-4 are dominated by predictor steps
+        line["iteration_steps_per_s"] = dyn_samples * world / (ms_per_step * 1e-3)
+        line["config"]["dynamic_samples_per_step"] = dyn_samples
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -111,10 +111,10 @@ def mig_timing_enable(on: bool = True) -> None:
 
 def mig_timing_query() -> dict:
     """{kernel group name: (total ms, launches)} since the last enable/query (synchronises the events)."""
-    buf = (mig_kernel_time * 8)()
+    buf = (mig_kernel_time * 32)()
     n = C.c_uint32(0)
-    _check(_lib.mig_timing_query(buf, 8, C.byref(n)))
-    return {buf[i].name.decode(): (buf[i].ms, int(buf[i].launches)) for i in range(min(n.value, 8))}
+    _check(_lib.mig_timing_query(buf, 32, C.byref(n)))
+    return {buf[i].name.decode(): (buf[i].ms, int(buf[i].launches)) for i in range(min(n.value, 32))}
 
 
 class Geometry:

@@ -15,8 +15,8 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint32_t* trans,
-                            uint32_t n_q, const uint32_t* a7, uint32_t n_a7);
+                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint16_t* sid,
+                            const uint32_t* a7, uint32_t n_a7);
 }  // namespace mig
 
 namespace {
@@ -106,17 +106,17 @@ mig_status device_geometry(const mig_geometry* gc, mig::DevGeom** out, int* dev_
         }
         g->dev[dev] = p;
     }
-    if (!g->trans_dev[dev] && !g->trans.empty()) {
-        uint32_t* t = nullptr;
-        const size_t bytes = g->trans.size() * sizeof(uint32_t);
+    if (!g->sid_dev[dev] && !g->sid16.empty()) {
+        uint16_t* t = nullptr;
+        const size_t bytes = g->sid16.size() * sizeof(uint16_t);
         e = cudaMalloc(&t, bytes);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(transitions)");
-        e = cudaMemcpy(t, g->trans.data(), bytes, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(state ids)");
+        e = cudaMemcpy(t, g->sid16.data(), bytes, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
             cudaFree(t);
-            return cuda_fail(e, "cudaMemcpy(transitions)");
+            return cuda_fail(e, "cudaMemcpy(state ids)");
         }
-        g->trans_dev[dev] = t;
+        g->sid_dev[dev] = t;
     }
     if (!g->a7_dev[dev] && !g->a7.empty()) {
         uint32_t* t = nullptr;
@@ -201,8 +201,8 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
     uint32_t nl = 0;
     e = timed("k_simulate", s, [&](uint32_t* tl) {
         cudaError_t e2 = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1,
-                                              sm_count_of(dev), s, &nl, g->dg.n_prof, g->trans_dev[dev],
-                                              g->n_q, g->a7_dev[dev], g->n_a7);
+                                              sm_count_of(dev), s, &nl, g->dg.n_prof, g->sid_dev[dev],
+                                              g->a7_dev[dev], g->n_a7);
         if (tl) *tl = nl;
         return e2;
     });
@@ -228,7 +228,7 @@ mig_geometry::~mig_geometry() {
             cudaGetDevice(&cur);
             cudaSetDevice(d);
             cudaFree(dev[d]);
-            if (trans_dev[d]) cudaFree(trans_dev[d]);
+            if (sid_dev[d]) cudaFree(sid_dev[d]);
             if (a7_dev[d]) cudaFree(a7_dev[d]);
             cudaSetDevice(cur);
         }

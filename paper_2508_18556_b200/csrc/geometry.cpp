@@ -94,7 +94,7 @@ void build_transitions(mig_geometry* g) {
             tab.push_back(((uint32_t)d.fcr[nocc] << 16) | ((15u - nd) << 8) | lo);
             tab.push_back(rm | ((uint32_t)id[key] << 8));
         }
-        if (keys.size() >= (1u << 24)) return;
+        if (keys.size() >= 0xFFFFu) return;  // u16 state ids (the key space is 2^16)
     }
     // fusion / fission answers per (state, profile, candidate mask)
     uint32_t na7 = 0;
@@ -122,6 +122,9 @@ void build_transitions(mig_geometry* g) {
             qb += np;
         }
     }
+    g->sid16.assign(id.size(), 0xFFFFu);
+    for (size_t k = 0; k < id.size(); ++k)
+        if (id[k] >= 0) g->sid16[k] = (uint16_t)id[k];
     g->trans.swap(tab);
     g->a7.swap(a7);
     g->trans_id.swap(id);

@@ -51,15 +51,16 @@ struct mig_geometry {
     // when nothing overlaps; fusion / fission R8 otherwise). Used by the lane kernel's FUSION_FISSION path.
     std::vector<uint32_t> trans;       // [n_trans_states][n_q][2]
     std::vector<int32_t> trans_id;     // state id by occ | start mask << 8 (-1 = not a reachable state)
+    std::vector<uint16_t> sid16;       // the same as u16 (0xFFFF = unreachable): the device copy the lane kernel reads
     uint32_t n_trans_states = 0, n_q = 0;
     // Fusion / fission answers (R8) by (state, profile p, candidate mask c over p's placements): the entry of the
     // best placement k in c that overlaps an instance ({0, 0} if none). Row = n_a7 entries, profile p's block
     // starts at sum over earlier profiles of 2^n_place.
     std::vector<uint32_t> a7;          // [n_trans_states][n_a7][2]
     uint32_t n_a7 = 0;
-    std::mutex mu;                     // guards dev[], trans_dev[], a7_dev[]
+    std::mutex mu;                     // guards dev[], sid_dev[], a7_dev[]
     mig::DevGeom* dev[64] = {};        // per-device copy, uploaded on first use
-    uint32_t* trans_dev[64] = {};
+    uint16_t* sid_dev[64] = {};
     uint32_t* a7_dev[64] = {};
     ~mig_geometry();
 };

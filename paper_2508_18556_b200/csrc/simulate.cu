@@ -23,6 +23,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "device_common.cuh"
 
 namespace mig {
@@ -940,7 +942,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
-                                 const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
+                                 const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
                                  uint4* pc, int sm_count, cudaStream_t stream);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
@@ -954,13 +956,43 @@ bool simulate_use_lane() {
     return forced == 1;
 }
 
+// Policy launches on forked streams (launch_simulate): on unless MIG_CONCURRENT_POLICIES=0.
+bool simulate_concurrent() {
+    static int on = -1;
+    if (on < 0) {
+        const char* env = getenv("MIG_CONCURRENT_POLICIES");
+        on = env ? atoi(env) != 0 : 1;
+    }
+    return on != 0;
+}
+
+// Up to `want` non-blocking side streams of device `dev` (created on first use, kept for the process).
+static uint32_t lane_side_streams(int dev, uint32_t want, cudaStream_t* out) {
+    static std::mutex mu;
+    static cudaStream_t streams[64][kMaxPolicies];
+    static uint32_t have[64];
+    if (dev < 0 || dev >= 64) return 0;
+    if (want > kMaxPolicies - 1) want = kMaxPolicies - 1;
+    std::lock_guard<std::mutex> lock(mu);
+    while (have[dev] < want) {
+        if (cudaStreamCreateWithFlags(&streams[dev][have[dev]], cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            break;
+        }
+        ++have[dev];
+    }
+    const uint32_t n = have[dev] < want ? have[dev] : want;
+    for (uint32_t i = 0; i < n; ++i) out[i] = streams[dev][i];
+    return n;
+}
+
 // counter: kSimCounters zeroed u64 trace counters ([0] group kernel Scheme B, [1] group kernel Scheme A,
 // [2 + i] lane kernel, policy i).
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
-                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint32_t* trans,
-                            uint32_t n_q, const uint32_t* a7, uint32_t n_a7) {
+                            cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint16_t* sid,
+                            const uint32_t* a7, uint32_t n_a7) {
     SimParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -988,33 +1020,67 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
     cudaError_t e = cudaSuccess;
     *launches = 0;
     // the lane kernel packs idle masks per profile in a u64 and takes fusion / fission from the host tables
-    const bool lane = simulate_use_lane() && n_prof <= 8 && trans && a7;
+    const bool lane = simulate_use_lane() && n_prof <= 8 && sid && a7;
     if (lane) {  // every policy, Scheme A included: one lane-kernel launch each
+        // The policies' launches are independent (own trace counter, scratch, results column, totals row), so
+        // they alternate between `stream` and one forked side stream: each launch's CTAs start on the SMs the
+        // previous launch's tail leaves idle (persistent grids with per-lane work stealing end unevenly), while
+        // at most two launches share the GPU (more streams mixed kernels of different residency on an SM and
+        // ran slower, config 5). Fork / join by events keeps the call stream-ordered on `stream` (and capturable
+        // in a CUDA graph). MIG_CONCURRENT_POLICIES=0 serialises every launch on `stream`.
         const uint64_t blocks = simulate_lane_grid(tr.n_traces, sm_count);
         const uint64_t stride = (uint64_t)tr.max_jobs * (PA.n_pol ? kMaxLevels : 1);  // Scheme A: group lists
-        uint16_t* ring = nullptr;
-        e = cudaMallocAsync(&ring, blocks * simulate_lane_threads() * stride * sizeof(uint16_t), stream);
-        if (e != cudaSuccess) return e;
+        const size_t ring_elems = blocks * simulate_lane_threads() * stride;
         bool any_pc = false;  // PCIe contention (R39): per lane and slot run state
         for (uint32_t i = 0; i < n_pol; ++i) any_pc |= (pols[i].flags & MIG_PCIE_CONTENTION) != 0;
+        const size_t pc_elems = any_pc ? blocks * simulate_lane_threads() * 8 * 2 : 0;
+        int dev = 0;
+        e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        cudaStream_t side[kMaxPolicies] = {};
+        const uint32_t n_side = (simulate_concurrent() && n_pol > 1) ? lane_side_streams(dev, 1u, side) : 0u;
+        const uint32_t n_scr = n_side + 1;  // scratch sets: one per concurrently running launch
+        uint16_t* ring = nullptr;  // one requeue-FIFO / group-list set per stream
+        e = cudaMallocAsync(&ring, n_scr * ring_elems * sizeof(uint16_t), stream);
+        if (e != cudaSuccess) return e;
         uint4* pc = nullptr;
         if (any_pc) {
-            e = cudaMallocAsync(&pc, blocks * simulate_lane_threads() * 8 * 2 * sizeof(uint4), stream);
+            e = cudaMallocAsync(&pc, n_scr * pc_elems * sizeof(uint4), stream);
             if (e != cudaSuccess) {
                 cudaFreeAsync(ring, stream);
                 return e;
             }
         }
-        static const char* kNames[5] = {"sim_baseline", "sim_static", "sim_dynamic", "sim_ff", "sim_scheme_a"};
+        cudaEvent_t fork = nullptr, join[kMaxPolicies] = {};
+        if (n_side) {
+            e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventRecord(fork, stream);
+        }
+        // timing groups (mig_timing_enable): "~" marks launches on the side stream, whose events also span the
+        // wait for the SMs of the launch before them
+        static const char* kNames[2][5] = {{"sim_baseline", "sim_static", "sim_dynamic", "sim_ff", "sim_scheme_a"},
+                                           {"sim_baseline~", "sim_static~", "sim_dynamic~", "sim_ff~", "sim_scheme_a~"}};
         for (uint32_t i = 0; i < n_pol && e == cudaSuccess; ++i) {
-            e = (cudaError_t)mig_timed(kNames[pols[i].kind], stream, [&](uint32_t* nl) {
+            const uint32_t k = n_side ? i % n_scr : 0u;  // stream / scratch set of policy i
+            cudaStream_t st = k ? side[k - 1] : stream;
+            if (k && i < n_scr) e = cudaStreamWaitEvent(st, fork, 0);
+            if (e != cudaSuccess) break;
+            e = (cudaError_t)mig_timed(kNames[k ? 1 : 0][pols[i].kind], st, [&](uint32_t* nl) {
                 if (nl) *nl = 1;
                 return (int)launch_simulate_lane(Gdev, tr, pols[i], i, n_pol, est, out, totals, counter + 2 + i,
-                                                 est_err, ring, blocks, trans, n_q, a7, n_a7, pc, sm_count,
-                                                 stream);
+                                                 est_err, ring + k * ring_elems, blocks, sid, a7, n_a7,
+                                                 pc ? pc + k * pc_elems : nullptr, sm_count, st);
             });
             ++*launches;
         }
+        for (uint32_t k = 1; k < n_scr; ++k) {  // join: `stream` waits for every side stream's launches
+            cudaError_t e2 = cudaEventCreateWithFlags(&join[k], cudaEventDisableTiming);
+            if (e2 == cudaSuccess) e2 = cudaEventRecord(join[k], side[k - 1]);
+            if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(stream, join[k], 0);
+            if (e == cudaSuccess) e = e2;
+            if (join[k]) cudaEventDestroy(join[k]);
+        }
+        if (fork) cudaEventDestroy(fork);
         cudaFreeAsync(ring, stream);
         if (pc) cudaFreeAsync(pc, stream);
         return e;

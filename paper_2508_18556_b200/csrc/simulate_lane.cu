@@ -12,8 +12,8 @@
 //   reuse (R7) ....... idle instance starts & a per-profile "tightly fits" mask over the per-slot
 //                                    profile nibbles (<= 7 idle instances, highest start first)
 //   fusion / fission (R8) .......... only when Alg. 2 fails: the candidates touching no busy slot (a table by busy
-//                                    mask) scored from the slot-level state's transition row (host-built, global
-//                                    memory, L1-resident): fcr(result), #destroyed, destroyed slots, next state
+//                                    mask): one entry of the host-built answer table by (slot-level state of
+//                                    (occ, SM), profile, candidates) (global memory, L1-resident)
 //   next event (R28) ............... min over the eight per-slot end ticks; ties by (kind, job) (shared memory)
 // The loop is a flat state machine (PASS: one head evaluation; EVT: one event; FIN: write the unit's result and take
 // the next unit), so the 32 lanes of a warp stay in one loop even though their traces are at different points:
@@ -21,7 +21,7 @@
 // from an atomic counter one ahead (lane-level work stealing); per-policy totals are per-lane shared-memory partials
 // reduced once per CTA.
 //
-// Per-lane state: occupancy occ, instance starts SM, slot-level state id sid, busy starts BS / busy slots BM, profile
+// Per-lane state: occupancy occ, instance starts SM, busy starts BS / busy slots BM, profile
 // nibble per start slot (prof4), end tick and job|kind per start slot (shared memory, [slot][lane]),
 // the head job's record (prefetched when the queue advances), a requeue FIFO in global scratch (rare: OOM /
 // preempt restarts, R13), packed 16-bit counters, FNV-1a-64 hash halves, four u64 accumulators.
@@ -48,11 +48,11 @@ struct LaneParams {
     unsigned long long* counter;
     const unsigned long long* est_err;  // error word of k_estimate (merged into this policy's totals)
     uint16_t* ring;                     // [grid threads][ring_cap] requeue FIFOs: job | need << 10 (15 = none)
-    const uint2* trans;                 // mig_geometry::trans, [state][n_q] (FUSION_FISSION)
+    const uint16_t* sid;                // mig_geometry::sid16: slot-level state id by occ | SM << 8 (FUSION_FISSION)
     const uint2* a7;                    // mig_geometry::a7, [state][n_a7] (FUSION_FISSION)
     uint4* pc;                          // PCIe contention: per lane and start slot, 2 x uint4 of run state (R39)
     const uint32_t* arr;                // arrival ticks aligned with jobs (R40), or NULL (batch)
-    uint32_t n_q, n_a7;
+    uint32_t n_a7;
     uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
     mig_policy pol;
 };
@@ -79,7 +79,6 @@ __constant__ const uint8_t kF64[kT64] = {12, 15, 16, 17, 18, 19};
 struct LaneShared {
     DevGeom G;
     uint8_t alloc[256 * 8];   // Alg. 2 result by (occupancy, profile): placement index k, or 0xFF = FAIL
-    uint8_t qbase[8];         // transition-table column of placement 0 of profile p
     uint16_t cbase[8];        // fusion/fission-table column of candidate mask 0 of profile p
     uint8_t nobusy[256 * 8];  // FF: placements k of profile p (bit k) that touch no busy slot, by busy-slot mask
     unsigned long long reuse_sel[16];  // FF: byte q = 0xFF if an idle instance of profile q tightly fits profile p
@@ -89,7 +88,8 @@ struct LaneShared {
     uint32_t lmem[8];         // level memories, padded with 0xFFFFFFFF beyond n_levels
     uint32_t jk[8][kLaneThreads];  // per lane and start slot: job | end kind << 16 of the running job
     uint32_t et[8][kLaneThreads];  // per lane and start slot: end tick of the running job (kNoEnd = idle)
-    // per-lane partial totals (no atomics: 64-bit shared atomics are CAS loops), reduced once per CTA
+    // per-lane partial totals (no atomics: 64-bit shared atomics are CAS loops), reduced once per CTA. (Measured:
+    // moving them to global scratch for a smaller shared-memory carveout was neutral to slower.)
     uint32_t c32[kT32];            // per-CTA 32-bit counts (shared atomics)
     unsigned long long c64[kT64][kLaneThreads];
 };
@@ -104,12 +104,23 @@ __device__ __forceinline__ void lrec(uint32_t& hl, uint32_t& hh, uint32_t tick, 
 
 // Tight fit (R6, R30): the smallest-memory profile holding req (ties -> fewer compute
 // slices; profiles are sorted by (memory, compute)), with warp folding the same wave count as the whole GPU.
+template <int KIND>
 __device__ __forceinline__ uint32_t lane_tight_fit(const LaneShared& S, uint32_t req, uint32_t warps, bool fold) {
     const DevGeom& G = S.G;
     if (!fold || warps == 0) {
+        // L = #levels with memory < req over the ascending level memories (padded with 0xFFFFFFFF; n_levels <= 5,
+        // so L <= n_levels and lvl_first[n_levels] = 0xFF is "no profile"). Scheme B kinds: a branch-free binary
+        // search over the 8 padded entries (3 loads); BASELINE, whose loop is a short dependent chain, keeps the
+        // independent compares (measured A/B).
         uint32_t L = 0;
+        if (KIND == MIG_BASELINE) {
 #pragma unroll
-        for (int l = 0; l < kMaxLevels; ++l) L += S.lmem[l] < req ? 1u : 0u;  // padded with 0xFFFFFFFF
+            for (int l = 0; l < kMaxLevels; ++l) L += S.lmem[l] < req ? 1u : 0u;
+        } else {
+            L = S.lmem[3] < req ? 4u : 0u;
+            L += S.lmem[L + 1] < req ? 2u : 0u;
+            L += S.lmem[L] < req ? 1u : 0u;
+        }
         return S.lvl_first[L];
     }
     const uint32_t cf = G.wave_cap[G.full_prof];
@@ -181,11 +192,9 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             S.scand[tid] = (uint8_t)sc;
         }
         if (tid == 0) {
-            uint32_t qb = 0, cb = 0;
+            uint32_t cb = 0;
             for (uint32_t p = 0; p < 8; ++p) {
-                S.qbase[p] = (uint8_t)qb;
                 S.cbase[p] = (uint16_t)cb;
-                qb += p < G.n_prof ? G.n_place[p] : 0u;
                 cb += p < G.n_prof ? 1u << G.n_place[p] : 0u;
             }
         }
@@ -231,7 +240,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     unsigned long long tr_next = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
     uint64_t j0 = 0;
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
-    uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0, sid = 0;
+    uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0;
     uint64_t IPM = 0;  // FF: idle instances by profile, byte p bit s = an idle instance of profile p starts at s
     uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
     // u64 accumulators: turnaround, busy slice-ticks, MiB-ticks, wasted ticks (lane_acc_smem)
@@ -297,7 +306,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
         }
         t = qh = rh = rn = evm = 0;
         BS = BM = 0;
-        occ = SM = prof4 = sid = 0;
+        occ = SM = prof4 = 0;
         IPM = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) et[k * kLaneThreads] = kNoEnd;
@@ -457,7 +466,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             const uint32_t cls = (hr.z >> 16) & 0xFFu, T = hr.z & 0xFFFFu;
             if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
             const uint32_t req0 = cls == kClassDynamic ? G.mem[0] : hr.x + he.x + P.ctx;  // R16 / est + ws + ctx
-            hneed = lane_tight_fit(S, req0, he.y, fold);
+            hneed = lane_tight_fit<KIND>(S, req0, he.y, fold);
         }
         return hneed;
     };
@@ -628,7 +637,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                         }
                         if (req) {  // the tail of the job's new (larger) group
                             const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
-                            const uint32_t nn = lane_tight_fit(S, req, w, fold);
+                            const uint32_t nn = lane_tight_fit<KIND>(S, req, w, fold);
                             if (nn == kNoNeed) {
                                 lrec(hl, hh, t, (job << 16) | (K_REJECT << 12) | 0xFF0u);
                                 K2 += 1u;
@@ -651,7 +660,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             // warp reconverged between phases: every decision path then shares one copy of the common code.
             if (mode == 0 && hj == kNoJob) mode = 1;
             const bool pass = mode == 0;
-            uint32_t j = 0, need = 0, s = 0, kd = 0, nd = 0, pr = 0, lo = 0, qk = 0;
+            uint32_t j = 0, need = 0, s = 0, kd = 0, nd = 0, pr = 0, lo = 0;
             if (pass) {
                 j = hj;
                 need = head_need();
@@ -703,7 +712,6 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                         const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2: placement k
                         if (a != 0xFFu) {
                             s = G.place[need][a] & 0xFFu;
-                            qk = a;
                             kd = K_ALLOC;
                         } else {
                             // fusion / fission candidates: placements touching no busy slot (none: WAIT)
@@ -712,7 +720,9 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                             if (KIND == MIG_FUSION_FISSION && cm) {
                                 // A7 (R8): placement k destroys the idle instances it overlaps;
                                 // best (fcr(result), -#destroyed, start) over the candidates c, one table entry
-                                // per (slot-level state, profile, c) (host-built, mig_geometry::a7)
+                                // per (slot-level state, profile, c) (host-built, mig_geometry::a7); the state id of
+                                // (occ, SM) is looked up here, on the (rare) fusion path only
+                                const uint32_t sid = __ldg(P.sid + (occ | (SM << 8)));
                                 const uint2 e = __ldg(P.a7 + (sid * P.n_a7 + S.cbase[need] + cm));
                                 const uint32_t best = e.x, by = e.y;
                                 if (best) {
@@ -722,7 +732,6 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                                     IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
                                     occ &= ~rm;
                                     SM &= ~rm;
-                                    sid = by >> 8;
                                     kd = K_RECONF;
                                 }
                             }
@@ -741,10 +750,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                 const bool place = kd != K_WAIT && kd != K_REJECT;
                 if (created) {
                     occ |= ((G.pinfo[need] >> 8) & 0xFFu) << s;
-                    if (KIND == MIG_FUSION_FISSION) {
-                        SM |= 1u << s;
-                        if (kd == K_ALLOC) sid = __ldg(P.trans + (sid * P.n_q + S.qbase[need] + qk)).y >> 8;
-                    }
+                    if (KIND == MIG_FUSION_FISSION) SM |= 1u << s;
                     prof4 = (prof4 & ~(0xFu << (4 * s))) | (need << (4 * s));
                 }
                 if (KIND == MIG_FUSION_FISSION && kd == K_REUSE) IPM &= ~(1ull << (8 * pr + s));
@@ -827,7 +833,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                         }
                         if (req) {  // back to the queue tail (R13) with the new tight fit
                             const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
-                            const uint32_t nn = lane_tight_fit(S, req, w, fold);
+                            const uint32_t nn = lane_tight_fit<KIND>(S, req, w, fold);
                             uint32_t pos = rh + rn;
                             if (pos >= P.ring_cap) pos -= P.ring_cap;
                             ring[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
@@ -962,7 +968,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
-                                 const uint32_t* trans, uint32_t n_q, const uint32_t* a7, uint32_t n_a7,
+                                 const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
                                  uint4* pc, int sm_count, cudaStream_t stream) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
@@ -982,8 +988,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     P.n_pol_all = n_pol_all;
     P.pol_idx = pol_idx;
     P.pol = pol;
-    P.trans = reinterpret_cast<const uint2*>(trans);
-    P.n_q = n_q;
+    P.sid = sid;
     P.a7 = reinterpret_cast<const uint2*>(a7);
     P.n_a7 = n_a7;
     P.pc = pc;
