@@ -104,6 +104,59 @@ __device__ __forceinline__ uint32_t warp_scan_u32(uint32_t v, uint32_t lane) {
     return v;
 }
 
+// Samples after the forecast has converged (or when the job is too short to forecast): only the first exceed of
+// each memory level and the memory integral remain, so the loop is the sample draw, one level
+// ballot per chunk while a level is still reachable, and one reduction. CHECK: per-sample input checks (the range
+// bounds could break them); QUNIT: constant inverse reuse 1.0 (physical = requested + ws + ctx). Without CHECK the
+// inputs satisfy y < 2^18 and 1 <= q < 2^26, so floor(y * 2^16 / q) is computed exactly as the floor of one
+// correctly rounded double division (numerator < 2^34: the rounding error stays below 1/q).
+template <bool CHECK, bool QUNIT>
+__device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_samples, uint32_t rec_count, uint32_t base,
+                                          uint32_t T, uint32_t lane, uint64_t key, uint32_t b, uint32_t slope,
+                                          uint32_t sigma_n, uint32_t q0, uint32_t qs, int64_t ws_ctx,
+                                          uint64_t phys_hi, uint32_t& lnext, uint32_t& Smem, bool& bad,
+                                          uint32_t (&fe)[5], uint32_t (&mfe)[5]) {
+    // levels that no sample can exceed are never tested (phys_hi bounds every physical MiB of the job)
+    uint32_t lend = lnext;
+    while (lend < G.n_levels && G.level_mem[lend] < phys_hi) ++lend;
+    for (; base < T; base += 32) {
+        const uint32_t n = base + lane + 1;
+        const bool valid = n <= T;
+        uint32_t y = 0, q = 0;
+        if (valid) {
+            if (rec_samples) {
+                const uint2 v = __ldg(rec_samples + (n <= rec_count ? n : rec_count) - 1);
+                y = v.x;
+                q = v.y;
+            } else {
+                tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
+            }
+            if (CHECK) bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
+        }
+        uint64_t phys64 = 0;
+        if (valid) {
+            if (QUNIT) phys64 = (uint64_t)y + ws_ctx;
+            else if (CHECK) phys64 = (q ? ((uint64_t)y * 65536ull) / q : 0ull) + ws_ctx;
+            else phys64 = (uint64_t)floor(__ddiv_rn((double)((uint64_t)y << 16), (double)q)) + ws_ctx;
+        }
+        const uint32_t phys = (uint32_t)phys64;
+        while (lnext < lend) {
+            const uint32_t m = __ballot_sync(FULL, valid && phys64 > G.level_mem[lnext]);
+            if (!m) break;
+            const uint32_t src = (uint32_t)__ffs(m) - 1u;
+            const uint32_t pre = Smem + __reduce_add_sync(FULL, lane <= src ? phys : 0u);
+#pragma unroll
+            for (int k = 0; k < kMaxLevels; ++k)
+                if ((uint32_t)k == lnext) {
+                    fe[k] = base + src + 1u;
+                    mfe[k] = pre;
+                }
+            ++lnext;
+        }
+        Smem += __reduce_add_sync(FULL, phys);
+    }
+}
+
 // Whole-warp estimation of one DYNAMIC job (lanes over iterations).
 __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t trace_id, uint32_t jidx, uint4 r,
                                  uint4 e, uint32_t lane, mig_job_estimate* dst, const uint2* rec_samples,
@@ -135,7 +188,12 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     const uint64_t y_hi = (uint64_t)b + (((uint64_t)slope * T) >> 8) +
                           (((uint64_t)131070u * ((sigma_n & 0xFFFFu) * 7094u)) >> 28) + 2u;
     const bool check = rec_samples || y_hi >= (1u << 18) || q0 == 0 || (uint64_t)q0 + (uint64_t)qs * T >= (1u << 26);
-    for (uint32_t base = 0; base < T; base += 32) {  // to T: the memory integral needs every iteration
+    // a bound on every physical MiB of the job (generated series; q >= q0 since the inverse reuse only grows)
+    // (the division by q0 is bounded from above by a shift by floor(log2 q0): no 64-bit division here)
+    const uint64_t phys_hi = rec_samples || check ? ~0ull
+                                                  : (q_unit ? y_hi : (y_hi << 16) >> (31 - __clz(q0))) + (uint64_t)ws_ctx;
+    uint32_t base = 0;
+    for (; base < T && !done_pred; base += 32) {  // until convergence; then scan_tail to T (memory integral)
         const uint32_t n = base + lane + 1;
         const bool valid = n <= T;
         uint32_t y = 0, q = 0;
@@ -165,10 +223,6 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
             ++lnext;
         }
         const uint32_t Snext = Smem + __reduce_add_sync(FULL, phys);
-        if (done_pred) {
-            Smem = Snext;
-            continue;
-        }
         // exact integer moments at n = base + lane + 1 (inclusive warp scans + carried totals)
         const int64_t yi = y, qi = q, ni = n;
         const int64_t sy = Sy + (int64_t)warp_scan_u32(y, lane);  // sum y <= 4096 * 2^18 fits 32 bits
@@ -232,6 +286,17 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
             okprev = M;
         }
         Smem = Snext;
+    }
+    if (check) {
+        if (q_unit) scan_tail<true, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                          ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+        else scan_tail<true, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                    ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+    } else {
+        if (q_unit) scan_tail<false, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                           ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+        else scan_tail<false, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                     ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
     if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig, mfe, mconv, Smem);
