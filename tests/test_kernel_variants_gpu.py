@@ -1,5 +1,6 @@
 """Every k_simulate variant (one lane per trace: k_simulate_lane; or a group of 8 | 32 lanes per trace with job
-staging layout wide | narrow) is parity-checked against the oracle. The variant is chosen per process from MIG_LANES_PER_TRACE / MIG_JOB_LAYOUT, so each runs in a
+staging layout wide | narrow; policy launches on two streams (default) or serialised, MIG_CONCURRENT_POLICIES) is
+parity-checked against the oracle. The variant is chosen per process from MIG_LANES_PER_TRACE / MIG_JOB_LAYOUT, so each runs in a
 subprocess."""
 import os
 import subprocess
@@ -34,10 +35,10 @@ print("variant OK")
 '''
 
 
-@pytest.mark.parametrize("lanes,layout", [("1", "narrow"), ("8", "wide"), ("8", "narrow"), ("32", "wide"),
-                                          ("32", "narrow")])
-def test_variant_parity(lanes, layout):
-    env = dict(os.environ, MIG_LANES_PER_TRACE=lanes, MIG_JOB_LAYOUT=layout)
+@pytest.mark.parametrize("lanes,layout,conc", [("1", "narrow", "1"), ("1", "narrow", "0"), ("8", "wide", "1"),
+                                               ("8", "narrow", "1"), ("32", "wide", "1"), ("32", "narrow", "1")])
+def test_variant_parity(lanes, layout, conc):
+    env = dict(os.environ, MIG_LANES_PER_TRACE=lanes, MIG_JOB_LAYOUT=layout, MIG_CONCURRENT_POLICIES=conc)
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "variant OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
