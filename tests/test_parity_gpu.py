@@ -366,3 +366,32 @@ def test_nine_profile_geometry_uses_the_group_kernel(tmp_path):
     want = orc.simulate(og, jobs, ext, off, [orc.policy(**s, ctx_mib=256, reconfig_ticks=100) for s in specs], seed=5)
     assert_same(got, want)
     check_totals(got, mig.totals_numpy(tot))
+
+
+def test_cuda_graph_capture_and_replay():
+    """mig_simulate is stream-ordered (scratch by cudaMallocAsync, policy launches forked onto a side stream and
+    joined by events), so a call can be captured into a CUDA graph and replayed: the replays reproduce the eager
+    results bit for bit, and the oracle's."""
+    cfg, n = 3, 400
+    jobs, ext, off = tg.generate_host(cfg, n)
+    geo = tg.CONFIG_GEOMETRY[cfg]
+    g = mig.mig_geometry_load(f"builtin:{geo}")
+    pols = [mig.policy(g, **s) for s in SPECS]
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=tg.seed_of(cfg))
+    res, tot = mig.mig_simulate(g, tr, pols)  # eager (also uploads the geometry tables)
+    torch.cuda.synchronize()
+    eager = mig.results_numpy(res, len(pols)).copy()
+    out = torch.zeros_like(res)
+    totals = torch.zeros_like(tot)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        mig.mig_simulate(g, tr, pols, out=out, totals=totals)
+    for _ in range(3):
+        out.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(mig.results_numpy(out, len(pols)), eager)
+        assert torch.equal(totals, tot)
+    want = orc.simulate(orc.Geometry(geom_path(geo)), jobs, ext, off, [orc.policy(**s) for s in SPECS],
+                        seed=tg.seed_of(cfg))
+    assert_same(eager, want)
