@@ -244,6 +244,13 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
  * (SPEC.md:228-236). Host only. MIG_E_PARSE on a malformed string. */
 mig_status mig_workspace_bytes(const char* cublas_workspace_config, uint32_t n_layers, uint64_t* bytes);
 
+/* Test hook (DEVICE buffers, stream-ordered): out[i] = floor(y[i] * 2^16 / q[i]) computed the way k_estimate maps a
+ * requested MiB to physical MiB under inverse reuse q (reading R22) on its fast path: a float estimate corrected
+ * by one integer remainder test. Defined for y < 2^18 and 2^16 <= q < 2^26 (the estimator's in-range inputs);
+ * other inputs give unspecified values. MIG_E_INVALID_ARG on null pointers with n > 0, MIG_E_CUDA on launch
+ * failure. */
+mig_status mig_debug_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n, void* stream);
+
 /* Number of kernel launches issued by the last device call on this thread (bench accounting). */
 uint32_t mig_last_launch_count(void);
 

@@ -302,6 +302,21 @@ def estimates_numpy(est_tensor):
     return est_tensor.cpu().numpy().view(ESTIMATE_DTYPE).reshape(-1)
 
 
+def mig_debug_phys_div(y, q, out=None, stream=None):
+    """Test hook (include/mig.h): floor(y * 2^16 / q) on the device the way k_estimate's fast path computes it.
+    y, q: uint32 data in int32 CUDA tensors of equal length."""
+    import torch
+
+    if out is None:
+        out = torch.empty_like(y)
+    _check(_lib.mig_debug_phys_div(C.c_void_p(y.data_ptr()), C.c_void_p(q.data_ptr()), C.c_void_p(out.data_ptr()),
+                                   y.numel(), _stream_ptr(stream)))
+    return out
+
+
+_lib.mig_debug_phys_div.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
+
+
 def mig_workspace_bytes(cublas_workspace_config: str, n_layers: int = 1) -> int:
     """Third-party workspace bytes from a CUBLAS_WORKSPACE_CONFIG string."""
     out = C.c_uint64()

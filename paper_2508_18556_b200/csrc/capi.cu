@@ -17,6 +17,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
                             cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint16_t* sid,
                             const uint32_t* a7, uint32_t n_a7);
+cudaError_t launch_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n, cudaStream_t s);
 }  // namespace mig
 
 namespace {
@@ -237,6 +238,15 @@ mig_geometry::~mig_geometry() {
 extern "C" {
 
 const char* mig_last_error(void) { return t_err.c_str(); }
+
+mig_status mig_debug_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n, void* stream) {
+    t_launches = 0;
+    if (n && (!y || !q || !out)) return mig_set_error(MIG_E_INVALID_ARG, "mig_debug_phys_div: null buffer");
+    const cudaError_t e = mig::launch_phys_div(y, q, out, n, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "mig_debug_phys_div launch");
+    t_launches = n ? 1u : 0u;
+    return MIG_OK;
+}
 
 mig_status mig_workspace_bytes(const char* cfg, uint32_t n_layers, uint64_t* bytes) {
     if (!cfg || !bytes) return mig_set_error(MIG_E_INVALID_ARG, "mig_workspace_bytes: null argument");

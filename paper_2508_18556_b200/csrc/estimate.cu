@@ -104,12 +104,32 @@ __device__ __forceinline__ uint32_t warp_scan_u32(uint32_t v, uint32_t lane) {
     return v;
 }
 
+// floor(y * 2^16 / q), the physical MiB of a requested y under inverse reuse q (R22), for y < 2^18 and
+// 2^16 <= q < 2^26 (the quotient is below 2^18). A float estimate (exact y, q rounded to 24 bits, approximate
+// reciprocal: relative error below 2^-21, so within 1/8 of the quotient) is off by at most one, and one integer
+// remainder test on each side makes it exact. Pinned against integer division on the GPU
+// (tests/test_parity_gpu.py::test_exact_division_hook via mig_debug_phys_div).
+__device__ __forceinline__ uint32_t phys_div(uint32_t y, uint32_t q) {
+    const uint32_t k = __float2uint_rz(__fmul_rn(__uint2float_rn(y), __fdividef(65536.0f, __uint2float_rn(q))));
+    const int64_t r = (int64_t)((uint64_t)y << 16) - (int64_t)((uint64_t)k * q);
+    return r < 0 ? k - 1u : (r >= (int64_t)q ? k + 1u : k);
+}
+
+__global__ void k_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = phys_div(y[i], q[i]);
+}
+
+cudaError_t launch_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n, cudaStream_t s) {
+    if (n) k_phys_div<<<1184, 256, 0, s>>>(y, q, out, n);
+    return cudaGetLastError();
+}
+
 // Samples after the forecast has converged (or when the job is too short to forecast): only the first exceed of
 // each memory level and the memory integral remain, so the loop is the sample draw, one level
 // ballot per chunk while a level is still reachable, and one reduction. CHECK: per-sample input checks (the range
-// bounds could break them); QUNIT: constant inverse reuse 1.0 (physical = requested + ws + ctx). Without CHECK the
-// inputs satisfy y < 2^18 and 1 <= q < 2^26, so floor(y * 2^16 / q) is computed exactly as the floor of one
-// correctly rounded double division (numerator < 2^34: the rounding error stays below 1/q).
+// bounds could break them, or q may fall below 1.0); QUNIT: constant inverse reuse 1.0 (physical = requested + ws
+// + ctx). Without CHECK the inputs satisfy y < 2^18 and 2^16 <= q < 2^26: floor(y * 2^16 / q) by phys_div.
 template <bool CHECK, bool QUNIT>
 __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_samples, uint32_t rec_count, uint32_t base,
                                           uint32_t T, uint32_t lane, uint64_t key, uint32_t b, uint32_t slope,
@@ -137,7 +157,7 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
         if (valid) {
             if (QUNIT) phys64 = (uint64_t)y + ws_ctx;
             else if (CHECK) phys64 = (q ? ((uint64_t)y * 65536ull) / q : 0ull) + ws_ctx;
-            else phys64 = (uint64_t)floor(__ddiv_rn((double)((uint64_t)y << 16), (double)q)) + ws_ctx;
+            else phys64 = (uint64_t)phys_div(y, q) + ws_ctx;
         }
         const uint32_t phys = (uint32_t)phys64;
         while (lnext < lend) {
@@ -188,6 +208,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     const uint64_t y_hi = (uint64_t)b + (((uint64_t)slope * T) >> 8) +
                           (((uint64_t)131070u * ((sigma_n & 0xFFFFu) * 7094u)) >> 28) + 2u;
     const bool check = rec_samples || y_hi >= (1u << 18) || q0 == 0 || (uint64_t)q0 + (uint64_t)qs * T >= (1u << 26);
+    const bool fastq = !check && q0 >= 65536u;  // phys_div's range: generated q never decreases from q0
     // a bound on every physical MiB of the job (generated series; q >= q0 since the inverse reuse only grows)
     // (the division by q0 is bounded from above by a shift by floor(log2 q0): no 64-bit division here)
     const uint64_t phys_hi = rec_samples || check ? ~0ull
@@ -208,7 +229,8 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
             if (check) bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
         }
         // physical MiB of iteration n and its running sum (R22: requested / inverse reuse, + ws + ctx)
-        const uint64_t phys64 = valid ? (q_unit ? (uint64_t)y : ((uint64_t)y * 65536ull) / q) + ws_ctx : 0ull;
+        const uint64_t phys64 =
+            valid ? (q_unit ? (uint64_t)y : fastq ? phys_div(y, q) : ((uint64_t)y * 65536ull) / q) + ws_ctx : 0ull;
         const uint32_t phys = (uint32_t)phys64;
         // running sum of the memory integral: one reduction per chunk, prefixes only where needed
         auto prefix = [&](uint32_t m) { return Smem + __reduce_add_sync(FULL, lane <= m ? phys : 0u); };
@@ -287,16 +309,16 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
         Smem = Snext;
     }
-    if (check) {
-        if (q_unit) scan_tail<true, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
-                                          ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+    if (q_unit) {
+        if (check) scan_tail<true, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                         ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+        else scan_tail<false, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                    ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+    } else {  // (q0 < 1.0 takes the checked path: its per-sample checks never fire, its division is exact for any q)
+        if (fastq) scan_tail<false, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                           ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
         else scan_tail<true, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
                                     ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
-    } else {
-        if (q_unit) scan_tail<false, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
-                                           ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
-        else scan_tail<false, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
-                                     ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
     if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig, mfe, mconv, Smem);

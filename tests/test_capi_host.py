@@ -81,6 +81,10 @@ def test_device_calls_fail_loudly_without_gpu():
     pol = mig.policy(g)
     rc = mig._lib.mig_simulate(g.h, C.byref(desc), C.byref(pol), 1, None, None, None, None)
     assert rc == 6 and "no CUDA device" in mig._lib.mig_last_error().decode()
+    y = (C.c_uint32 * 4)(1, 2, 3, 4)
+    rc = mig._lib.mig_debug_phys_div(C.addressof(y), C.addressof(y), C.addressof(y), 4, None)
+    assert rc == 6  # MIG_E_CUDA: the kernel cannot launch without a GPU (no host fallback)
+    assert mig._lib.mig_debug_phys_div(None, None, None, 4, None) == 1  # MIG_E_INVALID_ARG
 
 
 def test_workspace_parser_spec_examples():

@@ -395,3 +395,28 @@ def test_cuda_graph_capture_and_replay():
     want = orc.simulate(orc.Geometry(geom_path(geo)), jobs, ext, off, [orc.policy(**s) for s in SPECS],
                         seed=tg.seed_of(cfg))
     assert_same(eager, want)
+
+
+def test_exact_division_hook():
+    """k_estimate's fast physical-memory division (float estimate + one integer correction) equals integer
+    division floor(y * 2^16 / q) on its whole domain's edges and on 2^24 random pairs (y < 2^18, 2^16 <= q < 2^26)."""
+    rng = np.random.default_rng(7094)
+    n = 1 << 24
+    y = rng.integers(0, 1 << 18, n, dtype=np.uint64)
+    q = rng.integers(1 << 16, 1 << 26, n, dtype=np.uint64)
+    # edges: extreme y and q, exact multiples, quotients just below / above integers
+    ey = np.array([0, 1, (1 << 18) - 1, (1 << 18) - 1, (1 << 18) - 1, 65535, 65536, 3, 12345], np.uint64)
+    eq = np.array([1 << 16, 1 << 16, 1 << 16, (1 << 26) - 1, (1 << 16) + 1, 65536, 65537, 196608, 99999], np.uint64)
+    k = rng.integers(1, 1 << 12, 1 << 20, dtype=np.uint64)
+    yk = rng.integers(1, 1 << 18, k.size, dtype=np.uint64)
+    qk = np.clip((yk << np.uint64(16)) // k, 1 << 16, (1 << 26) - 1).astype(np.uint64)
+    ys = np.concatenate([y, ey, yk, yk, yk])
+    qs = np.concatenate([q, eq, qk, np.minimum(qk + np.uint64(1), (1 << 26) - 1),
+                         np.maximum(qk - np.uint64(1), 1 << 16)])
+    want = (ys << np.uint64(16)) // qs
+    dev = torch.device("cuda", 0)
+    ty = torch.from_numpy(ys.astype(np.uint32).view(np.int32)).to(dev)
+    tq = torch.from_numpy(qs.astype(np.uint32).view(np.int32)).to(dev)
+    got = mig.mig_debug_phys_div(ty, tq).cpu().numpy().view(np.uint32).astype(np.uint64)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (ys[bad[:5]], qs[bad[:5]], got[bad[:5]], want[bad[:5]])
