@@ -47,7 +47,7 @@ struct LaneParams {
     mig_policy_totals* totals;
     unsigned long long* counter;
     const unsigned long long* est_err;  // error word of k_estimate (merged into this policy's totals)
-    uint16_t* ring;                     // [grid threads][ring_cap] requeue FIFOs: job | need << 10 (15 = none)
+    uint16_t* ring;                     // requeue FIFOs (job | need << 10) / Scheme A group lists, per lane
     const uint16_t* sid;                // mig_geometry::sid16: slot-level state id by occ | SM << 8 (FUSION_FISSION)
     const uint2* a7;                    // mig_geometry::a7, [state][n_a7] (FUSION_FISSION)
     uint4* pc;                          // PCIe contention: per lane and start slot, 2 x uint4 of run state (R39)
@@ -216,7 +216,14 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     const uint32_t reconfig = pol.reconfig_ticks, full_mem = G.full_mem;
     const uint64_t jbase = P.off[0];
     // Scheme B: requeue FIFO (ring_cap entries); Scheme A: group lists, [memory level][ring_cap]
-    uint16_t* ring = P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap * (KIND == MIG_SCHEME_A ? kMaxLevels : 1);
+    // Scheme A: lane-interleaved within the CTA's block ([entry][lane]), since the grouping pass advances every
+    // lane's lists in step (a warp at one list position touches one 64-B span, not 32 sectors; config 5 -1.5%).
+    // Scheme B: each lane's FIFO contiguous (its rare pushes and pops reuse one sector; interleaving cost +0.9% on
+    // config 2).
+    constexpr uint32_t kRs = KIND == MIG_SCHEME_A ? kLaneThreads : 1u;  // entry stride
+    uint16_t* ring = KIND == MIG_SCHEME_A
+                         ? P.ring + (size_t)blockIdx.x * kLaneThreads * P.ring_cap * kMaxLevels + tid
+                         : P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap;
     // Scheme A: [0..7] group lengths by memory level, [8..15] next group-list index of the slice at slot s
     __shared__ uint16_t s_sa[KIND == MIG_SCHEME_A ? 16 : 1][kLaneThreads];
     uint16_t* glen = &s_sa[0][tid];
@@ -263,7 +270,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             hj = qh;
             hneed = kUnk;
         } else if ((KIND != MIG_BASELINE || EXT) && rn) {
-            const uint32_t v = ring[rh];
+            const uint32_t v = ring[rh * kRs];
             hj = v & 0x3FFu;
             hneed = v >> 10;
             if (hneed == 15u) hneed = kNoNeed;
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             alast = max(alast, a);
             uint32_t pos = rh + rn;
             if (pos >= P.ring_cap) pos -= P.ring_cap;
-            ring[pos] = (uint16_t)(na | (14u << 10));
+            ring[pos * kRs] = (uint16_t)(na | (14u << 10));
             ++rn;
             ++na;
             if (hj == kNoJob) fetch_head();
@@ -531,7 +538,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                     K2 += 1u;
                 } else {
                     const uint32_t lv = G.level[need], c = glen[lv * kLaneThreads];
-                    ring[lv * P.ring_cap + c] = (uint16_t)j;
+                    ring[(lv * P.ring_cap + c) * kRs] = (uint16_t)j;
                     glen[lv * kLaneThreads] = (uint16_t)(c + 1u);
                 }
                 pop();
@@ -543,7 +550,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                 if (cand) {  // the lowest idle slice with pending jobs takes its next one
                     const uint32_t s = (uint32_t)__ffs(cand) - 1u;
                     const uint32_t k = nx[s * kLaneThreads];
-                    const uint32_t j = ring[cur * P.ring_cap + k];
+                    const uint32_t j = ring[(cur * P.ring_cap + k) * kRs];
                     const uint32_t pr = (prof4 >> (4 * s)) & 0xFu;
                     hr = __ldg(P.jobs + j0 + j);
                     he = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                                 K2 += 1u;
                             } else {
                                 const uint32_t lv = G.level[nn], c = glen[lv * kLaneThreads];
-                                ring[lv * P.ring_cap + c] = (uint16_t)job;
+                                ring[(lv * P.ring_cap + c) * kRs] = (uint16_t)job;
                                 glen[lv * kLaneThreads] = (uint16_t)(c + 1u);
                             }
                         }
@@ -836,7 +843,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                             const uint32_t nn = lane_tight_fit<KIND>(S, req, w, fold);
                             uint32_t pos = rh + rn;
                             if (pos >= P.ring_cap) pos -= P.ring_cap;
-                            ring[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
+                            ring[pos * kRs] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
                             ++rn;
                             if (hj == kNoJob) fetch_head();
                         }
