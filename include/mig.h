@@ -20,6 +20,8 @@
  *   - Ownership: the library never frees or retains caller memory beyond a call (device calls: beyond the
  *     stream-ordered work they enqueue). A mig_geometry owns its host tables and per-device copies.
  *   - Asynchrony: device entry points are stream-ordered; outputs are valid once the stream is synchronised.
+ *     Internally mig_simulate may fork work onto a library-owned side stream; it joins back into the caller's
+ *     stream by events before returning, so the call stays stream-ordered and can be captured in a CUDA graph.
  *   - Semantic outcomes (rejected or failed jobs) are counted in results, never reported as errors. Call errors
  *     are malformed arguments (MIG_E_INVALID_ARG), geometry problems (MIG_E_IO / PARSE / VALIDATION / CAPACITY),
  *     trace-format violations detected on the device (reported in mig_policy_totals.error_flags), and CUDA
@@ -257,7 +259,10 @@ uint32_t mig_last_launch_count(void);
 /* Kernel timing (bench accounting). While enabled on a thread, every device call of that thread brackets its
  * kernel launches with CUDA events on the call's stream, grouped as "k_estimate" (the estimation kernel),
  * "k_simulate" (all simulation kernels of the call) and, inside it, one group per lane-kernel policy launch
- * ("sim_baseline", "sim_static", "sim_dynamic", "sim_ff"). mig_timing_query synchronises the recorded events,
+ * ("sim_baseline", "sim_static", "sim_dynamic", "sim_ff", "sim_scheme_a"; a trailing "~" marks a launch on the
+ * library's side stream, whose span starts at the fork and includes its wait for SMs: the policy launches of one
+ * call alternate between the caller's stream and one forked side stream, joined before the call returns; set
+ * MIG_CONCURRENT_POLICIES=0 to serialise them). mig_timing_query synchronises the recorded events,
  * writes up to cap entries {name, total milliseconds, launch count} and clears the record. Enabling or disabling
  * clears it. */
 typedef struct {
