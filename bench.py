@@ -5,10 +5,10 @@ A *step* is one pass of the whole hot path over one batch of device-resident syn
   k_estimate (mig_estimate_memory: per-job memory estimation)
   k_simulate (mig_simulate: tight fit, Alg. 2 placement, fusion/fission, OOM + early restart, event loop,
               per-trace results and per-policy totals, a4-a12)
-  [N>1] NCCL all_reduce of the per-policy totals (the metric reduce of north_star).
+  [N>1] NCCL all_gather + device reduce of the per-policy totals (the metric reduce of north_star).
 Workload at N=1 = BASELINE.json configs[1] (config 2): 10^6 traces x 100 Rodinia-style jobs on A100-40GB under
 FUSION_FISSION and BASELINE (the normalisation policy). Multi-GPU is weak scaling: every rank simulates its own
-10^6-trace shard (trace ids rank*N ...), no data-path collective, one metric all_reduce per step.
+10^6-trace shard (trace ids rank*N ...), no data-path collective, one metric all_gather per step.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference] [--config 2..5]
 Under torchrun (N>1) every rank runs; rank 0 prints one JSON line.
@@ -299,7 +299,7 @@ def run_mine(args):
         m = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         elapsed_ms = float(m.item())
-    totals = mig.totals_numpy(tot)  # all ranks after the all_reduce
+    totals = mig.totals_numpy(tot)  # all ranks after the reduce
     assert int(totals["error_flags"].max()) == 0, "device reported trace-format errors"
     dec_step = int(sum(int(t["placements"]) + int(t["waits"]) + int(t["rejected"]) for t in totals))
     events_step = int(sum(int(t["placements"]) for t in totals))

@@ -2,14 +2,17 @@
 
 Traces are independent: rank r of W simulates global trace ids [r*N, (r+1)*N) (weak scaling) or
 [r*N/W, (r+1)*N/W) (strong scaling) with no data-path exchange. The only exchange step is the per-policy metric
-reduce of north_star: the int64 totals (mig_policy_totals, 20 fields per policy) are summed over ranks, except the
-makespan maximum and the error flags, which are max-reduced. Integer sums are exact in any order, so the reduced
+reduce of north_star: one all_gather of every rank's int64 totals (mig_policy_totals, 24 fields per policy, 192 B
+per policy: latency-bound over NVLink / NVSwitch), then a local reduce on the device: fields are summed (wrapping,
+like the decision-hash sum), the makespan maximum is max-reduced and the error flags OR-ed (NCCL has no bitwise-OR
+reduction, and a MAX would drop flags set on different ranks). Integer sums are exact in any order, so the reduced
 totals are bit-identical for any W.
 """
 from __future__ import annotations
 
 N_FIELDS = 24
-MAX_FIELDS = (13, 20)  # makespan_max, error_flags
+MAX_FIELD = 13  # makespan_max
+OR_FIELD = 20  # error_flags
 
 
 def shard_range(rank: int, world: int, n_per_rank: int = 0, n_total: int = 0):
@@ -22,10 +25,19 @@ def shard_range(rank: int, world: int, n_per_rank: int = 0, n_total: int = 0):
 
 
 def reduce_totals(t64, dist, group=None):
-    """In-place all_reduce of an int64 [n_policies, 24] totals tensor (NCCL over NVLink, or gloo on CPU)."""
-    mx = t64[:, list(MAX_FIELDS)].clone()
-    dist.all_reduce(t64, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
-    for k, f in enumerate(MAX_FIELDS):
-        t64[:, f] = mx[:, k]
+    """In-place reduce over ranks of an int64 [n_policies, 24] totals tensor (NCCL over NVLink, or gloo on CPU):
+    one all_gather, then sum / max / bitwise-or per field on the tensor's device."""
+    import torch
+
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(t64) for _ in range(world)]
+    dist.all_gather(parts, t64.contiguous(), group=group)
+    allt = torch.stack(parts)  # [world, n_policies, 24]
+    red = allt.sum(dim=0)
+    red[:, MAX_FIELD] = allt[:, :, MAX_FIELD].max(dim=0).values
+    flags = allt[0, :, OR_FIELD].clone()
+    for r in range(1, world):
+        flags |= allt[r, :, OR_FIELD]
+    red[:, OR_FIELD] = flags
+    t64.copy_(red)
     return t64

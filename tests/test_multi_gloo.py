@@ -86,3 +86,35 @@ def test_shard_ranges():
 
     assert [shard_range(r, 4, n_total=10) for r in range(4)] == [(0, 2), (2, 3), (5, 2), (7, 3)]
     assert shard_range(3, 8, n_per_rank=1000) == (3000, 1000)
+
+
+def _flags_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_18556_b200.sharding import reduce_totals
+
+    t = torch.zeros((2, 24), dtype=torch.int64)
+    t[:, 20] = 1 << rank  # different error bits on each rank: the reduce ORs them
+    t[:, 13] = 100 + 7 * rank  # makespan max
+    t[:, 0] = 5  # a summed field
+    t[1, 17] = -(1 << 62)  # the wrapping hash sum (u64 mod 2^64 as int64): 3 * -2^62 wraps to 2^62
+    reduce_totals(t, dist)
+    if rank == 0:
+        out.put(t.numpy().copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_reduce_ors_error_flags_and_maxes_makespan():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_flags_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert list(got[:, 20]) == [7, 7] and list(got[:, 13]) == [114, 114] and list(got[:, 0]) == [15, 15]
+    assert got[1, 17] == 1 << 62 and got[0, 17] == 0
