@@ -345,8 +345,21 @@ def run_mine(args):
         h2d = hj.numel() * 4 + (0 if he is None else he.numel() * 4) + ho.nbytes
         d2h = hres.numel() + htot.nbytes
         log(f"e2e {e2e_s * 1e3:.1f} ms/step")
+        # the PCIe bound of this path: a plain pinned host-to-device copy of the same job records, timed alone
+        dj = torch.empty_like(hj, device=dev)
+        ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dj.copy_(hj, non_blocking=True)
+        ca.record(stream)
+        for _ in range(3):
+            dj.copy_(hj, non_blocking=True)
+        cb.record(stream)
+        torch.cuda.synchronize()
+        h2d_gbs = 3 * hj.numel() * 4 / (ca.elapsed_time(cb) * 1e-3) / 1e9
+        del dj
         e2e = {"value": dec_step / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3, "api": "mig_simulate_host"}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3, "api": "mig_simulate_host",
+               "pcie_h2d_gbs": h2d_gbs, "h2d_bound_ms": h2d / h2d_gbs / 1e6,
+               "frac_of_h2d_bound": (h2d / h2d_gbs / 1e9) / e2e_s}
 
     if rank != 0:
         if world > 1:
