@@ -329,7 +329,11 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
 // job's trace is found by a ballot over the batch's offsets held one per lane.
 constexpr uint32_t kEstBatch = 32;
 
-__global__ void __launch_bounds__(256, 3) k_estimate(const DevGeom G, const EstParams P) {
+// 5 CTAs x 8 warps per SM (48 registers, 84 B of spills): measured against 3 / 4 / 6 CTAs (80 / 64 / 40 registers),
+// config 3 / 4 / 5 k_estimate 11.46 / 85.8 / 162.0 ms at 3 CTAs, 10.75 / 82.1 / 152.9 at 4, 10.72 / 81.5 / 150.3 at
+// 5, 10.81 / 81.1 / 149.6 at 6: the per-sample loop is latency-bound (RNG chain, ballots, reductions), so more
+// resident warps beat a few spilled registers
+__global__ void __launch_bounds__(256, 5) k_estimate(const DevGeom G, const EstParams P) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t j_base = P.off[0];
     for (;;) {
