@@ -59,12 +59,13 @@ struct LaneParams {
 
 constexpr int kLaneThreads = 128;
 // Resident CTAs per SM (launch bounds) and where the u64 accumulators live: the Scheme B kernels (STATIC, DYNAMIC,
-// FUSION_FISSION) keep them in shared memory and run 7 CTAs; BASELINE (record streaming, L1-bound) and Scheme A
-// keep them in registers and run 6. Measured A/B, DESIGN.md §6.
+// FUSION_FISSION) keep them in shared memory and run 7 CTAs; Scheme A keeps them in registers and runs 7 (72
+// registers; its shared-memory variant shrank the L1 its record re-reads need: config 5 +6%); BASELINE (record
+// streaming, L1-bound) keeps registers (bound 6, 63 used: 8 resident). Measured A/B, DESIGN.md §6.
 template <int KIND>
 __host__ __device__ constexpr bool lane_acc_smem() { return KIND != MIG_BASELINE && KIND != MIG_SCHEME_A; }
 template <int KIND>
-__host__ __device__ constexpr int lane_min_blocks() { return lane_acc_smem<KIND>() ? 7 : 6; }
+__host__ __device__ constexpr int lane_min_blocks() { return KIND == MIG_BASELINE ? 6 : 7; }
 constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
 constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
 
