@@ -938,12 +938,13 @@ static cudaError_t launch_variant(const DevGeom* Gdev, const SimParams& P, const
 
 uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count);
 uint32_t simulate_lane_threads();
+uint32_t simulate_lane_partials();
 cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, const mig_policy& pol, uint32_t pol_idx,
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
-                                 uint4* pc, int sm_count, cudaStream_t stream);
+                                 uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
 // (8 or 32 lanes per trace).
@@ -1040,14 +1041,18 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
         cudaStream_t side[kMaxPolicies] = {};
         const uint32_t n_side = (simulate_concurrent() && n_pol > 1) ? lane_side_streams(dev, 1u, side) : 0u;
         const uint32_t n_scr = n_side + 1;  // scratch sets: one per concurrently running launch
-        uint16_t* ring = nullptr;  // one requeue-FIFO / group-list set per stream
-        e = cudaMallocAsync(&ring, n_scr * ring_elems * sizeof(uint16_t), stream);
+        // per scratch set (one per stream): requeue FIFOs / group lists (u16), then per-lane partial totals (u64)
+        const size_t part_elems = blocks * simulate_lane_threads() * simulate_lane_partials();
+        const size_t ring_bytes = (ring_elems * sizeof(uint16_t) + 255) & ~(size_t)255;
+        const size_t set_bytes = ring_bytes + part_elems * sizeof(unsigned long long);
+        char* scr = nullptr;
+        e = cudaMallocAsync(&scr, n_scr * set_bytes, stream);
         if (e != cudaSuccess) return e;
         uint4* pc = nullptr;
         if (any_pc) {
             e = cudaMallocAsync(&pc, n_scr * pc_elems * sizeof(uint4), stream);
             if (e != cudaSuccess) {
-                cudaFreeAsync(ring, stream);
+                cudaFreeAsync(scr, stream);
                 return e;
             }
         }
@@ -1068,8 +1073,10 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
             e = (cudaError_t)mig_timed(kNames[k ? 1 : 0][pols[i].kind], st, [&](uint32_t* nl) {
                 if (nl) *nl = 1;
                 return (int)launch_simulate_lane(Gdev, tr, pols[i], i, n_pol, est, out, totals, counter + 2 + i,
-                                                 est_err, ring + k * ring_elems, blocks, sid, a7, n_a7,
-                                                 pc ? pc + k * pc_elems : nullptr, sm_count, st);
+                                                 est_err, reinterpret_cast<uint16_t*>(scr + k * set_bytes), blocks,
+                                                 sid, a7, n_a7, pc ? pc + k * pc_elems : nullptr,
+                                                 reinterpret_cast<unsigned long long*>(scr + k * set_bytes + ring_bytes),
+                                                 sm_count, st);
             });
             ++*launches;
         }
@@ -1081,7 +1088,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
             if (join[k]) cudaEventDestroy(join[k]);
         }
         if (fork) cudaEventDestroy(fork);
-        cudaFreeAsync(ring, stream);
+        cudaFreeAsync(scr, stream);
         if (pc) cudaFreeAsync(pc, stream);
         return e;
     }

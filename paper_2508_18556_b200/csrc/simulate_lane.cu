@@ -51,6 +51,7 @@ struct LaneParams {
     const uint16_t* sid;                // mig_geometry::sid16: slot-level state id by occ | SM << 8 (FUSION_FISSION)
     const uint2* a7;                    // mig_geometry::a7, [state][n_a7] (FUSION_FISSION)
     uint4* pc;                          // PCIe contention: per lane and start slot, 2 x uint4 of run state (R39)
+    unsigned long long* part;           // per-lane partial 64-bit totals, [CTA][kT64][kLaneThreads] (global scratch)
     const uint32_t* arr;                // arrival ticks aligned with jobs (R40), or NULL (batch)
     uint32_t n_a7;
     uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
@@ -59,13 +60,16 @@ struct LaneParams {
 
 constexpr int kLaneThreads = 128;
 // Resident CTAs per SM (launch bounds) and where the u64 accumulators live: the Scheme B kernels (STATIC, DYNAMIC,
-// FUSION_FISSION) keep them in shared memory and run 7 CTAs; Scheme A keeps them in registers and runs 7 (72
-// registers; its shared-memory variant shrank the L1 its record re-reads need: config 5 +6%); BASELINE (record
-// streaming, L1-bound) keeps registers (bound 6, 63 used: 8 resident). Measured A/B, DESIGN.md §6.
+// FUSION_FISSION) keep them in shared memory, BASELINE and Scheme A in registers; Scheme A runs 7 CTAs (72
+// registers), every other kind 8 (64 registers). The per-lane partial totals live in global scratch, so 8 CTAs x
+// 19.8 KB of shared memory still leave the L1 the table and record loads need. Measured A/B, config 2
+// / config 5 k_simulate: 4.84 / 250.7 ms at 7 CTAs (BASELINE 6) with the partials in shared memory; 5.25 / 299 at 8
+// with them there (28 KB of L1); 4.80 / 240.6 at 8 with the partials in global scratch; 4.70 / 238.1 with BASELINE
+// at 8 too (BASELINE at 10 / 12 CTAs spills: 4.87 / 5.66 on config 2).
 template <int KIND>
 __host__ __device__ constexpr bool lane_acc_smem() { return KIND != MIG_BASELINE && KIND != MIG_SCHEME_A; }
 template <int KIND>
-__host__ __device__ constexpr int lane_min_blocks() { return KIND == MIG_BASELINE ? 6 : 7; }
+__host__ __device__ constexpr int lane_min_blocks() { return KIND == MIG_SCHEME_A ? 7 : 8; }
 constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
 constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
 
@@ -89,10 +93,8 @@ struct LaneShared {
     uint32_t lmem[8];         // level memories, padded with 0xFFFFFFFF beyond n_levels
     uint32_t jk[8][kLaneThreads];  // per lane and start slot: job | end kind << 16 of the running job
     uint32_t et[8][kLaneThreads];  // per lane and start slot: end tick of the running job (kNoEnd = idle)
-    // per-lane partial totals (no atomics: 64-bit shared atomics are CAS loops), reduced once per CTA. (Measured:
-    // moving them to global scratch for a smaller shared-memory carveout was neutral to slower.)
     uint32_t c32[kT32];            // per-CTA 32-bit counts (shared atomics)
-    unsigned long long c64[kT64][kLaneThreads];
+    // the per-lane partial 64-bit totals live in global scratch (LaneParams::part)
 };
 
 // FNV-1a-64 step on the two 32-bit halves of h (same as simulate.cu).
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
         for (uint32_t i = tid; i < sizeof(DevGeom) / 4; i += blockDim.x) dst[i] = __ldg(src + i);
         if (tid < kT32) S.c32[tid] = 0;
 #pragma unroll
-        for (int f = 0; f < kT64; ++f) S.c64[f][tid] = 0;
+        for (int f = 0; f < kT64; ++f) P.part[((size_t)blockIdx.x * kT64 + f) * kLaneThreads + tid] = 0;
     }
     __syncthreads();
     {
@@ -898,7 +900,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                 if (destroys) atomicAdd(c + 9, destroys);
                 atomicMax(c + 10, makespan);
                 if (err) atomicOr(c + 11, err);
-                unsigned long long* d = &S.c64[0][tid];
+                unsigned long long* d = P.part + (size_t)blockIdx.x * kT64 * kLaneThreads + tid;
                 d[0 * kLaneThreads] += makespan;
                 d[1 * kLaneThreads] += a_turn;
                 d[2 * kLaneThreads] += a_busy;
@@ -926,7 +928,8 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             if (tid < kT32) {
                 v = S.c32[tid];
             } else {
-                for (int k = 0; k < kLaneThreads; ++k) v += S.c64[tid - kT32][k];
+                const unsigned long long* row = P.part + ((size_t)blockIdx.x * kT64 + (tid - kT32)) * kLaneThreads;
+                for (int k = 0; k < kLaneThreads; ++k) v += row[k];
             }
             red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
         }
@@ -970,6 +973,7 @@ uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count) {
 }
 
 uint32_t simulate_lane_threads() { return kLaneThreads; }
+uint32_t simulate_lane_partials() { return kT64; }
 
 // One launch per policy. counter: a zeroed u64; ring: blocks * kLaneThreads * max_jobs u16 of scratch.
 cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, const mig_policy& pol, uint32_t pol_idx,
@@ -977,7 +981,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
-                                 uint4* pc, int sm_count, cudaStream_t stream) {
+                                 uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -997,6 +1001,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     P.pol_idx = pol_idx;
     P.pol = pol;
     P.sid = sid;
+    P.part = part;
     P.a7 = reinterpret_cast<const uint2*>(a7);
     P.n_a7 = n_a7;
     P.pc = pc;
