@@ -1,0 +1,46 @@
+"""bench.py's JSON contract on a small run (the driver parses this line): one line on stdout with the metric and
+config BASELINE.json names, the timing keys, roofline, cpu_baseline, e2e, gpu_launches and clocks; and the
+reference arm (the CPU oracle) in the same shape."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_line_keys():
+    d = _run(["--steps", "3", "--warmup", "3", "--traces", "20000", "--cpu-seconds", "1", "--e2e-steps", "1"])
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        assert d["metric"] == json.load(f)["metric"]
+    for k in ["value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling", "vs_baseline",
+              "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"]:
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["unit"] == "decisions/s" and d["config"]["workload"].startswith("config2")
+    assert d["gpu_launches"] == 3 * 3  # k_estimate + one lane launch per policy, per step
+    r = d["roofline"]
+    assert r["bound"] == "alu" and 0 < r["frac"] < 1 and r["achieved"] > 0 and r["peak"] > 0
+    c = d["cpu_baseline"]
+    assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--ref-seconds", "0.5"])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "decisions/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
