@@ -60,16 +60,16 @@ struct LaneParams {
 
 constexpr int kLaneThreads = 128;
 // Resident CTAs per SM (launch bounds) and where the u64 accumulators live: the Scheme B kernels (STATIC, DYNAMIC,
-// FUSION_FISSION) keep them in shared memory, BASELINE and Scheme A in registers; Scheme A runs 7 CTAs (72
-// registers), every other kind 8 (64 registers). The per-lane partial totals live in global scratch, so 8 CTAs x
-// 19.8 KB of shared memory still leave the L1 the table and record loads need. Measured A/B, config 2
-// / config 5 k_simulate: 4.84 / 250.7 ms at 7 CTAs (BASELINE 6) with the partials in shared memory; 5.25 / 299 at 8
-// with them there (28 KB of L1); 4.80 / 240.6 at 8 with the partials in global scratch; 4.70 / 238.1 with BASELINE
-// at 8 too (BASELINE at 10 / 12 CTAs spills: 4.87 / 5.66 on config 2).
+// FUSION_FISSION) keep them in shared memory, BASELINE and Scheme A in registers; every kind runs 8 CTAs (64
+// registers). The per-lane partial totals live in global scratch, so 8 CTAs x 19.8 KB of shared memory still leave
+// the L1 the table and record loads need. Measured A/B, config 2 / config 5 k_simulate: 4.84 / 250.7
+// ms at 7 CTAs (BASELINE 6) with the partials in shared memory; 5.25 / 299 at 8 with them there (28 KB of L1); 4.80 /
+// 240.6 at 8 with the partials in global scratch; 4.70 / 238.1 with BASELINE at 8 too (at 10 / 12 it spills: 4.87 /
+// 5.66 on config 2); Scheme A at 7 / 8: 238.6 / 238.0 on config 5.
 template <int KIND>
 __host__ __device__ constexpr bool lane_acc_smem() { return KIND != MIG_BASELINE && KIND != MIG_SCHEME_A; }
 template <int KIND>
-__host__ __device__ constexpr int lane_min_blocks() { return KIND == MIG_SCHEME_A ? 7 : 8; }
+__host__ __device__ constexpr int lane_min_blocks() { return 8; }
 constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
 constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
 
