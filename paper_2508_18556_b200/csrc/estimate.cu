@@ -43,16 +43,20 @@ struct FitOut {
 // diagnostic a = 6K/D is computed once for the reported lane (estimate_dynamic). q_unit: the inverse reuse is
 // exactly 1.0 at every sample, so its forecast is exactly 65536 and V = 1 (the canonical sequence gives the same).
 __device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int64_t Syy, int64_t Sq, int64_t Stq,
-                                         int64_t T, double z, int64_t ws_ctx, bool q_unit, bool ewma, int64_t L) {
+                                         int64_t T, double z, int64_t ws_ctx, bool q_unit, bool ewma, int64_t L,
+                                         bool small) {
     const int64_t n2m1 = n * n - 1;
     const int64_t D = n * n2m1;
     const int64_t Ky = 2 * Sty - (n + 1) * Sy;
     const int64_t h = 2 * T - n - 1;
-    const __int128 numY = (__int128)Sy * n2m1 + (__int128)3 * Ky * h;
+    // small (y < 2^18, T <= 4096): |Sy (n^2-1)| < 2^54 and |3 Ky h| < 2^57, so numY is exact in int64 and its
+    // conversion is the same single rounding as i128_to_double's
+    const __int128 numY = small ? (__int128)0 : (__int128)Sy * n2m1 + (__int128)3 * Ky * h;
+    const int64_t numY64 = small ? Sy * n2m1 + 3 * Ky * h : 0;
     const __int128 ssrN = (__int128)n2m1 * (__int128)(n * Syy - Sy * Sy) - (__int128)3 * Ky * Ky;  // n*Syy, Sy^2 < 2^62
     const double den = __ll2double_rn(D);
     FitOut f;
-    const double yT = __ddiv_rn(i128_to_double(numY), den);
+    const double yT = __ddiv_rn(small ? __ll2double_rn(numY64) : i128_to_double(numY), den);
     const double var = __ddiv_rn(i128_to_double(ssrN), __ll2double_rn(D * (n - 2)));
     f.sigma = __dsqrt_rn(var);
     double u = __dadd_rn(yT, __dmul_rn(z, f.sigma));
@@ -267,7 +271,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
         const bool has = valid && n >= P.min_n;
         FitOut f = {0, 0.0, 0.0, 0.0};
-        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit, P.ewma != 0, myL);
+        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit, P.ewma != 0, myL, !check && T <= 4096);
         int64_t Pprev = __shfl_up_sync(FULL, f.P, 1);
         if (lane == 0) Pprev = Plast;
         const bool prev_has = n >= P.min_n + 1;
