@@ -237,7 +237,8 @@ mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const m
 
 /* Same as mig_simulate with every pointer of `traces`, `out` and `totals` in HOST memory (page-locked memory
  * recommended). Copies in, estimates, simulates and copies back in chunks pipelined over two streams on the
- * current device; returns after the results are in host memory. */
+ * current device; returns after the results are in host memory. out may be NULL: then no per-trace results are
+ * written or copied back, only the per-policy totals. */
 mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, const mig_policy* policies,
                              uint32_t n_policies, mig_trace_result* out, mig_policy_totals* totals);
 

@@ -262,15 +262,15 @@ def mig_simulate(g: Geometry, tr: Traces, pols, est=None, out=None, totals=None,
 
 
 def mig_simulate_host(g: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0=0, max_jobs=None, out=None,
-                      totals=None, samples=None, sample_off=None, arrival=None):
+                      totals=None, samples=None, sample_off=None, arrival=None, results=True):
     """HOST buffers in, HOST results out (page-locked numpy views recommended). Returns (results [n_traces, n_pol]
-    RESULT_DTYPE, totals [n_pol] TOTALS_DTYPE)."""
+    RESULT_DTYPE, or None with results=False: only the per-policy totals come back, totals [n_pol] TOTALS_DTYPE)."""
     parr, n = _policies(pols)
     n_traces = len(trace_off) - 1
     if max_jobs is None:
         lens = np.diff(np.asarray(trace_off, np.int64))
         max_jobs = max(1, int(lens.max())) if len(lens) else 1
-    if out is None:
+    if out is None and results:
         out = np.zeros((n_traces, n), RESULT_DTYPE)
     if totals is None:
         totals = np.zeros(n, TOTALS_DTYPE)
@@ -284,7 +284,8 @@ def mig_simulate_host(g: Geometry, jobs, ext, trace_off, pols, seed=0, trace_id0
                       None if samples is None else samples.ctypes.data,
                       None if sample_off is None else sample_off.ctypes.data,
                       None if arrival is None else arrival.ctypes.data)
-    _check(_lib.mig_simulate_host(g.h, C.byref(desc), parr, n, out.ctypes.data, totals.ctypes.data))
+    _check(_lib.mig_simulate_host(g.h, C.byref(desc), parr, n, None if out is None else out.ctypes.data,
+                                  totals.ctypes.data))
     return out, totals
 
 

@@ -480,7 +480,8 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         ct.samples = d_smp;
         ct.sample_off = d_soff;
         ct.arrival = T.arrival ? d_arr : nullptr;
-        st = simulate_device(g, Gdev, dev, ct, policies, n_policies, nullptr, d_est, d_out, d_tot, d_cnt, s);
+        st = simulate_device(g, Gdev, dev, ct, policies, n_policies, nullptr, d_est, out ? d_out : nullptr, d_tot, d_cnt,
+                             s);  // no per-trace results wanted: none are written
         if (d_smp) cudaFreeAsync(d_smp, s);
         if (d_soff) cudaFreeAsync(d_soff, s);
         if (st != MIG_OK) break;

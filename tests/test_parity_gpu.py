@@ -180,6 +180,8 @@ def test_host_pipeline_matches_device(monkeypatch):
     res, tot = mig.mig_simulate(g, tr, pols)
     assert np.array_equal(hres, mig.results_numpy(res, len(pols)))
     assert np.array_equal(htot, mig.totals_numpy(tot))
+    none, htot2 = mig.mig_simulate_host(g, jobs, ext, off, pols, seed=tg.seed_of(cfg), results=False)
+    assert none is None and np.array_equal(htot2, htot)  # totals only (out = NULL): the same metrics
 
 
 @pytest.mark.parametrize("cfg", [2, 3, 4, 5])
