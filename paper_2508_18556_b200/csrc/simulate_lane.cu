@@ -143,9 +143,11 @@ __device__ __forceinline__ uint32_t lane_wave_ticks(const DevGeom& G, uint32_t t
     return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
 }
 
-template <int KIND, bool EXT>
+// XR: the traces may carry extension records (jobs_ext); XR = false compiles them out (every ws / warps field 0)
+template <int KIND, bool EXT, bool XR = true>
 __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
+    const uint4* const pext = XR ? P.ext : nullptr;
     __shared__ __align__(16) LaneShared S;
     const uint32_t tid = threadIdx.x;
     {
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             return;
         }
         hr = __ldg(P.jobs + j0 + hj);
-        he = P.ext ? __ldg(P.ext + j0 + hj) : make_uint4(0, 0, 0, 0);
+        he = pext ? __ldg(pext + j0 + hj) : make_uint4(0, 0, 0, 0);
     };
     // Arrival streams (reading R40): jobs whose arrival tick is <= t join the queue tail in queue order (after the
     // requeues of the tick's events); their tight fit is computed when they first reach the head.
@@ -556,7 +558,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                     const uint32_t j = ring[(cur * P.ring_cap + k) * kRs];
                     const uint32_t pr = (prof4 >> (4 * s)) & 0xFu;
                     hr = __ldg(P.jobs + j0 + j);
-                    he = P.ext ? __ldg(P.ext + j0 + j) : make_uint4(0, 0, 0, 0);
+                    he = pext ? __ldg(pext + j0 + j) : make_uint4(0, 0, 0, 0);
                     lrec(hl, hh, t, (j << 16) | (K_PLACE_GROUP << 12) | (s << 8) | (pr << 4));
                     K0 += 1u;
                     uint32_t end, ek;
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                             req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
                         }
                         if (req) {  // the tail of the job's new (larger) group
-                            const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
+                            const uint32_t w = (fold && pext) ? __ldg(&pext[j0 + job].y) : 0u;
                             const uint32_t nn = lane_tight_fit<KIND>(S, req, w, fold);
                             if (nn == kNoNeed) {
                                 lrec(hl, hh, t, (job << 16) | (K_REJECT << 12) | 0xFF0u);
@@ -842,7 +844,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                             req = min(__ldg(&P.est[j0 + job].pred_mib), full_mem);
                         }
                         if (req) {  // back to the queue tail (R13) with the new tight fit
-                            const uint32_t w = (fold && P.ext) ? __ldg(&P.ext[j0 + job].y) : 0u;
+                            const uint32_t w = (fold && pext) ? __ldg(&pext[j0 + job].y) : 0u;
                             const uint32_t nn = lane_tight_fit<KIND>(S, req, w, fold);
                             uint32_t pos = rh + rn;
                             if (pos >= P.ring_cap) pos -= P.ring_cap;
@@ -1017,24 +1019,29 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     switch (pol.kind) {
         case MIG_BASELINE:
             if (ext) k_simulate_lane<MIG_BASELINE, true><<<grid, block, 0, stream>>>(Gdev, P);
-            else k_simulate_lane<MIG_BASELINE, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (P.ext) k_simulate_lane<MIG_BASELINE, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_BASELINE, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_STATIC:
             if (ext) k_simulate_lane<MIG_STATIC, true><<<grid, block, 0, stream>>>(Gdev, P);
-            else k_simulate_lane<MIG_STATIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (P.ext) k_simulate_lane<MIG_STATIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_STATIC, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_DYNAMIC:
             if (ext) k_simulate_lane<MIG_DYNAMIC, true><<<grid, block, 0, stream>>>(Gdev, P);
-            else k_simulate_lane<MIG_DYNAMIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (P.ext) k_simulate_lane<MIG_DYNAMIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_DYNAMIC, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_FUSION_FISSION:
             if (ext) k_simulate_lane<MIG_FUSION_FISSION, true><<<grid, block, 0, stream>>>(Gdev, P);
-            else k_simulate_lane<MIG_FUSION_FISSION, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (P.ext) k_simulate_lane<MIG_FUSION_FISSION, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_FUSION_FISSION, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_SCHEME_A:
             if (P.arr) return cudaErrorInvalidValue;  // Scheme A groups the whole queue at t = 0
             if (ext) k_simulate_lane<MIG_SCHEME_A, true><<<grid, block, 0, stream>>>(Gdev, P);
-            else k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (P.ext) k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else k_simulate_lane<MIG_SCHEME_A, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         default: return cudaErrorInvalidValue;
     }
