@@ -143,8 +143,9 @@ __device__ __forceinline__ uint32_t lane_wave_ticks(const DevGeom& G, uint32_t t
     return (uint32_t)(((uint64_t)ticks * wp + wf - 1) / wf);
 }
 
-// XR: the traces may carry extension records (jobs_ext); XR = false compiles them out (every ws / warps field 0)
-template <int KIND, bool EXT, bool XR = true>
+// XR: the traces may carry extension records (jobs_ext); XR = false compiles them out (every ws / warps field 0).
+// PF: the policy has none of MIG_WARP_FOLD, MIG_EARLY_RESTART, MIG_WAVE_TIME (their paths compiled out).
+template <int KIND, bool EXT, bool XR = true, bool PF = false>
 __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     k_simulate_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     const uint4* const pext = XR ? P.ext : nullptr;
@@ -215,9 +216,9 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     const DevGeom& G = S.G;
 
     const mig_policy& pol = P.pol;
-    const bool fold = (pol.flags & MIG_WARP_FOLD) != 0;
-    const bool er = (pol.flags & MIG_EARLY_RESTART) != 0;
-    const bool wave = (pol.flags & MIG_WAVE_TIME) != 0;
+    const bool fold = !PF && (pol.flags & MIG_WARP_FOLD) != 0;
+    const bool er = !PF && (pol.flags & MIG_EARLY_RESTART) != 0;
+    const bool wave = !PF && (pol.flags & MIG_WAVE_TIME) != 0;
     const uint32_t reconfig = pol.reconfig_ticks, full_mem = G.full_mem;
     const uint64_t jbase = P.off[0];
     // Scheme B: requeue FIFO (ring_cap entries); Scheme A: group lists, [memory level][ring_cap]
@@ -1016,31 +1017,37 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     const bool con = (pol.flags & MIG_PCIE_CONTENTION) != 0 && pol.kind != MIG_BASELINE;  // BASELINE: c <= 1
     if (con && !P.pc) return cudaErrorInvalidValue;
     const bool ext = con || P.arr;  // the EXT instantiation: contention and / or arrival streams
+    const bool pf = (pol.flags & (MIG_WARP_FOLD | MIG_EARLY_RESTART | MIG_WAVE_TIME)) == 0;
     switch (pol.kind) {
         case MIG_BASELINE:
             if (ext) k_simulate_lane<MIG_BASELINE, true><<<grid, block, 0, stream>>>(Gdev, P);
             else if (P.ext) k_simulate_lane<MIG_BASELINE, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (pf) k_simulate_lane<MIG_BASELINE, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_BASELINE, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_STATIC:
             if (ext) k_simulate_lane<MIG_STATIC, true><<<grid, block, 0, stream>>>(Gdev, P);
             else if (P.ext) k_simulate_lane<MIG_STATIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (pf) k_simulate_lane<MIG_STATIC, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_STATIC, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_DYNAMIC:
             if (ext) k_simulate_lane<MIG_DYNAMIC, true><<<grid, block, 0, stream>>>(Gdev, P);
             else if (P.ext) k_simulate_lane<MIG_DYNAMIC, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (pf) k_simulate_lane<MIG_DYNAMIC, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_DYNAMIC, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_FUSION_FISSION:
             if (ext) k_simulate_lane<MIG_FUSION_FISSION, true><<<grid, block, 0, stream>>>(Gdev, P);
             else if (P.ext) k_simulate_lane<MIG_FUSION_FISSION, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (pf) k_simulate_lane<MIG_FUSION_FISSION, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_FUSION_FISSION, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         case MIG_SCHEME_A:
             if (P.arr) return cudaErrorInvalidValue;  // Scheme A groups the whole queue at t = 0
             if (ext) k_simulate_lane<MIG_SCHEME_A, true><<<grid, block, 0, stream>>>(Gdev, P);
             else if (P.ext) k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
+            else if (pf) k_simulate_lane<MIG_SCHEME_A, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);
             else k_simulate_lane<MIG_SCHEME_A, false, false><<<grid, block, 0, stream>>>(Gdev, P);
             break;
         default: return cudaErrorInvalidValue;
