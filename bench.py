@@ -335,7 +335,8 @@ def run_mine(args):
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         timing = {}
         for with_results in (False, True):  # the metric (per-policy totals) back; then also every per-trace result
-            host_call(with_results)
+            for _ in range(2):  # warm-up calls (first-call host allocations and page mapping)
+                host_call(with_results)
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
