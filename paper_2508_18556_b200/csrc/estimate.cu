@@ -182,9 +182,13 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
 }
 
 // Whole-warp estimation of one DYNAMIC job (lanes over iterations).
+// PLAIN: generated samples and no EWMA variant (the common case), so those paths compile out.
+template <bool PLAIN>
 __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t trace_id, uint32_t jidx, uint4 r,
                                  uint4 e, uint32_t lane, mig_job_estimate* dst, const uint2* rec_samples,
                                  uint32_t rec_count) {
+    if (PLAIN) rec_samples = nullptr;
+    const bool ewma = !PLAIN && P.ewma != 0;
     const uint32_t T = r.z & 0xFFFFu;
     const uint32_t b = r.x, q0 = r.y, ws = e.x, slope = e.z, sigma_n = e.w & 0xFFFFu, qs = e.w >> 16;
     const uint64_t key = tg_key(P.seed, trace_id, jidx);
@@ -260,7 +264,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         // EWMA of the inverse reuse ratio (R36): L_1 = q_1, L_i = L_{i-1} + ((q_i - L_{i-1}) >> 3); a sequential
         // recurrence, evaluated over the chunk's lanes in order (optional variant, never on the default path).
         int64_t myL = 0;
-        if (P.ewma) {
+        if (ewma) {
             int64_t L = Lcarry;
             for (uint32_t k = 0; k < 32; ++k) {
                 const int64_t qk = (int64_t)__shfl_sync(FULL, q, k);
@@ -271,7 +275,7 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
         const bool has = valid && n >= P.min_n;
         FitOut f = {0, 0.0, 0.0, 0.0};
-        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit, P.ewma != 0, myL, !check && T <= 4096);
+        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit, ewma, myL, !check && T <= 4096);
         int64_t Pprev = __shfl_up_sync(FULL, f.P, 1);
         if (lane == 0) Pprev = Plast;
         const bool prev_has = n >= P.min_n + 1;
@@ -337,6 +341,7 @@ constexpr uint32_t kEstBatch = 32;
 // config 3 / 4 / 5 k_estimate 11.46 / 85.8 / 162.0 ms at 3 CTAs, 10.75 / 82.1 / 152.9 at 4, 10.72 / 81.5 / 150.3 at
 // 5, 10.81 / 81.1 / 149.6 at 6: the per-sample loop is latency-bound (RNG chain, ballots, reductions), so more
 // resident warps beat a few spilled registers
+template <bool PLAIN>
 __global__ void __launch_bounds__(256, 5) k_estimate(const DevGeom G, const EstParams P) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t j_base = P.off[0];
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(256, 5) k_estimate(const DevGeom G, const EstP
                         if (rcount == 0) rs = nullptr;  // nothing recorded: fall back to the declared generator
                     }
                 }
-                estimate_dynamic(G, P, P.trace_id0 + t0 + tb, jt, rr, ee, lane, P.out + gL, rs, rcount);
+                estimate_dynamic<PLAIN>(G, P, P.trace_id0 + t0 + tb, jt, rr, ee, lane, P.out + gL, rs, rcount);
             }
         }
     }
@@ -449,13 +454,15 @@ cudaError_t launch_estimate(const DevGeom& G, const mig_traces& tr, const mig_po
     P.ewma = (pol.flags & MIG_EWMA_REUSE) ? 1u : 0u;
     const int threads = 256;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_estimate, threads, 0);
+    const bool plain = !P.samples && !P.ewma;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plain ? k_estimate<true> : k_estimate<false>, threads, 0);
     if (per_sm < 1) per_sm = 1;
     uint64_t want = (tr.n_traces + 8 * kEstBatch - 1) / (8 * kEstBatch);
     uint64_t blocks = (uint64_t)per_sm * sm_count;
     if (want < blocks) blocks = want;
     if (blocks < 1) blocks = 1;
-    k_estimate<<<(unsigned)blocks, threads, 0, stream>>>(G, P);
+    if (plain) k_estimate<true><<<(unsigned)blocks, threads, 0, stream>>>(G, P);
+    else k_estimate<false><<<(unsigned)blocks, threads, 0, stream>>>(G, P);
     return cudaGetLastError();
 }
 
