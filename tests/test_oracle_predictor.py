@@ -156,3 +156,35 @@ def test_recorded_series_equals_generated():
     dyn = ((jobs[:, 2] >> 16) & 0xFF) == 2
     assert dyn.sum() > 10
     assert np.array_equal(a[dyn], b[dyn])
+
+
+def test_ewma_reuse_hand_derived():
+    # MIG_EWMA_REUSE (reading R36; BASELINE.json north_star "least-squares and EWMA memory-forecast fit"): the inverse
+    # reuse trend is replaced by L_1 = q_1, L_i = L_{i-1} + ((q_i - L_{i-1}) >> 3) (int64, arithmetic shift = floor),
+    # V = max(L_n / 65536, 1). The L values below are worked by hand, not by the recurrence. y is constant 1000
+    # (a = 0, sigma = 0), so phi = 1000 / V exactly as written and P = ceil(phi) (ctx = ws = 0).
+    pol = orc.policy(ctx_mib=0, flags=orc.EWMA_REUSE)
+    y = [1000, 1000, 1000]
+    # rising: L1 = 65536; L2 = 65536 + 65536/8 = 73728; L3 = 73728 + (131072 - 73728)/8 = 73728 + 7168 = 80896
+    P, phi, a, s = orc.fit_once(y, [65536, 131072, 131072], T=50, pol=pol)
+    assert (a, s) == (0.0, 0.0)
+    assert phi == pytest.approx(1000 * 65536 / 80896, rel=1e-12) and P == 811  # 810.1266 -> 811
+    # falling, with floor (not truncation) of the negative differences:
+    # L2 = 131072 + floor(-65535/8) = 131072 - 8192 = 122880; L3 = 122880 + floor(-57343/8) = 122880 - 7168 = 115712
+    # (truncation would give 122881 and 115713)
+    P, phi, _, _ = orc.fit_once(y, [131072, 65537, 65537], T=50, pol=pol)
+    assert phi == pytest.approx(1000 * 65536 / 115712, rel=1e-12) and P == 567  # 566.3717 -> 567
+    assert phi != pytest.approx(1000 * 65536 / 115713, rel=1e-9)
+    # n = 4 extends the same hand sequence: L4 = 115712 + floor((65537 - 115712)/8) = 115712 + floor(-6271.875)
+    # = 115712 - 6272 = 109440
+    P, phi, _, _ = orc.fit_once(y + [1000], [131072, 65537, 65537, 65537], T=50, pol=pol)
+    assert phi == pytest.approx(1000 * 65536 / 109440, rel=1e-12) and P == 599  # 598.83 -> 599
+    # below 1.0 the ratio is clamped (V >= 1): phi = u
+    P, phi, _, _ = orc.fit_once(y, [32768, 32768, 32768], T=50, pol=pol)
+    assert phi == 1000.0 and P == 1000
+    # the EWMA is a level, not a trend: the OLS line through [65536, 66536, 67536] is 64536 + 1000 t, which at
+    # T = 50 divides by 114536 / 65536 = 1.7477; the EWMA is L = 65536, 65661, 65895 -> 1.00548
+    P, phi, _, _ = orc.fit_once(y, [65536, 66536, 67536], T=50, pol=pol)
+    assert phi == pytest.approx(1000 * 65536 / 65895, rel=1e-12) and P == 995  # 994.55 -> 995
+    P_ols, _, _, _ = orc.fit_once(y, [65536, 66536, 67536], T=50, pol=orc.policy(ctx_mib=0))
+    assert P_ols == 573  # 1000 * 65536 / 114536 = 572.18 -> 573
