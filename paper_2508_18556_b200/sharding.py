@@ -41,3 +41,57 @@ def reduce_totals(t64, dist, group=None):
     red[:, OR_FIELD] = flags
     t64.copy_(red)
     return t64
+
+
+def combine_totals(t64_list):
+    """Reduce a list of int64 [n_policies, 24] totals tensors (e.g. of consecutive chunks) into a new tensor:
+    sums (wrapping), the makespan maximum, the OR of the error flags."""
+    import torch
+
+    allt = torch.stack(list(t64_list))
+    red = allt.sum(dim=0)
+    red[:, MAX_FIELD] = allt[:, :, MAX_FIELD].max(dim=0).values
+    flags = allt[0, :, OR_FIELD].clone()
+    for r in range(1, allt.shape[0]):
+        flags |= allt[r, :, OR_FIELD]
+    red[:, OR_FIELD] = flags
+    return red
+
+
+def simulate_generated(g, cfg, pols, trace_id0, n, chunk=1 << 22, sample_stride=0, device=None, stream=None,
+                       on_chunk=None):
+    """Generate the config's traces [trace_id0, trace_id0 + n) on the device chunk by chunk (SURVEY.md §8(d) C5:
+    chunks of 2^22 traces, so 10^8 traces run on any number of GPUs) and simulate each chunk with one mig_simulate
+    call. Returns (totals int64 [n_policies, 24] on the device, summed over the chunks; sampled results uint8
+    [n_samples * n_policies, 96] of the trace ids that are multiples of sample_stride, or None).
+
+    Only the chunk loop lives here: generation is tracegen's (the seeded input generator), every step of the
+    method runs in libmig's kernels."""
+    import torch
+
+    import paper_2508_18556_b200 as mig
+    from tracegen import tracegen as tg
+
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    seed = tg.seed_of(cfg)
+    J = tg.jobs_per_trace(cfg)
+    n_pol = len(pols)
+    tots, samples = [], []
+    tot = torch.empty((n_pol, 192), dtype=torch.uint8, device=dev)
+    for c0 in range(0, n, chunk):
+        m = min(chunk, n - c0)
+        t0 = trace_id0 + c0
+        jobs, ext, off = tg.generate_device(cfg, m, trace_id0=t0, seed=seed, device=dev, stream=stream)
+        tr = mig.Traces(jobs, ext, off, m, seed=seed, trace_id0=t0, max_jobs=J)
+        res, _ = mig.mig_simulate(g, tr, pols, out=None, totals=tot, write_results=sample_stride > 0, stream=stream)
+        tots.append(tot.view(torch.int64).view(n_pol, N_FIELDS).clone())
+        if sample_stride:
+            first = (-t0) % sample_stride  # first id >= t0 that is a multiple of the stride
+            if first < m:
+                rows = torch.arange(first, m, sample_stride, device=dev)
+                samples.append(res.view(m, n_pol, 96)[rows].reshape(-1, 96))
+        if on_chunk is not None:
+            on_chunk(c0, m)
+        del jobs, ext, off, tr, res
+    red = combine_totals(tots)
+    return red, (torch.cat(samples) if samples else None)
