@@ -53,7 +53,7 @@ WORKLOADS = {
             traces=10_000_000, policies=[(3, 1), (3, 0), (0, 0)]),
     5: dict(desc="config5: 100M traces x 50 jobs, A100-40GB, 6-policy sweep, sharded over the GPUs (strong), "
                  "generated on device in chunks of 2^22 traces inside the step",
-            traces=100_000_000, total=True, policies=[(0, 0), (1, 0), (2, 0), (3, 0), (3, 1), (4, 0)]),
+            traces=100_000_000, total=True, chunk=1 << 22, policies=[(0, 0), (1, 0), (2, 0), (3, 0), (3, 1), (4, 0)]),
 }
 KIND_OF = {"sim_baseline": 0, "sim_static": 1, "sim_dynamic": 2, "sim_ff": 3, "sim_scheme_a": 4}
 
@@ -211,11 +211,18 @@ class Workload:
             self.dyn_samples = int(((zf & 0xFFFF) * dyn.to(torch.int64)).sum().item())
             self.n_dyn_jobs = int(dyn.sum().item())
             self.n_jobs = self.tr.n_jobs
-        else:
+        else:  # the units the roofline counts, from one pass of the generator over the shard (not timed)
             self.res = None
             self.n_jobs = n * self.J
-            self.dyn_samples = None
-            self.n_dyn_jobs = None
+            self.dyn_samples = self.n_dyn_jobs = 0
+            for c0 in range(0, n, chunk):
+                m = min(chunk, n - c0)
+                j, _, _ = tg.generate_device(cfg, m, trace_id0=t_id0 + c0, seed=self.seed, device=dev)
+                zf = j[:, 2].to(torch.int64)
+                dyn = ((zf >> 16) & 0xFF) == 2
+                self.dyn_samples += int(((zf & 0xFFFF) * dyn.to(torch.int64)).sum().item())
+                self.n_dyn_jobs += int(dyn.sum().item())
+                del j, zf, dyn
         self.launches = 0
         self.gen_ms = 0.0
 
@@ -526,7 +533,8 @@ def run_mine(args):
     from tracegen import tracegen as tg
 
     peaks, peak_src = measured_peaks()
-    m, wl = measure(cfg, n_per, t_id0, args.steps, args.warmup, world, dist, local, dev, args.chunk, mig, tg, peaks,
+    chunk = args.chunk or spec.get("chunk", 1 << 62)
+    m, wl = measure(cfg, n_per, t_id0, args.steps, args.warmup, world, dist, local, dev, chunk, mig, tg, peaks,
                     peak_src)
     log(f"timed {args.steps} steps: {m['ms_per_step']:.3f} ms/step")
     e2e = None
@@ -542,7 +550,7 @@ def run_mine(args):
         n4 = args.dynamic_traces or WORKLOADS[4]["traces"]
         t4, _ = shard_range(rank, world, n_per_rank=n4)
         m4, wl4 = measure(4, n4, t4, args.dynamic_steps, max(3, min(args.warmup, 3)), world, dist, local, dev,
-                          args.chunk, mig, tg, peaks, peak_src)
+                          args.chunk or (1 << 62), mig, tg, peaks, peak_src)
         dyn = {"workload": WORKLOADS[4]["desc"], "traces_per_gpu": n4, "jobs_per_trace": wl4.J,
                "policies": [POLICY_NAMES[p] for p in wl4.pol_keys], "steps": args.dynamic_steps,
                "warmup": max(3, min(args.warmup, 3)), "ms_per_step": m4["ms_per_step"],
@@ -665,7 +673,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
     ap.add_argument("--traces", type=int, default=0, help="traces per GPU (weak scaling; default: the config's)")
     ap.add_argument("--total-traces", type=int, default=0, help="traces over all GPUs (strong scaling)")
-    ap.add_argument("--chunk", type=int, default=1 << 22, help="shards larger than this are generated in chunks")
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="shards larger than this are generated in chunks (default: 2^22 for config 5, else none)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dynamic", action="store_true", help="skip the config-4 dynamic_path block")

@@ -16,7 +16,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
                             cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint16_t* sid,
-                            const uint32_t* a7, uint32_t n_a7);
+                            const uint32_t* a7, uint32_t n_a7, const DevGeom* Gh);
 cudaError_t launch_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n, cudaStream_t s);
 }  // namespace mig
 
@@ -203,7 +203,7 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
     e = timed("k_simulate", s, [&](uint32_t* tl) {
         cudaError_t e2 = mig::launch_simulate(Gdev, tr, pols, n_pol, est, out, totals, counters + 2, counters + 1,
                                               sm_count_of(dev), s, &nl, g->dg.n_prof, g->sid_dev[dev],
-                                              g->a7_dev[dev], g->n_a7);
+                                              g->a7_dev[dev], g->n_a7, &g->dg);
         if (tl) *tl = nl;
         return e2;
     });

@@ -944,7 +944,8 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
-                                 uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream);
+                                 uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream,
+                                 const DevGeom* Gh);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
 // (8 or 32 lanes per trace).
@@ -993,7 +994,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                             const mig_job_estimate* est, mig_trace_result* out, mig_policy_totals* totals,
                             unsigned long long* counter, const unsigned long long* est_err, int sm_count,
                             cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint16_t* sid,
-                            const uint32_t* a7, uint32_t n_a7) {
+                            const uint32_t* a7, uint32_t n_a7, const DevGeom* Gh) {
     SimParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -1076,7 +1077,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                                                  est_err, reinterpret_cast<uint16_t*>(scr + k * set_bytes), blocks,
                                                  sid, a7, n_a7, pc ? pc + k * pc_elems : nullptr,
                                                  reinterpret_cast<unsigned long long*>(scr + k * set_bytes + ring_bytes),
-                                                 sm_count, st);
+                                                 sm_count, st, Gh);
             });
             ++*launches;
         }

@@ -56,6 +56,10 @@ struct LaneParams {
     uint32_t n_a7;
     uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
     mig_policy pol;
+    // k_ff_lane: tight fit against the ascending level memories (padded with 0xFFFFFFFF) read as constant-bank
+    // operands, and the first profile of each level as nibbles (0xF = none)
+    uint32_t lm[kMaxLevels];
+    uint32_t lfirst;
 };
 
 constexpr int kLaneThreads = 128;
@@ -952,6 +956,406 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     }
 }
 
+// ================================================================================================================
+// k_ff_lane: the FUSION_FISSION launch of the common case (no extension records, no early restart / warp folding /
+// wave time, no arrival streams or PCIe contention) written for the fewest issued instructions per step. Same
+// method, records, counters and results as k_simulate_lane<MIG_FUSION_FISSION, false, false, true> (parity-tested
+// against the oracle by the same suites); what differs is the bookkeeping:
+//  - the running instances' next events are 64-bit keys {end tick, kind, job, slot} in shared memory, so the next
+//    event of a lane (R28: tick, then COMPLETE < OOM < PREEMPT, then job id) is one unrolled minimum over the 8
+//    start slots, kept in a register (kmin) and refreshed only when an event retires; a tick's remaining events
+//    and the move to the scheduler pass need no per-tick event mask or tie loop;
+//  - each iteration is EVT (one event) then PASS (one head evaluation), so the pass that follows a tick's last
+//    event runs in the same iteration;
+//  - the tight fit compares against the level memories in the kernel's constant bank (no table loads);
+//  - the four u64 accumulators stay in registers.
+// ================================================================================================================
+struct FFShared {
+    uint32_t pinfo[16];                 // level | comp << 4 | lenmask << 8 (DevGeom::pinfo)
+    uint32_t level_mem[8], level_next[8];
+    uint32_t mem0;
+    uint8_t place_s[8][8];              // start slot of placement k of profile p
+    uint8_t alloc[256 * 8];             // Alg. 2 by (occupancy, profile): placement index, 0xFF = FAIL
+    uint8_t nobusy[256 * 8];            // placements of p touching no busy slot, by busy-slot mask
+    unsigned long long reuse_sel[16];   // idle instances that tightly fit profile p (R7), over the IPM bytes
+    uint16_t cbase[8];                  // fusion/fission-table column of candidate mask 0 of profile p
+    unsigned long long key[8][kLaneThreads];  // per lane and start slot: end << 32 | (job | kind << 16) << 3 | slot
+    uint32_t c32[kT32];
+};
+
+__device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
+    uint32_t L = 0;
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) L += req > P.lm[l] ? 1u : 0u;
+    const uint32_t p = (P.lfirst >> (4 * L)) & 0xFu;
+    return p == 0xFu ? kNoNeed : p;
+}
+
+__global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
+    __shared__ __align__(16) FFShared S;
+    const uint32_t tid = threadIdx.x;
+    {
+        const DevGeom* G = Gg;
+        for (uint32_t i = tid; i < 256 * 8; i += blockDim.x) {  // Alg. 2 for every (occupancy, profile)
+            const uint32_t occ = i >> 3, p = i & 7u;
+            const uint32_t np = __ldg(&G->n_prof), ns = __ldg(&G->n_slots);
+            uint32_t best = 0, bk = 0xFFu, nb = 0;
+            if (p < np) {
+                const uint32_t npl = __ldg(&G->n_place[p]);
+                for (uint32_t k = 0; k < npl; ++k) {
+                    const uint32_t pl = __ldg(&G->place[p][k]), qm = pl >> 8;
+                    if (occ < (1u << ns)) {
+                        const uint32_t score =
+                            (pl && !(occ & qm)) ? ((uint32_t)__ldg(&G->fcr[occ | qm]) << 8) | (pl & 0xFFu) : 0u;
+                        if (score > best) {
+                            best = score;
+                            bk = k;
+                        }
+                    }
+                    nb |= (qm & occ) ? 0u : 1u << k;  // here occ plays the busy-slot mask
+                }
+            }
+            S.alloc[i] = (uint8_t)bk;
+            S.nobusy[i] = (uint8_t)nb;
+        }
+        if (tid < 16) {
+            const uint32_t np = __ldg(&G->n_prof);
+            uint32_t ok = 0;
+            if (tid < np)
+                for (uint32_t q = 0; q < np; ++q)
+                    if (__ldg(&G->level[q]) == __ldg(&G->level[tid]) && __ldg(&G->comp[q]) >= __ldg(&G->comp[tid]))
+                        ok |= 1u << q;
+            unsigned long long sel = 0;
+            for (uint32_t q = 0; q < 8; ++q)
+                if ((ok >> q) & 1u) sel |= 0xFFull << (8 * q);
+            S.reuse_sel[tid] = sel;
+            S.pinfo[tid] = __ldg(&G->pinfo[tid]);
+        }
+        if (tid < 64) S.place_s[tid >> 3][tid & 7] = (uint8_t)__ldg(&G->place[tid >> 3][tid & 7]);
+        if (tid < 8) {
+            S.level_mem[tid] = __ldg(&G->level_mem[tid]);
+            S.level_next[tid] = __ldg(&G->level_next[tid]);
+        }
+        if (tid == 0) {
+            uint32_t cb = 0;
+            const uint32_t np = __ldg(&G->n_prof);
+            for (uint32_t p = 0; p < 8; ++p) {
+                S.cbase[p] = (uint16_t)cb;
+                cb += p < np ? 1u << __ldg(&G->n_place[p]) : 0u;
+            }
+            S.mem0 = __ldg(&G->mem[0]);
+        }
+        if (tid < kT32) S.c32[tid] = 0;
+#pragma unroll
+        for (int f = 0; f < kT64; ++f) P.part[((size_t)blockIdx.x * kT64 + f) * kLaneThreads + tid] = 0;
+    }
+    __syncthreads();
+
+    const uint32_t reconfig = P.pol.reconfig_ticks, ctx = P.ctx;
+    const uint64_t jbase = P.off[0];
+    uint16_t* const ring = P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap;
+    unsigned long long* const key = &S.key[0][tid];
+    constexpr unsigned long long kIdle = ~0ull;
+
+    unsigned long long tr = atomicAdd(P.counter, 1ull);
+    unsigned long long tr_next = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
+    const uint4* jrec = P.jobs;  // the unit's first job record
+    const mig_job_estimate* jest = P.est;
+    uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
+    uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0;
+    uint64_t IPM = 0;  // idle instances by profile: byte p bit s = an idle instance of profile p starts at s
+    uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
+    unsigned long long a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0, kmin = kIdle;
+    uint32_t hj = kNoJob, hneed = kUnk;
+    uint4 hr = make_uint4(0, 0, 0, 0);
+
+    auto fetch_head = [&]() {  // queue = jobs[qh..n) ++ requeue FIFO
+        if (qh < n) {
+            hj = qh;
+            hneed = kUnk;
+        } else if (rn) {
+            const uint32_t v = ring[rh];
+            hj = v & 0x3FFu;
+            hneed = v >> 10;
+            if (hneed == 15u) hneed = kNoNeed;
+        } else {
+            hj = kNoJob;
+            return;
+        }
+        hr = __ldg(jrec + hj);
+    };
+    auto init_unit = [&]() {
+        const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
+        jrec = P.jobs + (o0 - jbase);
+        jest = P.est + (o0 - jbase);
+        const uint64_t n64 = o1 - o0;
+        err = 0;
+        n = (uint32_t)n64;
+        if (n64 > P.max_jobs) {
+            err = (uint32_t)MIG_ERR_TRACE_TOO_LONG;
+            n = 0;
+        }
+        t = qh = rh = rn = 0;
+        occ = SM = BS = BM = prof4 = 0;
+        IPM = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) key[k * kLaneThreads] = kIdle;
+        kmin = kIdle;
+        K0 = K1 = K2 = K3 = 0;
+        a_turn = a_busy = a_mem = a_waste = 0;
+        hl = (uint32_t)kFnvOffset;
+        hh = (uint32_t)(kFnvOffset >> 32);
+        mode = 0;
+        fetch_head();
+    };
+
+    bool active = tr < P.n_traces;
+    if (active) init_unit();
+    else mode = 3;
+    while (__any_sync(FULL, active)) {
+        // ---- EVT: apply the event of kmin (R28 order), then refresh kmin ----
+        if (mode == 1) {
+            if (kmin == kIdle) {
+                mode = 2;  // nothing running and nothing placeable: the unit is done
+            } else {
+                const uint32_t lo = (uint32_t)kmin, es = lo & 7u, job = (lo >> 3) & 0xFFFFu, ek = lo >> 19;
+                t = (uint32_t)(kmin >> 32);
+                const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = S.pinfo[epr];
+                const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
+                lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7
+                if (ek == 0) {
+                    a_turn += t;
+                } else {  // OOM: next larger slice (R14) or FAILED on the whole GPU
+                    K2 += 1u << 16;
+                    const uint32_t req = S.level_next[si & 0xFu];
+                    if (req == 0) {
+                        lrec(hl, hh, t, elo | (K_FAILED << 12));
+                        K3 += 1u << 16;
+                    } else {  // back to the queue tail (R13) with the new tight fit
+                        const uint32_t nn = ff_fit(P, req);
+                        uint32_t pos = rh + rn;
+                        if (pos >= P.ring_cap) pos -= P.ring_cap;
+                        ring[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
+                        ++rn;
+                        if (hj == kNoJob) fetch_head();
+                    }
+                }
+                key[es * kLaneThreads] = kIdle;
+                BS &= ~(1u << es);
+                BM &= ~(((si >> 8) & 0xFFu) << es);
+                IPM |= 1ull << (8 * epr + es);  // the instance is idle
+                unsigned long long m = key[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) m = min(m, key[k * kLaneThreads]);
+                kmin = m;
+                if ((uint32_t)(m >> 32) != t || m == kIdle) mode = 0;  // the tick is over: one scheduler pass
+            }
+        }
+        __syncwarp();
+        // ---- PASS: evaluate the head of the queue (Alg. 4, one decision) ----
+        // P1 decides (kd, s, pr, nd); the warp reconverges; P2 records, creates and starts the run, and pops, so
+        // every decision kind shares one copy of P2
+        if (mode == 0 && hj == kNoJob) mode = 1;
+        const bool pass = mode == 0;
+        uint32_t kd = 0, s = 0, pr = 0, nd = 0;
+        if (pass) {
+            if (hneed == kUnk) {  // first evaluation of an initial queue entry: record checks + tight fit
+                const uint32_t cls = (hr.z >> 16) & 0xFFu, T = hr.z & 0xFFFFu;
+                if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
+                hneed = ff_fit(P, cls == kClassDynamic ? S.mem0 : hr.x + ctx);  // R16 / est + ctx (a2)
+            }
+            const uint32_t need = hneed;
+            pr = need;
+            if (need == kNoNeed) {  // no profile can ever hold the job: REJECT
+                kd = K_REJECT;
+            } else {
+                uint64_t x = IPM & S.reuse_sel[need];  // an idle slice that tightly fits (R7)
+                x |= x >> 32;
+                x |= x >> 16;
+                x |= x >> 8;
+                const uint32_t cand = (uint32_t)x & 0xFFu;
+                if (cand) {
+                    s = 31u - __clz(cand);
+                    pr = (prof4 >> (4 * s)) & 0xFu;
+                    kd = K_REUSE;
+                } else {
+                    const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2
+                    if (a != 0xFFu) {
+                        s = S.place_s[need][a];
+                        kd = K_ALLOC;
+                    } else {
+                        const uint32_t cm = (SM & ~BS) ? S.nobusy[(BM << 3) | need] : 0u;
+                        kd = K_WAIT;  // sleep() until a running job finishes, unless A7 finds one
+                        if (cm) {  // A7 fusion / fission (R8), host-built answer table
+                            const uint32_t sid = __ldg(P.sid + (occ | (SM << 8)));
+                            const uint2 e = __ldg(P.a7 + (sid * P.n_a7 + S.cbase[need] + cm));
+                            if (e.x) {
+                                s = e.x & 0xFFu;
+                                nd = 15u - ((e.x >> 8) & 0xFFu);
+                                const uint32_t rm = e.y & 0xFFu;
+                                IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
+                                occ &= ~rm;
+                                SM &= ~rm;
+                                kd = K_RECONF;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (pass) {
+            const uint32_t j = hj;
+            const bool place = kd <= K_RECONF;
+            if (!place) {  // WAIT / REJECT: slot 0xF, the tight fit (REJECT: 0xF)
+                lrec(hl, hh, t, (j << 16) | (kd << 12) | 0xF00u | (pr << 4));
+                if (kd == K_WAIT) {
+                    K1 += 1u << 16;
+                    mode = 1;
+                } else {
+                    K2 += 1u;
+                }
+            } else {
+                // ---- create (ALLOC / RECONF, try_new_mig_slice PAPER.md:609), record, run start ----
+                const bool created = kd != K_REUSE;
+                const uint32_t si = S.pinfo[pr];
+                const uint32_t lm8 = (si >> 8) & 0xFFu;
+                if (created) {
+                    occ |= lm8 << s;
+                    SM |= 1u << s;
+                    prof4 = (prof4 & ~(0xFu << (4 * s))) | (pr << (4 * s));
+                } else {
+                    IPM &= ~(1ull << (8 * pr + s));
+                }
+                lrec(hl, hh, t, (j << 16) | (kd << 12) | (s << 8) | (pr << 4) | nd);
+                K0 += created ? 0x10001u : 1u;
+                K1 += nd;
+                // start_run: end tick and kind (OOM > COMPLETE in one iteration, R29)
+                const uint32_t rs = t + (created ? reconfig : 0u);
+                const uint32_t lev = si & 0xFu, comp = (si >> 4) & 0xFu, T = hr.z & 0xFFFFu, ticks = hr.w;
+                uint32_t dur, ek;
+                if (((hr.z >> 16) & 0xFFu) != kClassDynamic) {
+                    const uint32_t phys = hr.y + ctx < hr.y ? 0xFFFFFFFFu : hr.y + ctx;
+                    ek = (T >= 1 && phys > S.level_mem[lev]) ? 1u : 0u;  // R12: static jobs OOM at iteration 1
+                    dur = (ek ? 1u : T) * ticks;
+                    a_mem += (uint64_t)phys * dur;
+                } else {
+                    const mig_job_estimate* ej = jest + j;
+                    const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
+                    ek = fe <= T ? 1u : 0u;
+                    dur = (ek ? fe : T) * ticks;
+                    a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? lev : 6u)) * ticks;
+                }
+                a_busy += (uint64_t)comp * dur;
+                if (ek) a_waste += dur;
+                const unsigned long long kk = ((unsigned long long)(rs + dur) << 32) | (((j | (ek << 16)) << 3) | s);
+                key[s * kLaneThreads] = kk;
+                kmin = min(kmin, kk);
+                BS |= 1u << s;
+                BM |= lm8 << s;
+            }
+            if (kd != K_WAIT) {  // pop the head
+                if (qh < n) {
+                    ++qh;
+                } else {
+                    rh = rh + 1 == P.ring_cap ? 0u : rh + 1u;
+                    --rn;
+                }
+                fetch_head();
+            }
+        }
+        __syncwarp();
+        // ---- FIN: the unit's result (96 B) and totals; take the next unit ----
+        if (mode == 2) {
+            const uint32_t placements = K0 & 0xFFFFu, creates = K0 >> 16, destroys = K1 & 0xFFFFu, waits = K1 >> 16,
+                           rejected = K2 & 0xFFFFu, ooms = K2 >> 16, preempts = K3 & 0xFFFFu, failed = K3 >> 16;
+            const uint32_t completed = n - rejected - failed, restarts = ooms - failed + preempts;
+            const uint32_t makespan = t;
+            const uint64_t energy = (uint64_t)P.pol.idle_w * makespan + (uint64_t)P.pol.w_per_slice * a_busy;
+            if (P.out) {
+                uint4* o = reinterpret_cast<uint4*>(P.out + tr * P.n_pol_all + P.pol_idx);
+                o[0] = make_uint4(makespan, n, completed, rejected);
+                o[1] = make_uint4(failed, ooms, preempts, restarts);
+                o[2] = make_uint4(placements, waits, creates, destroys);
+                o[3] = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)a_turn,
+                                  (uint32_t)(a_turn >> 32));
+                o[4] = make_uint4((uint32_t)a_busy, (uint32_t)(a_busy >> 32), hl, hh);
+                o[5] = make_uint4((uint32_t)a_mem, (uint32_t)(a_mem >> 32), (uint32_t)a_waste,
+                                  (uint32_t)(a_waste >> 32));
+            }
+            {  // a12: 32-bit counts by shared atomics, 64-bit sums in this lane's partial slots
+                uint32_t* c = S.c32;
+                atomicAdd(c + 0, 1u);
+                atomicAdd(c + 1, n);
+                if (rejected) atomicAdd(c + 2, rejected);
+                if (failed) atomicAdd(c + 3, failed);
+                if (ooms) atomicAdd(c + 4, ooms);
+                if (preempts) atomicAdd(c + 5, preempts);
+                atomicAdd(c + 6, placements);
+                if (waits) atomicAdd(c + 7, waits);
+                if (creates) atomicAdd(c + 8, creates);
+                if (destroys) atomicAdd(c + 9, destroys);
+                atomicMax(c + 10, makespan);
+                if (err) atomicOr(c + 11, err);
+                unsigned long long* d = P.part + (size_t)blockIdx.x * kT64 * kLaneThreads + tid;
+                d[0 * kLaneThreads] += makespan;
+                d[1 * kLaneThreads] += a_turn;
+                d[2 * kLaneThreads] += a_busy;
+                d[3 * kLaneThreads] += ((unsigned long long)hh << 32) | hl;
+                d[4 * kLaneThreads] += a_mem;
+                d[5 * kLaneThreads] += a_waste;
+            }
+            tr = tr_next;
+            if (tr < P.n_traces) {
+                tr_next = atomicAdd(P.counter, 1ull);
+                init_unit();
+            } else {
+                active = false;
+                mode = 3;
+            }
+        }
+    }
+    __syncthreads();
+    if (P.totals) {
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);
+        if (tid == 0 && blockIdx.x == 0 && P.est_err && *P.est_err) atomicOr(dst + 20, *P.est_err);
+        __shared__ unsigned long long red[24];
+        if (tid < kT32 + kT64) {
+            unsigned long long v = 0;
+            if (tid < kT32) {
+                v = S.c32[tid];
+            } else {
+                const unsigned long long* row = P.part + ((size_t)blockIdx.x * kT64 + (tid - kT32)) * kLaneThreads;
+                for (int k = 0; k < kLaneThreads; ++k) v += row[k];
+            }
+            red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
+        }
+        __syncthreads();
+        if (tid < 21) {
+            unsigned long long v;
+            if (tid == 2) v = red[1] - red[3] - red[4];
+            else if (tid == 7) v = red[5] - red[4] + red[6];
+            else if (tid == 14) v = (unsigned long long)P.pol.idle_w * red[12] + (unsigned long long)P.pol.w_per_slice * red[16];
+            else v = red[tid];
+            if (v) {
+                if (tid == 13) atomicMax(dst + 13, v);
+                else if (tid == 20) atomicOr(dst + 20, v);
+                else atomicAdd(dst + tid, v);
+            }
+        }
+    }
+}
+
+// MIG_FF_FAST=0 selects k_simulate_lane for the FUSION_FISSION fast case too (A/B and parity of both kernels).
+static bool ff_fast_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* env = getenv("MIG_FF_FAST");
+        on = env ? atoi(env) != 0 : 1;
+    }
+    return on != 0;
+}
+
 // Grid: resident CTAs per SM x SMs (persistent; units are taken from the counter), capped by the unit count.
 template <int KIND>
 static int lane_per_sm() {
@@ -984,7 +1388,8 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
-                                 uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream) {
+                                 uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream,
+                                 const DevGeom* Gh) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
     P.jobs = (const uint4*)tr.jobs;
@@ -1018,6 +1423,25 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     if (con && !P.pc) return cudaErrorInvalidValue;
     const bool ext = con || P.arr;  // the EXT instantiation: contention and / or arrival streams
     const bool pf = (pol.flags & (MIG_WARP_FOLD | MIG_EARLY_RESTART | MIG_WAVE_TIME)) == 0;
+    if (pol.kind == MIG_FUSION_FISSION && !ext && !P.ext && pf && Gh && ff_fast_enabled()) {
+        for (int l = 0; l < kMaxLevels; ++l) P.lm[l] = l < (int)Gh->n_levels ? Gh->level_mem[l] : 0xFFFFFFFFu;
+        uint32_t lf = 0;
+        for (uint32_t l = 0; l < 8; ++l) {  // first (fewest compute) profile of each level; 0xF = none
+            uint32_t f = 0xFu;
+            for (uint32_t p = Gh->n_prof; p-- > 0;)
+                if (l < Gh->n_levels && Gh->level[p] == l) f = p;
+            lf |= f << (4 * l);
+        }
+        P.lfirst = lf;
+        static int ff_per_sm = 0;
+        if (!ff_per_sm) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ff_per_sm, k_ff_lane, kLaneThreads, 0);
+            if (ff_per_sm < 1) ff_per_sm = 1;
+        }
+        const dim3 g2((unsigned)std::min<uint64_t>(blocks, lane_blocks(ff_per_sm, tr.n_traces, sm_count)));
+        k_ff_lane<<<g2, block, 0, stream>>>(Gdev, P);
+        return cudaGetLastError();
+    }
     switch (pol.kind) {
         case MIG_BASELINE:
             if (ext) k_simulate_lane<MIG_BASELINE, true><<<grid, block, 0, stream>>>(Gdev, P);
