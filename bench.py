@@ -202,9 +202,12 @@ class Workload:
         self.stream = torch.cuda.current_stream(dev)
         self.tot = torch.empty((self.n_pol, 192), dtype=torch.uint8, device=dev)
         self.has_ext = tg.has_ext(cfg)
+        # the generator's configs without DYNAMIC jobs (config 2) tell the library so: no estimator pass
+        self.tflags = 0 if tg.CONFIG_HAS_DYNAMIC[cfg] else mig.MIG_TRACES_NO_DYNAMIC
         if not self.chunked:
             self.jobs, self.ext, self.off = tg.generate_device(cfg, n, trace_id0=t_id0, seed=self.seed, device=dev)
-            self.tr = mig.Traces(self.jobs, self.ext, self.off, n, seed=self.seed, trace_id0=t_id0, max_jobs=self.J)
+            self.tr = mig.Traces(self.jobs, self.ext, self.off, n, seed=self.seed, trace_id0=t_id0, max_jobs=self.J,
+                                 flags=self.tflags)
             self.res = torch.empty((n * self.n_pol, 96), dtype=torch.uint8, device=dev)
             zf = self.jobs[:, 2].to(torch.int64)
             dyn = ((zf >> 16) & 0xFF) == 2

@@ -131,7 +131,7 @@ typedef struct {
     uint64_t seed;              /* sample-generator seed                                                 */
     uint64_t n_jobs;            /* trace_off[n_traces] - trace_off[0] (sizes internal estimate scratch)  */
     uint32_t max_jobs;          /* upper bound on jobs per trace, 1..MIG_MAX_JOBS_PER_TRACE               */
-    uint32_t reserved;          /* must be 0                                                             */
+    uint32_t flags;             /* MIG_TRACES_* hints, or 0                                              */
     /* Recorded per-iteration samples (requested MiB and inverse reuse ratio per iteration), or NULL
      * to draw them from the generator. samples points at the sample of index sample_off[0]; DYNAMIC job j's
      * iteration i (1-based) is samples[sample_off[j] - sample_off[0] + i - 1] = {req_mib, inv_reuse_q16}, and
@@ -149,6 +149,14 @@ typedef struct {
 } mig_traces;
 
 #define MIG_MAX_JOBS_PER_TRACE 768 /* on-chip (shared-memory) staging limit of one trace */
+
+/* mig_traces.flags. MIG_TRACES_NO_DYNAMIC: the caller asserts that no job has class DYNAMIC. Only DYNAMIC jobs
+ * need the time-series estimator (Alg. 3; the STATIC / MODEL estimate est + ws + ctx, PAPER.md:210,
+ * is formed inside the simulation kernels), so mig_simulate then skips the estimator pass over the job records
+ * (one HBM read of every record). A DYNAMIC record met under this flag is reported as MIG_ERR_BAD_RECORD in
+ * mig_policy_totals.error_flags and simulated without a forecast (no OOM and no early restart for it); its
+ * trace's results are then not meaningful. mig_estimate_memory ignores the flag. */
+#define MIG_TRACES_NO_DYNAMIC 1u
 
 /* ------------------------------------------------------------------------------------------------------------------
  * Policies

@@ -23,6 +23,7 @@ _lib = C.CDLL(LIB_PATH)
 MIG_BASELINE, MIG_STATIC, MIG_DYNAMIC, MIG_FUSION_FISSION, MIG_SCHEME_A = 0, 1, 2, 3, 4
 MIG_EARLY_RESTART, MIG_WARP_FOLD, MIG_EWMA_REUSE, MIG_WAVE_TIME, MIG_PCIE_CONTENTION = 1, 2, 4, 8, 16
 MIG_MAX_JOBS_PER_TRACE = 768
+MIG_TRACES_NO_DYNAMIC = 1  # mig_traces.flags: no DYNAMIC-class job (the estimator pass is skipped)
 MIG_NEVER = 0xFFFF
 STATUS = {0: "MIG_OK", 1: "MIG_E_INVALID_ARG", 2: "MIG_E_IO", 3: "MIG_E_PARSE", 4: "MIG_E_VALIDATION",
           5: "MIG_E_CAPACITY", 6: "MIG_E_CUDA", 7: "MIG_E_UNSUPPORTED"}
@@ -57,7 +58,7 @@ class mig_geometry_info(C.Structure):
 class mig_traces(C.Structure):
     _fields_ = [("jobs", C.c_void_p), ("jobs_ext", C.c_void_p), ("trace_off", C.c_void_p), ("n_traces", C.c_uint64),
                 ("trace_id0", C.c_uint64), ("seed", C.c_uint64), ("n_jobs", C.c_uint64), ("max_jobs", C.c_uint32),
-                ("reserved", C.c_uint32), ("samples", C.c_void_p), ("sample_off", C.c_void_p),
+                ("flags", C.c_uint32), ("samples", C.c_void_p), ("sample_off", C.c_void_p),
                 ("arrival", C.c_void_p)]
 
 
@@ -179,7 +180,7 @@ class Traces:
     """Device-resident traces: keeps the tensors alive and carries the mig_traces descriptor."""
 
     def __init__(self, jobs, ext, trace_off, n_traces, seed=0, trace_id0=0, max_jobs=None, n_jobs=None,
-                 samples=None, sample_off=None, arrival=None):
+                 samples=None, sample_off=None, arrival=None, flags=0):
         self.jobs, self.ext, self.trace_off = jobs, ext, trace_off
         self.arrival = arrival
         self.samples, self.sample_off = samples, sample_off
@@ -192,7 +193,7 @@ class Traces:
         self.max_jobs = int(max_jobs)
         self.desc = mig_traces(jobs.data_ptr() if self.n_jobs else None,
                                ext.data_ptr() if ext is not None else None, trace_off.data_ptr(), self.n_traces,
-                               trace_id0, seed, self.n_jobs, self.max_jobs, 0,
+                               trace_id0, seed, self.n_jobs, self.max_jobs, flags,
                                None if samples is None else samples.data_ptr(),
                                None if sample_off is None else sample_off.data_ptr(),
                                None if arrival is None else arrival.data_ptr())

@@ -18,6 +18,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                             cudaStream_t stream, uint32_t* launches, uint32_t n_prof, const uint16_t* sid,
                             const uint32_t* a7, uint32_t n_a7, const DevGeom* Gh);
 cudaError_t launch_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n, cudaStream_t s);
+bool simulate_lane_path(uint32_t n_prof, const void* sid, const void* a7);
 }  // namespace mig
 
 namespace {
@@ -144,7 +145,7 @@ mig_status check_traces(const mig_traces* tr) {
     if (tr->max_jobs < 1 || tr->max_jobs > MIG_MAX_JOBS_PER_TRACE)
         return mig_set_error(MIG_E_INVALID_ARG, "traces.max_jobs must be 1.." +
                                                     std::to_string(MIG_MAX_JOBS_PER_TRACE));
-    if (tr->reserved != 0) return mig_set_error(MIG_E_INVALID_ARG, "traces.reserved must be 0");
+    if (tr->flags & ~MIG_TRACES_NO_DYNAMIC) return mig_set_error(MIG_E_INVALID_ARG, "unknown traces.flags bit");
     if ((tr->samples == nullptr) != (tr->sample_off == nullptr))
         return mig_set_error(MIG_E_INVALID_ARG, "traces.samples and traces.sample_off go together");
     return MIG_OK;
@@ -190,7 +191,11 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
                            unsigned long long* counters, cudaStream_t s) {
     cudaError_t e;
     uint32_t launches = 0;
-    if (!est) {
+    // MIG_TRACES_NO_DYNAMIC: no estimates are needed (the lane kernels form the STATIC / MODEL estimate themselves
+    // and flag a DYNAMIC record); the group kernel always gets them
+    const bool skip_est = !est && (tr.flags & MIG_TRACES_NO_DYNAMIC) && mig::simulate_lane_path(g->dg.n_prof,
+                                                                                                 g->sid_dev[dev], g->a7_dev[dev]);
+    if (!est && !skip_est) {
         e = timed("k_estimate", s, [&](uint32_t* nl) {
             if (nl) *nl = 1;
             return mig::launch_estimate(g->dg, tr, pols[0], est_scratch, counters, sm_count_of(dev), true, s);
@@ -372,14 +377,17 @@ mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const m
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(totals)");
     }
     if (traces->n_traces == 0) return MIG_OK;
-    size_t est_bytes = est ? 0 : traces->n_jobs * sizeof(mig_job_estimate);
+    const bool skip_est = !est && (traces->flags & MIG_TRACES_NO_DYNAMIC) &&
+                          mig::simulate_lane_path(g->dg.n_prof, g->sid_dev[dev], g->a7_dev[dev]);
+    size_t est_bytes = (est || skip_est) ? 0 : traces->n_jobs * sizeof(mig_job_estimate);
     uint8_t* scratch = nullptr;
     cudaError_t e = cudaMallocAsync(&scratch, kCounterBytes + est_bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scratch)");
     e = cudaMemsetAsync(scratch, 0, kCounterBytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(scratch)");
     st = simulate_device(g, Gdev, dev, *traces, policies, n_policies, est,
-                         est ? nullptr : reinterpret_cast<mig_job_estimate*>(scratch + kCounterBytes), out, totals,
+                         (est || !est_bytes) ? nullptr : reinterpret_cast<mig_job_estimate*>(scratch + kCounterBytes),
+                         out, totals,
                          reinterpret_cast<unsigned long long*>(scratch), s);
     cudaFreeAsync(scratch, s);
     return st;

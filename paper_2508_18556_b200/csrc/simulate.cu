@@ -988,6 +988,11 @@ static uint32_t lane_side_streams(int dev, uint32_t want, cudaStream_t* out) {
     return n;
 }
 
+// Whether launch_simulate runs every policy on the lane kernels (which need no estimates for STATIC / MODEL jobs).
+bool simulate_lane_path(uint32_t n_prof, const void* sid, const void* a7) {
+    return simulate_use_lane() && n_prof <= 8 && sid && a7;
+}
+
 // counter: kSimCounters zeroed u64 trace counters ([0] group kernel Scheme B, [1] group kernel Scheme A,
 // [2 + i] lane kernel, policy i).
 cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig_policy* pols, uint32_t n_pol,

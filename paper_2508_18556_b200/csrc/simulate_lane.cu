@@ -377,7 +377,10 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
         const bool dyn = ((hr.z >> 16) & 0xFFu) == kClassDynamic;
         uint32_t fe, pred = 0, conv = 0, phys = 0;
         const mig_job_estimate* ej = nullptr;
-        if (__builtin_expect(dyn, 0)) {
+        if (__builtin_expect(dyn, 0) && !P.est) {  // DYNAMIC under MIG_TRACES_NO_DYNAMIC: flagged, no forecast
+            err |= (uint32_t)MIG_ERR_BAD_RECORD;
+            fe = kNever;
+        } else if (__builtin_expect(dyn, 0)) {
             ej = P.est + j0 + j;
             const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(ej));
             pred = e0.y;
@@ -406,7 +409,8 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
         if (EXT && pcie) {  // R39: the run's end follows its progress; power, memory and waste at its end
             const uint32_t it = ek == 1 ? fe : ek == 2 ? i_pre : T;
             const uint32_t mem =
-                dyn ? __ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) : phys;
+                dyn ? (ej ? __ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) : 0u)
+                    : phys;
             pcs[2 * s] = make_uint4(0u, 0u, rs, rs);
             pcs[2 * s + 1] = make_uint4(dur, mem, it, (hr.z >> 24) | (dyn ? 0x200u : 0u));
             end = rs;  // the slot's next event: the run's start
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
         a_busy += (uint64_t)comp * dur;
         if (__builtin_expect(dyn, 0)) {
             const uint32_t* m = reinterpret_cast<const uint32_t*>(ej) + 12;  // mem_fe[5], mem_conv, mem_T
-            a_mem += (uint64_t)__ldg(m + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) * ticks;
+            if (ej) a_mem += (uint64_t)__ldg(m + (ek == 1 ? lev : ek == 2 ? 5u : 6u)) * ticks;
         } else {
             a_mem += (uint64_t)phys * dur;
         }
@@ -991,7 +995,10 @@ __device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
     return p == 0xFu ? kNoNeed : p;
 }
 
-__global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
+#ifndef FF_MINB
+#define FF_MINB 8
+#endif
+__global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) FFShared S;
     const uint32_t tid = threadIdx.x;
     {
@@ -1053,14 +1060,14 @@ __global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __re
 
     const uint32_t reconfig = P.pol.reconfig_ticks, ctx = P.ctx;
     const uint64_t jbase = P.off[0];
-    uint16_t* const ring = P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap;
+#define FF_RING (P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap)
     unsigned long long* const key = &S.key[0][tid];
     constexpr unsigned long long kIdle = ~0ull;
 
     unsigned long long tr = atomicAdd(P.counter, 1ull);
-    unsigned long long tr_next = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
-    const uint4* jrec = P.jobs;  // the unit's first job record
-    const mig_job_estimate* jest = P.est;
+    __shared__ unsigned long long s_next[kLaneThreads];  // the lane's next unit (taken one ahead)
+    s_next[tid] = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
+    uint64_t j0 = 0;  // index of the unit's first job record
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
     uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0;
     uint64_t IPM = 0;  // idle instances by profile: byte p bit s = an idle instance of profile p starts at s
@@ -1074,7 +1081,7 @@ __global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __re
             hj = qh;
             hneed = kUnk;
         } else if (rn) {
-            const uint32_t v = ring[rh];
+            const uint32_t v = FF_RING[rh];
             hj = v & 0x3FFu;
             hneed = v >> 10;
             if (hneed == 15u) hneed = kNoNeed;
@@ -1082,12 +1089,11 @@ __global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __re
             hj = kNoJob;
             return;
         }
-        hr = __ldg(jrec + hj);
+        hr = __ldg(P.jobs + j0 + hj);
     };
     auto init_unit = [&]() {
         const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
-        jrec = P.jobs + (o0 - jbase);
-        jest = P.est + (o0 - jbase);
+        j0 = o0 - jbase;
         const uint64_t n64 = o1 - o0;
         err = 0;
         n = (uint32_t)n64;
@@ -1135,7 +1141,7 @@ __global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __re
                         const uint32_t nn = ff_fit(P, req);
                         uint32_t pos = rh + rn;
                         if (pos >= P.ring_cap) pos -= P.ring_cap;
-                        ring[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
+                        FF_RING[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
                         ++rn;
                         if (hj == kNoJob) fetch_head();
                     }
@@ -1239,12 +1245,16 @@ __global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __re
                     ek = (T >= 1 && phys > S.level_mem[lev]) ? 1u : 0u;  // R12: static jobs OOM at iteration 1
                     dur = (ek ? 1u : T) * ticks;
                     a_mem += (uint64_t)phys * dur;
-                } else {
-                    const mig_job_estimate* ej = jest + j;
+                } else if (P.est) {
+                    const mig_job_estimate* ej = P.est + j0 + j;
                     const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
                     ek = fe <= T ? 1u : 0u;
                     dur = (ek ? fe : T) * ticks;
                     a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? lev : 6u)) * ticks;
+                } else {  // a DYNAMIC record under MIG_TRACES_NO_DYNAMIC (no estimates): flagged, no forecast
+                    err |= (uint32_t)MIG_ERR_BAD_RECORD;
+                    ek = 0;
+                    dur = T * ticks;
                 }
                 a_busy += (uint64_t)comp * dur;
                 if (ek) a_waste += dur;
@@ -1305,9 +1315,9 @@ __global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __re
                 d[4 * kLaneThreads] += a_mem;
                 d[5 * kLaneThreads] += a_waste;
             }
-            tr = tr_next;
+            tr = s_next[tid];
             if (tr < P.n_traces) {
-                tr_next = atomicAdd(P.counter, 1ull);
+                s_next[tid] = atomicAdd(P.counter, 1ull);
                 init_unit();
             } else {
                 active = false;
@@ -1315,6 +1325,7 @@ __global__ void __launch_bounds__(kLaneThreads, 8) k_ff_lane(const DevGeom* __re
             }
         }
     }
+#undef FF_RING
     __syncthreads();
     if (P.totals) {
         unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);

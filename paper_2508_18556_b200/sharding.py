@@ -82,7 +82,8 @@ def simulate_generated(g, cfg, pols, trace_id0, n, chunk=1 << 22, sample_stride=
         m = min(chunk, n - c0)
         t0 = trace_id0 + c0
         jobs, ext, off = tg.generate_device(cfg, m, trace_id0=t0, seed=seed, device=dev, stream=stream)
-        tr = mig.Traces(jobs, ext, off, m, seed=seed, trace_id0=t0, max_jobs=J)
+        tr = mig.Traces(jobs, ext, off, m, seed=seed, trace_id0=t0, max_jobs=J,
+                        flags=0 if tg.CONFIG_HAS_DYNAMIC[cfg] else mig.MIG_TRACES_NO_DYNAMIC)
         res, _ = mig.mig_simulate(g, tr, pols, out=None, totals=tot, write_results=sample_stride > 0, stream=stream)
         tots.append(tot.view(torch.int64).view(n_pol, N_FIELDS).clone())
         if sample_stride:

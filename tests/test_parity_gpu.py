@@ -422,3 +422,29 @@ def test_exact_division_hook():
     got = mig.mig_debug_phys_div(ty, tq).cpu().numpy().view(np.uint32).astype(np.uint64)
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, (ys[bad[:5]], qs[bad[:5]], got[bad[:5]], want[bad[:5]])
+
+
+def test_no_dynamic_flag_skips_estimator_same_results():
+    # MIG_TRACES_NO_DYNAMIC (include/mig.h): on static-only traces the estimator pass is skipped (one launch fewer)
+    # and every result is unchanged; a DYNAMIC record under the flag is reported as MIG_ERR_BAD_RECORD
+    cfg, n = 2, 3000
+    jobs, ext, off = tg.generate_host(cfg, n)
+    g = mig.mig_geometry_load(f"builtin:{tg.CONFIG_GEOMETRY[cfg]}")
+    pols = [mig.policy(g, **s) for s in SPECS]
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=tg.seed_of(cfg))
+    res_a, tot_a = mig.mig_simulate(g, tr, pols)
+    la = mig.mig_last_launch_count()
+    tr.desc.flags = mig.MIG_TRACES_NO_DYNAMIC
+    res_b, tot_b = mig.mig_simulate(g, tr, pols)
+    lb = mig.mig_last_launch_count()
+    torch.cuda.synchronize()
+    assert lb == la - 1
+    assert torch.equal(res_a, res_b) and torch.equal(tot_a, tot_b)
+    # a DYNAMIC job under the flag: flagged in every policy's totals
+    j3, e3, o3 = tg.generate_host(3, 50)
+    tr3 = mig.traces_from_numpy(j3, e3, o3, seed=tg.seed_of(3))
+    tr3.desc.flags = mig.MIG_TRACES_NO_DYNAMIC
+    g3 = mig.mig_geometry_load("builtin:a100-80gb")
+    _, tot3 = mig.mig_simulate(g3, tr3, [mig.policy(g3, **s) for s in SPECS])
+    t3 = mig.totals_numpy(tot3)
+    assert ((t3["error_flags"] & 2) != 0).all()

@@ -56,3 +56,11 @@ def test_dyn_sample_noise_is_unbiased():
     assert abs(resid.mean()) < 3 * 100 / np.sqrt(4000)
     assert 90 < resid.std() < 110
     assert np.all(q == 65536)
+
+
+def test_config_has_dynamic_table():
+    # CONFIG_HAS_DYNAMIC is what lets bench.py pass MIG_TRACES_NO_DYNAMIC: it must match the generator's classes
+    for cfg in [2, 3, 4, 5]:
+        jobs, _, _ = tg.generate_host(cfg, 3000, trace_id0=777)
+        has = bool((((jobs[:, 2] >> 16) & 0xFF) == 2).any())
+        assert has == tg.CONFIG_HAS_DYNAMIC[cfg], cfg

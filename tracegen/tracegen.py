@@ -16,6 +16,9 @@ LIB_PATH = os.path.join(HERE, "libtracegen.so")
 # Config -> geometry name; cfg 1 is the fixed hand-worked A30 trace (tests/golden/config1_w.json).
 CONFIG_GEOMETRY = {1: "a30-24gb", 2: "a100-40gb", 3: "a100-80gb", 4: "h100-80gb", 5: "a100-40gb"}
 CONFIG_TRACES = {1: 1, 2: 1_000_000, 3: 1_000_000, 4: 10_000_000, 5: 100_000_000}
+# Configs whose generator emits DYNAMIC-class jobs (tracegen.h tg_gen_trace: config 2 is Rodinia STATIC only); the
+# others let a caller pass mig_traces.flags = MIG_TRACES_NO_DYNAMIC.
+CONFIG_HAS_DYNAMIC = {1: False, 2: False, 3: True, 4: True, 5: True}
 
 _lib = None
 
