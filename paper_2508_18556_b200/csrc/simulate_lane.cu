@@ -1357,6 +1357,197 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
     }
 }
 
+// ================================================================================================================
+// k_base_lane: the BASELINE launch of the common case (no extension records, no policy flags, no arrival streams).
+// BASELINE is an in-order fold over the queue: each job waits for the previous one on the whole
+// GPU, so a trace is one pass over its records with no event queue. One lane per trace; a warp takes 32 consecutive
+// traces and advances them one job per iteration in lockstep (the record of job k+1 is loaded while job k is
+// folded). Records, counters and results are those of k_simulate_lane<MIG_BASELINE> (same parity suites):
+//   per job j, at tick t:  REJECT(j) if no profile holds it; else [WAIT(j) at t, the previous run's end at its end
+//   tick (COMPLETE, or OOM + FAILED on the whole GPU), t = that tick] then PLACE_BASELINE(j) at t.
+// ================================================================================================================
+#ifndef BASE_MINB
+#define BASE_MINB 8
+#endif
+__global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
+    __shared__ uint32_t c32[kT32];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    if (tid < kT32) c32[tid] = 0;
+#pragma unroll
+    for (int f = 0; f < kT64; ++f) P.part[((size_t)blockIdx.x * kT64 + f) * kLaneThreads + tid] = 0;
+    const uint32_t fp = __ldg(&Gg->full_prof);
+    const uint32_t fsi = __ldg(&Gg->pinfo[fp]);
+    const uint32_t flev = fsi & 0xFu, fcomp = (fsi >> 4) & 0xFu, fcap = __ldg(&Gg->level_mem[flev]);
+    const uint32_t mem0 = __ldg(&Gg->mem[0]);
+    const uint32_t ctx = P.ctx;
+    const uint64_t jbase = P.off[0];
+    __syncthreads();
+    unsigned long long p_make = 0, p_turn = 0, p_busy = 0, p_hash = 0, p_mem = 0, p_waste = 0;
+    for (;;) {
+        unsigned long long w0 = 0;
+        if (lane == 0) w0 = atomicAdd(P.counter, 32ull);
+        w0 = __shfl_sync(FULL, w0, 0);
+        if (w0 >= P.n_traces) break;
+        const unsigned long long tr = w0 + lane;
+        const bool act = tr < P.n_traces;
+        uint64_t j0 = 0;
+        uint32_t n = 0, err = 0;
+        if (act) {
+            const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
+            j0 = o0 - jbase;
+            n = (uint32_t)(o1 - o0);
+            if (o1 - o0 > P.max_jobs) {
+                err = (uint32_t)MIG_ERR_TRACE_TOO_LONG;
+                n = 0;
+            }
+        }
+        const uint32_t nmax = __reduce_max_sync(FULL, n);
+        uint32_t t = 0, bend = 0, bjob = 0, hl = (uint32_t)kFnvOffset, hh = (uint32_t)(kFnvOffset >> 32);
+        uint32_t placements = 0, waits = 0, rejected = 0, failed = 0;
+        bool busy = false, boom = false;
+        unsigned long long a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
+        const uint4* rec = P.jobs + j0;
+        uint4 r = n ? __ldg(rec) : make_uint4(0, 0, 0, 0);
+        for (uint32_t k = 0; k < nmax; ++k) {
+            const uint4 rn = (k + 1 < n) ? __ldg(rec + k + 1) : make_uint4(0, 0, 0, 0);  // one ahead
+            if (k < n) {
+                const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu, j = k;
+                if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
+                const uint32_t need = ff_fit(P, cls == kClassDynamic ? mem0 : r.x + ctx);  // R16 / est + ctx
+                if (need == kNoNeed) {  // no profile can ever hold the job: REJECT (no wait)
+                    lrec(hl, hh, t, (j << 16) | (K_REJECT << 12) | 0xFF0u);
+                    ++rejected;
+                } else {
+                    if (busy) {  // the head waits for the running job, then its end event
+                        lrec(hl, hh, t, (j << 16) | (K_WAIT << 12) | 0xF00u | (need << 4));
+                        ++waits;
+                        t = bend;
+                        const uint32_t lo = (bjob << 16) | (fp << 4);
+                        if (boom) {  // OOM on the whole GPU = FAILED
+                            lrec(hl, hh, t, lo | (K_OOM << 12));
+                            lrec(hl, hh, t, lo | (K_FAILED << 12));
+                            ++failed;
+                        } else {
+                            lrec(hl, hh, t, lo | (K_COMPLETE << 12));
+                            a_turn += t;
+                        }
+                    }
+                    lrec(hl, hh, t, (j << 16) | (K_PLACE_BASELINE << 12) | (fp << 4));
+                    ++placements;
+                    // start_run on the whole GPU (OOM > COMPLETE in one iteration, R29)
+                    const uint32_t ticks = r.w;
+                    uint32_t dur, ek;
+                    if (cls != kClassDynamic) {
+                        const uint32_t phys = r.y + ctx < r.y ? 0xFFFFFFFFu : r.y + ctx;
+                        ek = (T >= 1 && phys > fcap) ? 1u : 0u;  // R12: static jobs OOM at iteration 1
+                        dur = (ek ? 1u : T) * ticks;
+                        a_mem += (uint64_t)phys * dur;
+                    } else if (P.est) {
+                        const mig_job_estimate* ej = P.est + j0 + j;
+                        const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + flev);
+                        ek = fe <= T ? 1u : 0u;
+                        dur = (ek ? fe : T) * ticks;
+                        a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? flev : 6u)) * ticks;
+                    } else {  // DYNAMIC under MIG_TRACES_NO_DYNAMIC: flagged, no forecast
+                        err |= (uint32_t)MIG_ERR_BAD_RECORD;
+                        ek = 0;
+                        dur = T * ticks;
+                    }
+                    a_busy += (uint64_t)fcomp * dur;
+                    if (ek) a_waste += dur;
+                    bend = t + dur;
+                    bjob = j;
+                    boom = ek != 0;
+                    busy = true;
+                }
+            }
+            r = rn;
+        }
+        if (busy) {  // the last run's end
+            t = bend;
+            const uint32_t lo = (bjob << 16) | (fp << 4);
+            if (boom) {
+                lrec(hl, hh, t, lo | (K_OOM << 12));
+                lrec(hl, hh, t, lo | (K_FAILED << 12));
+                ++failed;
+            } else {
+                lrec(hl, hh, t, lo | (K_COMPLETE << 12));
+                a_turn += t;
+            }
+        }
+        if (act) {
+            const uint32_t ooms = failed, completed = n - rejected - failed, makespan = t;
+            const uint64_t energy = (uint64_t)P.pol.idle_w * makespan + (uint64_t)P.pol.w_per_slice * a_busy;
+            if (P.out) {
+                uint4* o = reinterpret_cast<uint4*>(P.out + tr * P.n_pol_all + P.pol_idx);
+                o[0] = make_uint4(makespan, n, completed, rejected);
+                o[1] = make_uint4(failed, ooms, 0u, ooms - failed);
+                o[2] = make_uint4(placements, waits, 0u, 0u);
+                o[3] = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)a_turn,
+                                  (uint32_t)(a_turn >> 32));
+                o[4] = make_uint4((uint32_t)a_busy, (uint32_t)(a_busy >> 32), hl, hh);
+                o[5] = make_uint4((uint32_t)a_mem, (uint32_t)(a_mem >> 32), (uint32_t)a_waste,
+                                  (uint32_t)(a_waste >> 32));
+            }
+            atomicAdd(c32 + 0, 1u);
+            atomicAdd(c32 + 1, n);
+            if (rejected) atomicAdd(c32 + 2, rejected);
+            if (failed) {
+                atomicAdd(c32 + 3, failed);
+                atomicAdd(c32 + 4, ooms);
+            }
+            atomicAdd(c32 + 6, placements);
+            if (waits) atomicAdd(c32 + 7, waits);
+            atomicMax(c32 + 10, makespan);
+            if (err) atomicOr(c32 + 11, err);
+            p_make += makespan;
+            p_turn += a_turn;
+            p_busy += a_busy;
+            p_hash += ((unsigned long long)hh << 32) | hl;
+            p_mem += a_mem;
+            p_waste += a_waste;
+        }
+    }
+    {
+        unsigned long long* d = P.part + (size_t)blockIdx.x * kT64 * kLaneThreads + tid;
+        d[0 * kLaneThreads] = p_make;
+        d[1 * kLaneThreads] = p_turn;
+        d[2 * kLaneThreads] = p_busy;
+        d[3 * kLaneThreads] = p_hash;
+        d[4 * kLaneThreads] = p_mem;
+        d[5 * kLaneThreads] = p_waste;
+    }
+    __syncthreads();
+    if (P.totals) {
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);
+        if (tid == 0 && blockIdx.x == 0 && P.est_err && *P.est_err) atomicOr(dst + 20, *P.est_err);
+        __shared__ unsigned long long red[24];
+        if (tid < kT32 + kT64) {
+            unsigned long long v = 0;
+            if (tid < kT32) {
+                v = c32[tid];
+            } else {
+                const unsigned long long* row = P.part + ((size_t)blockIdx.x * kT64 + (tid - kT32)) * kLaneThreads;
+                for (int k = 0; k < kLaneThreads; ++k) v += row[k];
+            }
+            red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
+        }
+        __syncthreads();
+        if (tid < 21) {
+            unsigned long long v;
+            if (tid == 2) v = red[1] - red[3] - red[4];
+            else if (tid == 7) v = red[5] - red[4] + red[6];
+            else if (tid == 14) v = (unsigned long long)P.pol.idle_w * red[12] + (unsigned long long)P.pol.w_per_slice * red[16];
+            else v = red[tid];
+            if (v) {
+                if (tid == 13) atomicMax(dst + 13, v);
+                else if (tid == 20) atomicOr(dst + 20, v);
+                else atomicAdd(dst + tid, v);
+            }
+        }
+    }
+}
+
 // MIG_FF_FAST=0 selects k_simulate_lane for the FUSION_FISSION fast case too (A/B and parity of both kernels).
 static bool ff_fast_enabled() {
     static int on = -1;
@@ -1434,7 +1625,9 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     if (con && !P.pc) return cudaErrorInvalidValue;
     const bool ext = con || P.arr;  // the EXT instantiation: contention and / or arrival streams
     const bool pf = (pol.flags & (MIG_WARP_FOLD | MIG_EARLY_RESTART | MIG_WAVE_TIME)) == 0;
-    if (pol.kind == MIG_FUSION_FISSION && !ext && !P.ext && pf && Gh && ff_fast_enabled()) {
+    const bool fast = (pol.kind == MIG_FUSION_FISSION || pol.kind == MIG_BASELINE) && !ext && !P.ext && pf && Gh &&
+                      ff_fast_enabled();
+    if (fast) {
         for (int l = 0; l < kMaxLevels; ++l) P.lm[l] = l < (int)Gh->n_levels ? Gh->level_mem[l] : 0xFFFFFFFFu;
         uint32_t lf = 0;
         for (uint32_t l = 0; l < 8; ++l) {  // first (fewest compute) profile of each level; 0xF = none
@@ -1444,6 +1637,16 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
             lf |= f << (4 * l);
         }
         P.lfirst = lf;
+        if (pol.kind == MIG_BASELINE) {
+            static int b_per_sm = 0;
+            if (!b_per_sm) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_per_sm, k_base_lane, kLaneThreads, 0);
+                if (b_per_sm < 1) b_per_sm = 1;
+            }
+            const dim3 g3((unsigned)std::min<uint64_t>(blocks, lane_blocks(b_per_sm, tr.n_traces, sm_count)));
+            k_base_lane<<<g3, block, 0, stream>>>(Gdev, P);
+            return cudaGetLastError();
+        }
         static int ff_per_sm = 0;
         if (!ff_per_sm) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ff_per_sm, k_ff_lane, kLaneThreads, 0);
