@@ -979,13 +979,24 @@ struct FFShared {
     uint32_t level_mem[8], level_next[8];
     uint32_t mem0;
     uint8_t place_s[8][8];              // start slot of placement k of profile p
-    uint8_t alloc[256 * 8];             // Alg. 2 by (occupancy, profile): placement index, 0xFF = FAIL
+    uint8_t alloc[256 * 8];             // Alg. 2 by (occupancy, profile): start slot of the placement, 0xFF = FAIL
+    uint32_t lmem[8];                   // level memories, padded with 0xFFFFFFFF (tight-fit binary search)
+    uint8_t lvl_first[8];               // first profile of each level ([n_levels..] = 0xFF = none)
     uint8_t nobusy[256 * 8];            // placements of p touching no busy slot, by busy-slot mask
     unsigned long long reuse_sel[16];   // idle instances that tightly fit profile p (R7), over the IPM bytes
     uint16_t cbase[8];                  // fusion/fission-table column of candidate mask 0 of profile p
     unsigned long long key[8][kLaneThreads];  // per lane and start slot: end << 32 | (job | kind << 16) << 3 | slot
     uint32_t c32[kT32];
 };
+
+// Tight fit by a branch-free binary search over the 8 padded level memories in shared memory (3 loads).
+#define FF_FIT_S(req)                                                  \
+    ([&](uint32_t r_) {                                                \
+        uint32_t L_ = S.lmem[3] < r_ ? 4u : 0u;                        \
+        L_ += S.lmem[L_ + 1] < r_ ? 2u : 0u;                           \
+        L_ += S.lmem[L_] < r_ ? 1u : 0u;                               \
+        return (uint32_t)S.lvl_first[L_];                              \
+    }(req))
 
 __device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
     uint32_t L = 0;
@@ -1016,7 +1027,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                             (pl && !(occ & qm)) ? ((uint32_t)__ldg(&G->fcr[occ | qm]) << 8) | (pl & 0xFFu) : 0u;
                         if (score > best) {
                             best = score;
-                            bk = k;
+                            bk = pl & 0xFFu;  // the start slot of the best placement
                         }
                     }
                     nb |= (qm & occ) ? 0u : 1u << k;  // here occ plays the busy-slot mask
@@ -1040,8 +1051,14 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
         }
         if (tid < 64) S.place_s[tid >> 3][tid & 7] = (uint8_t)__ldg(&G->place[tid >> 3][tid & 7]);
         if (tid < 8) {
+            const uint32_t nl = __ldg(&G->n_levels), np = __ldg(&G->n_prof);
             S.level_mem[tid] = __ldg(&G->level_mem[tid]);
             S.level_next[tid] = __ldg(&G->level_next[tid]);
+            S.lmem[tid] = tid < nl ? __ldg(&G->level_mem[tid]) : 0xFFFFFFFFu;
+            uint32_t f = 0xFFu;
+            for (uint32_t p = np; p-- > 0;)
+                if (__ldg(&G->level[p]) == tid) f = p;
+            S.lvl_first[tid] = (uint8_t)(tid < nl ? f : 0xFFu);
         }
         if (tid == 0) {
             uint32_t cb = 0;
@@ -1168,26 +1185,26 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
             if (hneed == kUnk) {  // first evaluation of an initial queue entry: record checks + tight fit
                 const uint32_t cls = (hr.z >> 16) & 0xFFu, T = hr.z & 0xFFFFu;
                 if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
-                hneed = ff_fit(P, cls == kClassDynamic ? S.mem0 : hr.x + ctx);  // R16 / est + ctx (a2)
+                hneed = FF_FIT_S(cls == kClassDynamic ? S.mem0 : hr.x + ctx);  // R16 / est + ctx (a2)
             }
             const uint32_t need = hneed;
             pr = need;
             if (need == kNoNeed) {  // no profile can ever hold the job: REJECT
                 kd = K_REJECT;
             } else {
-                uint64_t x = IPM & S.reuse_sel[need];  // an idle slice that tightly fits (R7)
-                x |= x >> 32;
-                x |= x >> 16;
-                x |= x >> 8;
-                const uint32_t cand = (uint32_t)x & 0xFFu;
+                const uint64_t x = IPM & S.reuse_sel[need];  // an idle slice that tightly fits (R7)
+                uint32_t y = (uint32_t)x | (uint32_t)(x >> 32);
+                y |= y >> 16;
+                y |= y >> 8;
+                const uint32_t cand = y & 0xFFu;
                 if (cand) {
                     s = 31u - __clz(cand);
                     pr = (prof4 >> (4 * s)) & 0xFu;
                     kd = K_REUSE;
                 } else {
-                    const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2
+                    const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2: its start
                     if (a != 0xFFu) {
-                        s = S.place_s[need][a];
+                        s = a;
                         kd = K_ALLOC;
                     } else {
                         const uint32_t cm = (SM & ~BS) ? S.nobusy[(BM << 3) | need] : 0u;
