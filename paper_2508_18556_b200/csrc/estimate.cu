@@ -134,7 +134,7 @@ cudaError_t launch_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out,
 // ballot per chunk while a level is still reachable, and one reduction. CHECK: per-sample input checks (the range
 // bounds could break them, or q may fall below 1.0); QUNIT: constant inverse reuse 1.0 (physical = requested + ws
 // + ctx). Without CHECK the inputs satisfy y < 2^18 and 2^16 <= q < 2^26: floor(y * 2^16 / q) by phys_div.
-template <bool CHECK, bool QUNIT>
+template <bool CHECK, bool QUNIT, bool W32>
 __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_samples, uint32_t rec_count, uint32_t base,
                                           uint32_t T, uint32_t lane, uint64_t key, uint32_t b, uint32_t slope,
                                           uint32_t sigma_n, uint32_t q0, uint32_t qs, int64_t ws_ctx,
@@ -143,29 +143,41 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
     // levels that no sample can exceed are never tested (phys_hi bounds every physical MiB of the job)
     uint32_t lend = lnext;
     while (lend < G.n_levels && G.level_mem[lend] < phys_hi) ++lend;
-    for (; base < T; base += 32) {
+    uint64_t lvl = lnext < lend ? G.level_mem[lnext] : ~0ull;  // the level being watched (lnext)
+    // W32 (no checks, ws + ctx < 2^31): every physical MiB is below 2^32, so the sums and tests run in 32 bits
+    const uint32_t wc32 = (uint32_t)ws_ctx;
+    auto chunk = [&](bool last) {
         const uint32_t n = base + lane + 1;
-        const bool valid = n <= T;
+        const bool valid = !last || n <= T;
         uint32_t y = 0, q = 0;
         if (valid) {
             if (rec_samples) {
                 const uint2 v = __ldg(rec_samples + (n <= rec_count ? n : rec_count) - 1);
                 y = v.x;
                 q = v.y;
-            } else {
+            } else if (CHECK) {
                 tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
+            } else {  // the series' bounds keep the draw in 32-bit range (y_hi < 2^18)
+                tg_dyn_sample_fast(key, n, b, slope, sigma_n, q0, qs, &y, &q);
             }
             if (CHECK) bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
         }
         uint64_t phys64 = 0;
-        if (valid) {
-            if (QUNIT) phys64 = (uint64_t)y + ws_ctx;
-            else if (CHECK) phys64 = (q ? ((uint64_t)y * 65536ull) / q : 0ull) + ws_ctx;
-            else phys64 = (uint64_t)phys_div(y, q) + ws_ctx;
+        uint32_t phys = 0;
+        if (W32) {
+            phys = valid ? (QUNIT ? y : phys_div(y, q)) + wc32 : 0u;
+            phys64 = phys;
+        } else {
+            if (valid) {
+                if (QUNIT) phys64 = (uint64_t)y + ws_ctx;
+                else if (CHECK) phys64 = (q ? ((uint64_t)y * 65536ull) / q : 0ull) + ws_ctx;
+                else phys64 = (uint64_t)phys_div(y, q) + ws_ctx;
+            }
+            phys = (uint32_t)phys64;
         }
-        const uint32_t phys = (uint32_t)phys64;
         while (lnext < lend) {
-            const uint32_t m = __ballot_sync(FULL, valid && phys64 > G.level_mem[lnext]);
+            const bool over = W32 ? (valid && phys > (uint32_t)lvl) : (valid && phys64 > lvl);
+            const uint32_t m = __ballot_sync(FULL, over);
             if (!m) break;
             const uint32_t src = (uint32_t)__ffs(m) - 1u;
             const uint32_t pre = Smem + __reduce_add_sync(FULL, lane <= src ? phys : 0u);
@@ -176,22 +188,26 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
                     mfe[k] = pre;
                 }
             ++lnext;
+            lvl = lnext < lend ? G.level_mem[lnext] : ~0ull;
         }
         Smem += __reduce_add_sync(FULL, phys);
-    }
+    };
+    // full chunks need no per-lane bound test; the last (partial) chunk does
+    for (; base + 32 <= T; base += 32) chunk(false);
+    if (base < T) chunk(true);
 }
 
 // Whole-warp estimation of one DYNAMIC job (lanes over iterations).
 // PLAIN: generated samples and no EWMA variant (the common case), so those paths compile out.
 template <bool PLAIN>
-__device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t trace_id, uint32_t jidx, uint4 r,
+__device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t trace_key, uint32_t jidx, uint4 r,
                                  uint4 e, uint32_t lane, mig_job_estimate* dst, const uint2* rec_samples,
                                  uint32_t rec_count) {
     if (PLAIN) rec_samples = nullptr;
     const bool ewma = !PLAIN && P.ewma != 0;
     const uint32_t T = r.z & 0xFFFFu;
     const uint32_t b = r.x, q0 = r.y, ws = e.x, slope = e.z, sigma_n = e.w & 0xFFFFu, qs = e.w >> 16;
-    const uint64_t key = tg_key(P.seed, trace_id, jidx);
+    const uint64_t key = tg_job_key(trace_key, jidx);  // = tg_key(seed, trace, jidx)
     const int64_t ws_ctx = (int64_t)ws + P.ctx;
     uint32_t fe[5] = {kNever, kNever, kNever, kNever, kNever};
     uint32_t mfe[5] = {0u, 0u, 0u, 0u, 0u};  // physical MiB summed over iterations 1..fe[l]
@@ -231,8 +247,10 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
                 const uint2 v = __ldg(rec_samples + (n <= rec_count ? n : rec_count) - 1);  // short series: flagged
                 y = v.x;
                 q = v.y;
-            } else {
+            } else if (check) {
                 tg_dyn_sample(key, n, b, slope, sigma_n, q0, qs, &y, &q);
+            } else {  // the series' bounds keep the draw in 32-bit range (y_hi < 2^18)
+                tg_dyn_sample_fast(key, n, b, slope, sigma_n, q0, qs, &y, &q);
             }
             if (check) bad |= (q == 0) | (y >= (1u << 18)) | (q >= (1u << 26));
         }
@@ -317,16 +335,22 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
         Smem = Snext;
     }
+    // W32: every physical MiB of the tail is below 2^32 (generated in-range series, ws + ctx < 2^31)
+    const bool w32 = !check && ws_ctx < (1ll << 31);
     if (q_unit) {
-        if (check) scan_tail<true, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
-                                         ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
-        else scan_tail<false, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
-                                    ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
-    } else {  // (q0 < 1.0 takes the checked path: its per-sample checks never fire, its division is exact for any q)
-        if (fastq) scan_tail<false, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+        if (check) scan_tail<true, true, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0,
+                                                qs, ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+        else if (w32) scan_tail<false, true, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n,
+                                                   q0, qs, ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+        else scan_tail<false, true, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
                                            ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
-        else scan_tail<true, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
-                                    ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+    } else {  // (q0 < 1.0 takes the checked path: its per-sample checks never fire, its division is exact for any q)
+        if (fastq && w32) scan_tail<false, false, true>(G, rec_samples, rec_count, base, T, lane, key, b, slope,
+                                                        sigma_n, q0, qs, ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+        else if (fastq) scan_tail<false, false, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope,
+                                                       sigma_n, q0, qs, ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
+        else scan_tail<true, false, false>(G, rec_samples, rec_count, base, T, lane, key, b, slope, sigma_n, q0, qs,
+                                           ws_ctx, phys_hi, lnext, Smem, bad, fe, mfe);
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, (unsigned long long)MIG_ERR_BAD_RECORD);
     if (lane == 0) store_estimate(dst, G.mem[0], pred, conv, G.n_levels, fe, phi, a, sig, mfe, mconv, Smem);
@@ -341,10 +365,14 @@ constexpr uint32_t kEstBatch = 32;
 // config 3 / 4 / 5 k_estimate 11.46 / 85.8 / 162.0 ms at 3 CTAs, 10.75 / 82.1 / 152.9 at 4, 10.72 / 81.5 / 150.3 at
 // 5, 10.81 / 81.1 / 149.6 at 6: the per-sample loop is latency-bound (RNG chain, ballots, reductions), so more
 // resident warps beat a few spilled registers
+#ifndef EST_MINB
+#define EST_MINB 5
+#endif
 template <bool PLAIN>
-__global__ void __launch_bounds__(256, 5) k_estimate(const DevGeom G, const EstParams P) {
+__global__ void __launch_bounds__(256, EST_MINB) k_estimate(const DevGeom G, const EstParams P) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t j_base = P.off[0];
+    __shared__ uint64_t s_tkey[8][32];
     for (;;) {
         unsigned long long t0 = 0;
         if (lane == 0) t0 = atomicAdd(P.counter, (unsigned long long)kEstBatch);
@@ -352,6 +380,9 @@ __global__ void __launch_bounds__(256, 5) k_estimate(const DevGeom G, const EstP
         if (t0 >= P.n_traces) break;
         const uint32_t nb = (uint32_t)min((unsigned long long)kEstBatch, P.n_traces - t0);
         const uint64_t my_off = lane < nb ? P.off[t0 + lane] - j_base : ~0ull;  // first job of batch trace `lane`
+        // the sample-generator key of every batch trace (tracegen.h tg_trace_key), one per lane, in shared memory
+        s_tkey[threadIdx.x >> 5][lane] = tg_trace_key(P.seed, P.trace_id0 + t0 + lane);
+        __syncwarp();
         const uint64_t gend = P.off[t0 + nb] - j_base;
         const uint64_t gbeg = __shfl_sync(FULL, my_off, 0);
         for (uint64_t c = gbeg; c < gend; c += 32) {
@@ -423,7 +454,8 @@ __global__ void __launch_bounds__(256, 5) k_estimate(const DevGeom G, const EstP
                         if (rcount == 0) rs = nullptr;  // nothing recorded: fall back to the declared generator
                     }
                 }
-                estimate_dynamic<PLAIN>(G, P, P.trace_id0 + t0 + tb, jt, rr, ee, lane, P.out + gL, rs, rcount);
+                const uint64_t tkey = s_tkey[threadIdx.x >> 5][tb];
+                estimate_dynamic<PLAIN>(G, P, tkey, jt, rr, ee, lane, P.out + gL, rs, rcount);
             }
         }
     }

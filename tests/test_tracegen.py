@@ -64,3 +64,36 @@ def test_config_has_dynamic_table():
         jobs, _, _ = tg.generate_host(cfg, 3000, trace_id0=777)
         has = bool((((jobs[:, 2] >> 16) & 0xFF) == 2).any())
         assert has == tg.CONFIG_HAS_DYNAMIC[cfg], cfg
+
+
+def test_dyn_sample_noise_shape():
+    # the per-iteration draw (tg_iter_bits: two 32-bit counter hashes) gives Irwin-Hall(4) noise: symmetric, with
+    # the normal's central masses (68.3% within 1 sigma, 95.4% within 2; Irwin-Hall(4): 67.8% / 95.8%), and no
+    # lag-1 correlation between consecutive iterations
+    sig = 1000
+    job = np.array([100000, 65536, 20000 | (2 << 16), 10], np.uint32)
+    ext = np.array([0, 0, 0, sig], np.uint32)
+    y, _ = tg.dyn_samples(7, 11, 2, job, ext, 20000)
+    r = y.astype(np.float64) - 100000.5
+    s = r.std()
+    assert abs(r.mean()) < 4 * sig / np.sqrt(len(r)) and 0.97 * sig < s < 1.03 * sig
+    assert 0.66 < np.mean(np.abs(r) < s) < 0.70 and 0.945 < np.mean(np.abs(r) < 2 * s) < 0.965
+    assert abs(np.mean(r > 0) - 0.5) < 0.02
+    assert abs(np.corrcoef(r[:-1], r[1:])[0, 1]) < 0.03
+
+
+def test_dyn_sample_fast_equals_reference_in_range():
+    # tg_dyn_sample_fast (32-bit) == tg_dyn_sample under its bounds: b + slope*T/256 + 2^19 < 2^31, slope*T < 2^32,
+    # at the edges of the noise range (sigma up to 65535) and on the configs' own dynamic jobs
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        T = int(rng.integers(1, 4097))
+        slope = int(rng.integers(0, min(2**32 // T, 2**24)))
+        b = int(rng.integers(0, 2**30 - (slope * T >> 8)))
+        sig = int(rng.choice([0, 1, 100, 65535, int(rng.integers(0, 65536))]))
+        job = np.array([b, 65536, T | (2 << 16), 10], np.uint32)
+        ext = np.array([0, 0, slope, sig | (int(rng.integers(0, 64)) << 16)], np.uint32)
+        key_t, key_j = int(rng.integers(0, 2**40)), int(rng.integers(0, 50))
+        a = tg.dyn_samples(9, key_t, key_j, job, ext, T)
+        f = tg.dyn_samples(9, key_t, key_j, job, ext, T, fast=True)
+        assert np.array_equal(a[0], f[0]) and np.array_equal(a[1], f[1])

@@ -23,11 +23,12 @@ def main():
     os.makedirs(os.path.join(ROOT, "build/var"), exist_ok=True)
     for f in os.listdir(os.path.join(ROOT, "build/var")):
         os.remove(os.path.join(ROOT, "build/var", f))
-    others = [s for s in ge.MIG_SOURCES if not s.endswith("simulate_lane.cu")]
+    var_src = os.environ.get("VAR_SRC", "paper_2508_18556_b200/csrc/simulate_lane.cu")
+    others = [s for s in ge.MIG_SOURCES if s != var_src]
     variants = [a.split("=", 1) for a in sys.argv[1:]]
     with ThreadPoolExecutor(8) as ex:
         futs = [ex.submit(obj, s, f"build/obj/{os.path.basename(s)}.o") for s in others]
-        vfuts = [ex.submit(obj, "paper_2508_18556_b200/csrc/simulate_lane.cu", f"build/obj/lane_{n}.o", fl.split())
+        vfuts = [ex.submit(obj, var_src, f"build/obj/var_{n}.o", fl.split())
                  for n, fl in variants]
         objs = [f.result() for f in futs]
         vobjs = [f.result() for f in vfuts]

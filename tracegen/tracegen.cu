@@ -38,6 +38,14 @@ void tg_dyn_samples_host(uint64_t seed, uint64_t trace_id, uint32_t job_idx, con
         tg_dyn_sample(key, i, job[0], ext[2], ext[3] & 0xFFFFu, job[1], ext[3] >> 16, &y[i - 1], &q[i - 1]);
 }
 
+// The same through tg_dyn_sample_fast (tests: equality under its range bounds).
+void tg_dyn_samples_host_fast(uint64_t seed, uint64_t trace_id, uint32_t job_idx, const uint32_t* job,
+                              const uint32_t* ext, uint32_t T, uint32_t* y, uint32_t* q) {
+    uint64_t key = tg_key(seed, trace_id, job_idx);
+    for (uint32_t i = 1; i <= T; ++i)
+        tg_dyn_sample_fast(key, i, job[0], ext[2], ext[3] & 0xFFFFu, job[1], ext[3] >> 16, &y[i - 1], &q[i - 1]);
+}
+
 }  // extern "C"
 
 __global__ void tg_generate_kernel(uint32_t cfg, uint64_t seed, uint64_t trace_id0, uint64_t n, uint32_t J,

@@ -48,8 +48,10 @@ TG_HD uint64_t tg_mix64(uint64_t x) {
 }
 
 /* Counter-based stream key for (seed, trace, job). job = 0xFFFFFFFF names the trace-level stream. */
+TG_HD uint64_t tg_trace_key(uint64_t seed, uint64_t trace) { return tg_mix64(seed ^ tg_mix64(trace)); }
+TG_HD uint64_t tg_job_key(uint64_t trace_key, uint32_t job) { return tg_mix64(trace_key + (uint64_t)job * TG_GOLDEN); }
 TG_HD uint64_t tg_key(uint64_t seed, uint64_t trace, uint32_t job) {
-    return tg_mix64(tg_mix64(seed ^ tg_mix64(trace)) + (uint64_t)job * TG_GOLDEN);
+    return tg_job_key(tg_trace_key(seed, trace), job);
 }
 
 /* Draw number ctr of a stream. */
@@ -76,14 +78,47 @@ TG_HD int32_t tg_irwin_hall(uint64_t r, uint32_t sigma) {
     return (int32_t)(((int64_t)(s - 131070) * (int64_t)(int32_t)((sigma & 0xFFFFu) * 7094u)) >> 28);
 }
 
+/* 32-bit integer hash ("lowbias32", C. Wellons 2018: two multiplies, three xorshifts). */
+TG_HD uint32_t tg_hash32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+/* The 64 random bits of iteration i of a DYNAMIC job's sample stream: two 32-bit counter hashes keyed by the two
+ * halves of the job's splitmix64 key. The per-iteration draw is the hot part of generating a series in-kernel
+ * (SURVEY.md §8(d) budgets ~15 ops for RNG + Irwin-Hall per iteration); splitmix64's 64-bit multiplies cost ~30
+ * 32-bit instructions, these two hashes ~16. */
+TG_HD uint64_t tg_iter_bits(uint64_t job_key, uint32_t i) {
+    const uint32_t c = i * 0x9E3779B9u;
+    const uint32_t h1 = tg_hash32((uint32_t)job_key ^ c);
+    const uint32_t h2 = tg_hash32((uint32_t)(job_key >> 32) + c);
+    return ((uint64_t)h2 << 32) | h1;
+}
+
 /* Per-iteration sample i (1-based) of a DYNAMIC job: requested MiB y_i (allocator-rounded up to 2 MiB, >= 2) and
  * inverse reuse ratio q_i in Q16 (inv_reuse = 1/reuse_ratio >= 1). */
 TG_HD void tg_dyn_sample(uint64_t job_key, uint32_t i, uint32_t b_mib, uint32_t slope_q8, uint32_t sigma_mib,
                          uint32_t q0_q16, uint32_t qslope_q16, uint32_t* y, uint32_t* q) {
     int64_t v = (int64_t)b_mib + (int64_t)(((uint64_t)slope_q8 * i) >> 8) +
-                (int64_t)tg_irwin_hall(tg_draw(job_key, i), sigma_mib);
+                (int64_t)tg_irwin_hall(tg_iter_bits(job_key, i), sigma_mib);
     if (v < 2) v = 2;
     v = (v + 1) & ~(int64_t)1;
+    *y = (uint32_t)v;
+    *q = q0_q16 + qslope_q16 * i;
+}
+
+/* tg_dyn_sample in 32-bit arithmetic, for series whose bounds keep every intermediate in range: b + (slope_q8 * T
+ * >> 8) + 2^19 < 2^31 and slope_q8 * T < 2^32 (the Irwin-Hall noise is below 2^18 in magnitude). Equal to
+ * tg_dyn_sample for every i <= T under those bounds (tests/test_tracegen.py). */
+TG_HD void tg_dyn_sample_fast(uint64_t job_key, uint32_t i, uint32_t b_mib, uint32_t slope_q8, uint32_t sigma_mib,
+                              uint32_t q0_q16, uint32_t qslope_q16, uint32_t* y, uint32_t* q) {
+    int32_t v = (int32_t)(b_mib + ((slope_q8 * i) >> 8)) + tg_irwin_hall(tg_iter_bits(job_key, i), sigma_mib);
+    v = v < 2 ? 2 : v;
+    v = (v + 1) & ~1;
     *y = (uint32_t)v;
     *q = q0_q16 + qslope_q16 * i;
 }

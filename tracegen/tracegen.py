@@ -39,6 +39,7 @@ def lib():
                                        C.c_void_p]
         L.tg_dyn_samples_host.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
                                           C.c_void_p, C.c_void_p]
+        L.tg_dyn_samples_host_fast.argtypes = L.tg_dyn_samples_host.argtypes
         L.tg_generate_device.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
         _lib = L
@@ -99,13 +100,14 @@ def generate_device(cfg: int, n_traces: int, trace_id0: int = 0, seed: int | Non
     return jobs, ext, off
 
 
-def dyn_samples(seed: int, trace_id: int, job_idx: int, job, ext, T: int):
-    """Per-iteration samples (y MiB, q Q16), i = 1..T, of one dynamic job record."""
+def dyn_samples(seed: int, trace_id: int, job_idx: int, job, ext, T: int, fast=False):
+    """Per-iteration samples (y MiB, q Q16), i = 1..T, of one dynamic job record (fast: tg_dyn_sample_fast)."""
     job = np.ascontiguousarray(job, np.uint32)
     ext = np.ascontiguousarray(ext, np.uint32)
     y = np.zeros(T, np.uint32)
     q = np.zeros(T, np.uint32)
-    lib().tg_dyn_samples_host(seed, trace_id, job_idx, job.ctypes.data_as(C.c_void_p),
+    fn = lib().tg_dyn_samples_host_fast if fast else lib().tg_dyn_samples_host
+    fn(seed, trace_id, job_idx, job.ctypes.data_as(C.c_void_p),
                               ext.ctypes.data_as(C.c_void_p), T, y.ctypes.data_as(C.c_void_p),
                               q.ctypes.data_as(C.c_void_p))
     return y, q
