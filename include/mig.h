@@ -20,8 +20,11 @@
  *   - Ownership: the library never frees or retains caller memory beyond a call (device calls: beyond the
  *     stream-ordered work they enqueue). A mig_geometry owns its host tables and per-device copies.
  *   - Asynchrony: device entry points are stream-ordered; outputs are valid once the stream is synchronised.
- *     Internally mig_simulate may fork work onto a library-owned side stream; it joins back into the caller's
- *     stream by events before returning, so the call stays stream-ordered and can be captured in a CUDA graph.
+ *     Internally mig_simulate may fork work onto a library-owned side stream of the calling thread (one per thread
+ *     and device, so calls from different threads never share one); it joins back into the caller's stream by
+ *     events before returning, so the call stays stream-ordered and can be captured in a CUDA graph while other
+ *     threads keep calling the library. Device scratch comes from a pool private to the library
+ *     (mig_release_scratch).
  *   - Semantic outcomes (rejected or failed jobs) are counted in results, never reported as errors. Call errors
  *     are malformed arguments (MIG_E_INVALID_ARG), geometry problems (MIG_E_IO / PARSE / VALIDATION / CAPACITY),
  *     trace-format violations detected on the device (reported in mig_policy_totals.error_flags), and CUDA
@@ -223,6 +226,7 @@ typedef struct {             /* 96 B, one per (trace, policy)                   
 
 #define MIG_ERR_TRACE_TOO_LONG 1ull /* a trace has more than max_jobs jobs                             */
 #define MIG_ERR_BAD_RECORD 2ull     /* class > 2, iters > 4096, or a sample outside the predictor's range */
+#define MIG_ERR_TICK_OVERFLOW 4ull  /* a run's end tick exceeds 2^32 - 1 (ticks are u32; the trace's times wrapped) */
 
 typedef struct {             /* 192 B, one per policy: sums over traces (integer, exact in any order)     */
     uint64_t n_traces, n_jobs, completed, rejected, failed, ooms, preempts, restarts, placements, waits,
@@ -264,6 +268,13 @@ mig_status mig_debug_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* ou
 
 /* Number of kernel launches issued by the last device call on this thread (bench accounting). */
 uint32_t mig_last_launch_count(void);
+
+/* Device scratch (estimates of DYNAMIC jobs, requeue FIFOs, per-lane partial totals, host-pipeline chunks) comes
+ * from a memory pool private to the library, one per device, created on first use; it keeps its memory between
+ * calls (large per-call scratch is not re-mapped every call) and never changes the device's default pool.
+ * mig_release_scratch returns the unused part of every such pool to the device (call it after the streams that
+ * used the library are synchronised). MIG_E_CUDA on failure. */
+mig_status mig_release_scratch(void);
 
 /* Kernel timing (bench accounting). While enabled on a thread, every device call of that thread brackets its
  * kernel launches with CUDA events on the call's stream, grouped as "k_estimate" (the estimation kernel),

@@ -71,6 +71,7 @@ class mig_policy(C.Structure):
 
 _lib.mig_last_error.restype = C.c_char_p
 _lib.mig_last_launch_count.restype = C.c_uint32
+_lib.mig_release_scratch.restype = C.c_int
 _lib.mig_geometry_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
 _lib.mig_geometry_free.argtypes = [C.c_void_p]
 _lib.mig_geometry_query.argtypes = [C.c_void_p, C.POINTER(mig_geometry_info)]
@@ -95,6 +96,11 @@ def _check(status):
 
 def mig_last_launch_count() -> int:
     return int(_lib.mig_last_launch_count())
+
+
+def mig_release_scratch() -> None:
+    """Return the library's unused device scratch (its private pools) to the devices (include/mig.h)."""
+    _check(_lib.mig_release_scratch())
 
 
 class mig_kernel_time(C.Structure):

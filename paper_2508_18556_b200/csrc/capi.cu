@@ -78,16 +78,30 @@ int sm_count_of(int dev) {
     return cache[dev];
 }
 
-// Keep stream-ordered scratch in the device's default pool between calls (no release at synchronisation).
-void configure_pool(int dev) {
-    static bool done[64] = {false};
-    if (dev < 0 || dev >= 64 || done[dev]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+// The library's private scratch pool of a device, created on first use (release threshold: keep everything, the
+// pool is the library's own; mig_release_scratch trims it).
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+
+cudaError_t scratch_pool(int dev, cudaMemPool_t* out) {
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props;
+        memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p;
+        cudaError_t e = cudaMemPoolCreate(&p, &props);
+        if (e != cudaSuccess) return e;
         uint64_t thr = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+        g_pool[dev] = p;
     }
-    done[dev] = true;
+    *out = g_pool[dev];
+    return cudaSuccess;
 }
 
 mig_status device_geometry(const mig_geometry* gc, mig::DevGeom** out, int* dev_out) {
@@ -134,7 +148,6 @@ mig_status device_geometry(const mig_geometry* gc, mig::DevGeom** out, int* dev_
     }
     *out = g->dev[dev];
     *dev_out = dev;
-    configure_pool(dev);
     return MIG_OK;
 }
 
@@ -220,6 +233,17 @@ mig_status simulate_device(const mig_geometry* g, mig::DevGeom* Gdev, int dev, c
 
 }  // namespace
 
+cudaError_t mig_scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (e == cudaSuccess) e = scratch_pool(dev, &pool);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, s);
+    return e;
+}
+
+cudaError_t mig_scratch_free(void* p, cudaStream_t s) { return p ? cudaFreeAsync(p, s) : cudaSuccess; }
+
 mig_status mig_set_error(mig_status s, const std::string& msg) {
     t_err = msg;
     return s;
@@ -286,6 +310,16 @@ mig_status mig_workspace_bytes(const char* cfg, uint32_t n_layers, uint64_t* byt
 
 uint32_t mig_last_launch_count(void) { return t_launches; }
 
+mig_status mig_release_scratch(void) {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    for (int d = 0; d < 64; ++d) {
+        if (!g_pool[d]) continue;
+        cudaError_t e = cudaMemPoolTrimTo(g_pool[d], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "mig_release_scratch");
+    }
+    return MIG_OK;
+}
+
 }  // extern "C"
 
 int mig_timed(const char* name, mig_stream_t stream, const std::function<int(uint32_t*)>& f) {
@@ -345,14 +379,14 @@ mig_status mig_estimate_memory(const mig_geometry* g, const mig_traces* traces, 
     if (st != MIG_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, 2 * sizeof(unsigned long long), s);
+    cudaError_t e = mig_scratch_alloc((void**)&scratch, 2 * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scratch)");
     cudaMemsetAsync(scratch, 0, 2 * sizeof(unsigned long long), s);
     e = timed("k_estimate", s, [&](uint32_t* nl) {
         if (nl) *nl = 1;
         return mig::launch_estimate(g->dg, *traces, *policy, out, scratch, sm_count_of(dev), false, s);
     });
-    cudaFreeAsync(scratch, s);
+    mig_scratch_free(scratch, s);
     if (e != cudaSuccess) return cuda_fail(e, "k_estimate launch");
     t_launches = 1;
     return MIG_OK;
@@ -381,7 +415,7 @@ mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const m
                           mig::simulate_lane_path(g->dg.n_prof, g->sid_dev[dev], g->a7_dev[dev]);
     size_t est_bytes = (est || skip_est) ? 0 : traces->n_jobs * sizeof(mig_job_estimate);
     uint8_t* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, kCounterBytes + est_bytes, s);
+    cudaError_t e = mig_scratch_alloc((void**)&scratch, kCounterBytes + est_bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(scratch)");
     e = cudaMemsetAsync(scratch, 0, kCounterBytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(scratch)");
@@ -389,7 +423,7 @@ mig_status mig_simulate(const mig_geometry* g, const mig_traces* traces, const m
                          (est || !est_bytes) ? nullptr : reinterpret_cast<mig_job_estimate*>(scratch + kCounterBytes),
                          out, totals,
                          reinterpret_cast<unsigned long long*>(scratch), s);
-    cudaFreeAsync(scratch, s);
+    mig_scratch_free(scratch, s);
     return st;
 }
 
@@ -422,7 +456,7 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
                  rb = al(chunk_traces * n_policies * sizeof(mig_trace_result));
     const size_t ab = T.arrival ? al(chunk_jobs_cap * 4) : 0;  // arrival ticks (R40)
     const size_t per = jb + eb + ob + esb + rb + ab + kCounterBytes;
-    cudaStream_t ss[2];
+    cudaStream_t ss[2] = {nullptr, nullptr};
     uint8_t* buf[2] = {nullptr, nullptr};
     std::vector<mig_policy_totals> host_tot(n_chunks * n_policies);
     // per-chunk totals stay on the device until the end (a D2H into pageable memory per chunk would block the
@@ -430,10 +464,14 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
     mig_policy_totals* d_tot_all = nullptr;
     cudaError_t e = cudaMalloc(&d_tot_all, n_chunks * n_policies * sizeof(mig_policy_totals));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(totals)");
-    for (int k = 0; k < 2; ++k) {
-        if ((e = cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking)) != cudaSuccess)
-            return cuda_fail(e, "cudaStreamCreate");
-        if ((e = cudaMallocAsync(&buf[k], per, ss[k])) != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    for (int k = 0; k < 2 && st == MIG_OK; ++k) {  // every failure below goes through the one cleanup block
+        if ((e = cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking)) != cudaSuccess) {
+            ss[k] = nullptr;
+            st = cuda_fail(e, "cudaStreamCreate");
+        } else if ((e = mig_scratch_alloc((void**)&buf[k], per, ss[k])) != cudaSuccess) {
+            buf[k] = nullptr;
+            st = cuda_fail(e, "host pipeline scratch");
+        }
     }
     const uint64_t* off = T.trace_off;
     for (uint64_t c = 0; c < n_chunks && st == MIG_OK; ++c) {
@@ -466,8 +504,8 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         if (e == cudaSuccess && T.samples) {  // recorded samples of this chunk's jobs (stream-ordered scratch)
             const uint64_t* so = T.sample_off;
             const uint64_t slo = so[jlo] - so[0], shi = so[jhi] - so[0];
-            e = cudaMallocAsync(&d_smp, (shi - slo) * 8 + 8, s);
-            if (e == cudaSuccess) e = cudaMallocAsync(&d_soff, (nj + 1) * 8, s);
+            e = mig_scratch_alloc((void**)&d_smp, (shi - slo) * 8 + 8, s);
+            if (e == cudaSuccess) e = mig_scratch_alloc((void**)&d_soff, (nj + 1) * 8, s);
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(d_smp, (const uint8_t*)T.samples + slo * 8, (shi - slo) * 8, cudaMemcpyHostToDevice, s);
             if (e == cudaSuccess) e = cudaMemcpyAsync(d_soff, so + jlo, (nj + 1) * 8, cudaMemcpyHostToDevice, s);
@@ -490,16 +528,17 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
         ct.arrival = T.arrival ? d_arr : nullptr;
         st = simulate_device(g, Gdev, dev, ct, policies, n_policies, nullptr, d_est, out ? d_out : nullptr, d_tot, d_cnt,
                              s);  // no per-trace results wanted: none are written
-        if (d_smp) cudaFreeAsync(d_smp, s);
-        if (d_soff) cudaFreeAsync(d_soff, s);
+        if (d_smp) mig_scratch_free(d_smp, s);
+        if (d_soff) mig_scratch_free(d_soff, s);
         if (st != MIG_OK) break;
         if (out)
             e = cudaMemcpyAsync(out + t0 * n_policies, d_out, nt * n_policies * sizeof(mig_trace_result),
                                 cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) st = cuda_fail(e, "host pipeline D2H");
     }
-    for (int k = 0; k < 2; ++k) {
-        cudaFreeAsync(buf[k], ss[k]);
+    for (int k = 0; k < 2; ++k) {  // cleanup (every path): scratch, streams; the totals buffer below
+        if (!ss[k]) continue;
+        if (buf[k]) mig_scratch_free(buf[k], ss[k]);
         e = cudaStreamSynchronize(ss[k]);
         if (e != cudaSuccess && st == MIG_OK) st = cuda_fail(e, "host pipeline");
         cudaStreamDestroy(ss[k]);

@@ -65,6 +65,13 @@ struct mig_geometry {
     ~mig_geometry();
 };
 
+// Stream-ordered library scratch from a private memory pool per device (capi.cu): allocations persist in the pool
+// between calls (no re-mapping of large scratch every call) without changing the device's default pool, which
+// other users of the process share; mig_release_scratch() trims it.
+#include <cuda_runtime.h>
+cudaError_t mig_scratch_alloc(void** p, size_t bytes, cudaStream_t s);
+cudaError_t mig_scratch_free(void* p, cudaStream_t s);
+
 // error helpers (capi.cu)
 mig_status mig_set_error(mig_status s, const std::string& msg);
 void mig_note_launches(uint32_t n);

@@ -968,23 +968,34 @@ bool simulate_concurrent() {
     return on != 0;
 }
 
-// Up to `want` non-blocking side streams of device `dev` (created on first use, kept for the process).
+// Up to `want` non-blocking side streams of device `dev` for the calling thread (created on first use, kept for the
+// thread's lifetime). Per thread, so calls from different threads never share a side stream: no false dependency
+// between them through the join event, and a thread capturing mig_simulate into a CUDA graph pulls only its own side
+// stream into the capture.
+namespace {
+struct ThreadSideStreams {
+    cudaStream_t s[64][kMaxPolicies] = {};
+    uint32_t have[64] = {};
+    ~ThreadSideStreams() {
+        for (int d = 0; d < 64; ++d)
+            for (uint32_t i = 0; i < have[d]; ++i) cudaStreamDestroy(s[d][i]);  // errors at process exit ignored
+    }
+};
+thread_local ThreadSideStreams t_side;
+}  // namespace
+
 static uint32_t lane_side_streams(int dev, uint32_t want, cudaStream_t* out) {
-    static std::mutex mu;
-    static cudaStream_t streams[64][kMaxPolicies];
-    static uint32_t have[64];
     if (dev < 0 || dev >= 64) return 0;
     if (want > kMaxPolicies - 1) want = kMaxPolicies - 1;
-    std::lock_guard<std::mutex> lock(mu);
-    while (have[dev] < want) {
-        if (cudaStreamCreateWithFlags(&streams[dev][have[dev]], cudaStreamNonBlocking) != cudaSuccess) {
+    while (t_side.have[dev] < want) {
+        if (cudaStreamCreateWithFlags(&t_side.s[dev][t_side.have[dev]], cudaStreamNonBlocking) != cudaSuccess) {
             cudaGetLastError();
             break;
         }
-        ++have[dev];
+        ++t_side.have[dev];
     }
-    const uint32_t n = have[dev] < want ? have[dev] : want;
-    for (uint32_t i = 0; i < n; ++i) out[i] = streams[dev][i];
+    const uint32_t n = t_side.have[dev] < want ? t_side.have[dev] : want;
+    for (uint32_t i = 0; i < n; ++i) out[i] = t_side.s[dev][i];
     return n;
 }
 
@@ -1052,13 +1063,13 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
         const size_t ring_bytes = (ring_elems * sizeof(uint16_t) + 255) & ~(size_t)255;
         const size_t set_bytes = ring_bytes + part_elems * sizeof(unsigned long long);
         char* scr = nullptr;
-        e = cudaMallocAsync(&scr, n_scr * set_bytes, stream);
+        e = mig_scratch_alloc((void**)&scr, n_scr * set_bytes, stream);
         if (e != cudaSuccess) return e;
         uint4* pc = nullptr;
         if (any_pc) {
-            e = cudaMallocAsync(&pc, n_scr * pc_elems * sizeof(uint4), stream);
+            e = mig_scratch_alloc((void**)&pc, n_scr * pc_elems * sizeof(uint4), stream);
             if (e != cudaSuccess) {
-                cudaFreeAsync(scr, stream);
+                mig_scratch_free(scr, stream);
                 return e;
             }
         }
@@ -1094,8 +1105,8 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
             if (join[k]) cudaEventDestroy(join[k]);
         }
         if (fork) cudaEventDestroy(fork);
-        cudaFreeAsync(scr, stream);
-        if (pc) cudaFreeAsync(pc, stream);
+        mig_scratch_free(scr, stream);
+        if (pc) mig_scratch_free(pc, stream);
         return e;
     }
     for (uint32_t i = 0; i < n_pol; ++i)  // the group kernel has no contention model and no arrival streams
@@ -1106,7 +1117,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
         ++*launches;
     }
     if (PA.n_pol) {
-        if (P.n_pol) PA.est_err = nullptr;  // merged once
+        // est_err is OR-ed into every policy row of both launches (an OR is idempotent)
         e = launch_variant<true>(Gdev, PA, tr, sm_count, stream);
         if (e != cudaSuccess) return e;
         ++*launches;

@@ -82,6 +82,14 @@ constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
 // restarts and energy are linear in these (n - rejected - failed; ooms - failed + preempts; idle_w * makespan +
 // w_per_slice * busy) and are derived once per CTA.
 constexpr int kT32 = 12, kT64 = 6;
+// The per-trace counters are packed two per u32 (K0..K3: placements | creates, destroys | waits, rejected | ooms,
+// preempts | failed), so each must stay below 2^16. A job runs at most 1 + 2 * kMaxLevels times (every OOM restart
+// moves to a strictly larger memory level, R14; an early restart moves to a slice holding the converged forecast,
+// R25, where it cannot preempt again before an OOM moves it up), so placements <= jobs * (1 + 2 * kMaxLevels);
+// creates <= placements, destroys <= creates (only created instances are destroyed), and every WAIT is followed by
+// an event or an arrival before the head is evaluated again, so waits <= placements + jobs.
+static_assert((uint64_t)MIG_MAX_JOBS_PER_TRACE * (2 + 2 * kMaxLevels) < 65536,
+              "packed 16-bit per-trace counters could overflow");
 __constant__ const uint8_t kF32[kT32] = {0, 1, 3, 4, 5, 6, 8, 9, 10, 11, 13, 20};
 __constant__ const uint8_t kF64[kT64] = {12, 15, 16, 17, 18, 19};
 
@@ -406,6 +414,10 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             end = rs + T * ticks;
         }
         const uint32_t dur = end - rs;
+        {  // ticks are u32: flag a run whose end would not fit (the trace's times wrapped; mig.h)
+            const uint32_t it = ek == 1 ? fe : ek == 2 ? i_pre : T;
+            if (((uint64_t)it * ticks + rs) >> 32) err |= (uint32_t)MIG_ERR_TICK_OVERFLOW;
+        }
         if (EXT && pcie) {  // R39: the run's end follows its progress; power, memory and waste at its end
             const uint32_t it = ek == 1 ? fe : ek == 2 ? i_pre : T;
             const uint32_t mem =
@@ -1256,23 +1268,27 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 // start_run: end tick and kind (OOM > COMPLETE in one iteration, R29)
                 const uint32_t rs = t + (created ? reconfig : 0u);
                 const uint32_t lev = si & 0xFu, comp = (si >> 4) & 0xFu, T = hr.z & 0xFFFFu, ticks = hr.w;
-                uint32_t dur, ek;
+                uint32_t dur, ek, it;
                 if (((hr.z >> 16) & 0xFFu) != kClassDynamic) {
                     const uint32_t phys = hr.y + ctx < hr.y ? 0xFFFFFFFFu : hr.y + ctx;
                     ek = (T >= 1 && phys > S.level_mem[lev]) ? 1u : 0u;  // R12: static jobs OOM at iteration 1
-                    dur = (ek ? 1u : T) * ticks;
+                    it = ek ? 1u : T;
+                    dur = it * ticks;
                     a_mem += (uint64_t)phys * dur;
                 } else if (P.est) {
                     const mig_job_estimate* ej = P.est + j0 + j;
                     const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
                     ek = fe <= T ? 1u : 0u;
-                    dur = (ek ? fe : T) * ticks;
+                    it = ek ? fe : T;
+                    dur = it * ticks;
                     a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? lev : 6u)) * ticks;
                 } else {  // a DYNAMIC record under MIG_TRACES_NO_DYNAMIC (no estimates): flagged, no forecast
                     err |= (uint32_t)MIG_ERR_BAD_RECORD;
                     ek = 0;
+                    it = T;
                     dur = T * ticks;
                 }
+                if (((uint64_t)it * ticks + rs) >> 32) err |= (uint32_t)MIG_ERR_TICK_OVERFLOW;  // u32 ticks (mig.h)
                 a_busy += (uint64_t)comp * dur;
                 if (ek) a_waste += dur;
                 const unsigned long long kk = ((unsigned long long)(rs + dur) << 32) | (((j | (ek << 16)) << 3) | s);
@@ -1453,23 +1469,27 @@ __global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const Dev
                     ++placements;
                     // start_run on the whole GPU (OOM > COMPLETE in one iteration, R29)
                     const uint32_t ticks = r.w;
-                    uint32_t dur, ek;
+                    uint32_t dur, ek, it;
                     if (cls != kClassDynamic) {
                         const uint32_t phys = r.y + ctx < r.y ? 0xFFFFFFFFu : r.y + ctx;
                         ek = (T >= 1 && phys > fcap) ? 1u : 0u;  // R12: static jobs OOM at iteration 1
-                        dur = (ek ? 1u : T) * ticks;
+                        it = ek ? 1u : T;
+                        dur = it * ticks;
                         a_mem += (uint64_t)phys * dur;
                     } else if (P.est) {
                         const mig_job_estimate* ej = P.est + j0 + j;
                         const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + flev);
                         ek = fe <= T ? 1u : 0u;
-                        dur = (ek ? fe : T) * ticks;
+                        it = ek ? fe : T;
+                        dur = it * ticks;
                         a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? flev : 6u)) * ticks;
                     } else {  // DYNAMIC under MIG_TRACES_NO_DYNAMIC: flagged, no forecast
                         err |= (uint32_t)MIG_ERR_BAD_RECORD;
                         ek = 0;
+                        it = T;
                         dur = T * ticks;
                     }
+                    if (((uint64_t)it * ticks + t) >> 32) err |= (uint32_t)MIG_ERR_TICK_OVERFLOW;  // u32 ticks
                     a_busy += (uint64_t)fcomp * dur;
                     if (ek) a_waste += dur;
                     bend = t + dur;

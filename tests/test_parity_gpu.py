@@ -448,3 +448,48 @@ def test_no_dynamic_flag_skips_estimator_same_results():
     _, tot3 = mig.mig_simulate(g3, tr3, [mig.policy(g3, **s) for s in SPECS])
     t3 = mig.totals_numpy(tot3)
     assert ((t3["error_flags"] & 2) != 0).all()
+
+
+def test_tick_overflow_flagged():
+    # ticks are u32 (include/mig.h): a run whose end does not fit is flagged MIG_ERR_TICK_OVERFLOW in every policy's
+    # totals (lane kernels: generic, FUSION_FISSION fast case, BASELINE fold); an in-range trace is not
+    big = [tg.pack_job(1000, 1000, 4, 0, 1 << 31)]
+    ok = [tg.pack_job(1000, 1000, 4, 0, 1000)]
+    g = mig.mig_geometry_load("builtin:a100-40gb")
+    for jobs_list, want in [(big, 4), (ok, 0)]:
+        jobs, ext, off = tg.pack_traces([jobs_list])
+        tr = mig.traces_from_numpy(jobs, None, off)
+        _, tot = mig.mig_simulate(g, tr, [mig.policy(g, **s) for s in SPECS])
+        flags = mig.totals_numpy(tot)["error_flags"]
+        assert ((flags & 4) == want).all(), flags
+
+
+def test_threads_and_scratch_release():
+    # calls from two host threads on their own streams (each thread has its own library side stream) give the
+    # single-threaded results; mig_release_scratch trims the library's private pool afterwards
+    import threading
+
+    cfg, n = 2, 2000
+    jobs, ext, off = tg.generate_host(cfg, n)
+    g = mig.mig_geometry_load("builtin:a100-40gb")
+    pols = [mig.policy(g, **s) for s in SPECS]
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=tg.seed_of(cfg))
+    ref, rtot = mig.mig_simulate(g, tr, pols)
+    torch.cuda.synchronize()
+    outs = [None, None]
+
+    def work(k):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                outs[k] = mig.mig_simulate(g, tr, pols, stream=s)
+        s.synchronize()
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for res, tot in outs:
+        assert torch.equal(res, ref) and torch.equal(tot, rtot)
+    mig.mig_release_scratch()
