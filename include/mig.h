@@ -266,6 +266,27 @@ mig_status mig_workspace_bytes(const char* cublas_workspace_config, uint32_t n_l
  * failure. */
 mig_status mig_debug_phys_div(const uint32_t* y, const uint32_t* q, uint32_t* out, uint64_t n, void* stream);
 
+/* ------------------------------------------------------------------------------------------------------------------
+ * Alg. 1 on the device for larger slot geometries
+ * precompute_reachability (PAPER.md:459-474; "can be precomputed offline", :492) for an n_slots-slot GPU,
+ * 1 <= n_slots <= 24 (the loaded geometries have <= 8 slots and are tabled on the host). placement_masks: HOST
+ * array of the n_placements legal placements (bit i = memory slot i; 1..1024, each non-empty and inside the slots;
+ * two profiles may share a mask, e.g. 3g.20gb@0 and 4g.20gb@0). A partition state is a set of disjoint placements;
+ * it is final when no placement fits in its free slots (R2); its fcr is the number of distinct final states that
+ * adding placements can reach, which depends only on its occupancy (R3). fcr: DEVICE u32[2^n_slots], fcr[m] of
+ * every state with occupancy m (0 where no state has occupancy m); state_flags: DEVICE u8[2^n_slots] (bit 0 = some
+ * state has occupancy m, bit 1 = final) or NULL; info: HOST, filled when the call returns (it synchronises
+ * `stream`) with |S| (states), |F| (finals) and fcr(s0) = |F|. Compute slices are not modelled: in the MIG tables
+ * a profile's compute slices lie inside its memory range, so disjoint memory implies disjoint compute (R1).
+ * Work: 3^n_slots submask visits. MIG_E_INVALID_ARG on bad sizes or masks, MIG_E_CAPACITY when a count exceeds
+ * 2^32 - 1, MIG_E_CUDA on a CUDA failure.
+ * ---------------------------------------------------------------------------------------------------------------- */
+typedef struct {
+    uint64_t n_states, n_finals, fcr_s0;
+} mig_reach_info;
+mig_status mig_reachability(uint32_t n_slots, const uint32_t* placement_masks, uint32_t n_placements, uint32_t* fcr,
+                            uint8_t* state_flags, mig_reach_info* info, void* stream);
+
 /* Number of kernel launches issued by the last device call on this thread (bench accounting). */
 uint32_t mig_last_launch_count(void);
 

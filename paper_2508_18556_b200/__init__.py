@@ -98,6 +98,29 @@ def mig_last_launch_count() -> int:
     return int(_lib.mig_last_launch_count())
 
 
+class mig_reach_info(C.Structure):
+    _fields_ = [("n_states", C.c_uint64), ("n_finals", C.c_uint64), ("fcr_s0", C.c_uint64)]
+
+
+_lib.mig_reachability.argtypes = [C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
+                                  C.POINTER(mig_reach_info), C.c_void_p]
+
+
+def mig_reachability(n_slots: int, placement_masks, flags=True, stream=None):
+    """Alg. 1 on the device (include/mig.h mig_reachability): returns (fcr uint32 CUDA tensor [2^n_slots],
+    state flags uint8 CUDA tensor or None, info dict)."""
+    import torch
+
+    masks = np.ascontiguousarray(placement_masks, np.uint32)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    fcr = torch.empty(1 << n_slots, dtype=torch.int32, device=dev)
+    fl = torch.empty(1 << n_slots, dtype=torch.uint8, device=dev) if flags else None
+    info = mig_reach_info()
+    _check(_lib.mig_reachability(n_slots, masks.ctypes.data, len(masks), C.c_void_p(fcr.data_ptr()),
+                                 None if fl is None else C.c_void_p(fl.data_ptr()), C.byref(info), _stream_ptr(stream)))
+    return fcr, fl, {"n_states": info.n_states, "n_finals": info.n_finals, "fcr_s0": info.fcr_s0}
+
+
 def mig_release_scratch() -> None:
     """Return the library's unused device scratch (its private pools) to the devices (include/mig.h)."""
     _check(_lib.mig_release_scratch())

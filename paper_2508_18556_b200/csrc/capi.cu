@@ -250,6 +250,7 @@ mig_status mig_set_error(mig_status s, const std::string& msg) {
 }
 
 void mig_note_launches(uint32_t n) { t_launches += n; }
+void mig_set_launches(uint32_t n) { t_launches = n; }
 
 mig_geometry::~mig_geometry() {
     for (int d = 0; d < 64; ++d)

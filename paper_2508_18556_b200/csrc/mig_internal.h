@@ -75,6 +75,7 @@ cudaError_t mig_scratch_free(void* p, cudaStream_t s);
 // error helpers (capi.cu)
 mig_status mig_set_error(mig_status s, const std::string& msg);
 void mig_note_launches(uint32_t n);
+void mig_set_launches(uint32_t n);
 
 // mig_timing_enable support (capi.cu): when timing is on for this thread, records events on `stream` around the
 // launches issued by f (f returns a cudaError_t and the number of launches through its argument) under `name`.

@@ -134,3 +134,28 @@ class Replay:
             assert not (sl & used)
             used |= sl
         assert sum(self.mem[pp] for pp, _ in self.inst.values()) <= self.spec["total_memory_slots"] * self.spec["slot_mib"]
+
+
+def reach_counts(n_slots, masks):
+    """Alg. 1 by definition on occupancy masks (pure Python): D[t] = number of distinct sets of
+    disjoint placements with union t (by brute-force recursion on the lowest occupied slot), finals = states where
+    no placement fits, fcr[m] = number of distinct final placement sets reachable from a state with occupancy m
+    (sum of D[t] over t in the free slots of m with m | t final). Returns (|S|, |F|, fcr list)."""
+    N = 1 << n_slots
+    D = [0] * N
+    D[0] = 1
+    for t in range(1, N):
+        low = t & -t
+        D[t] = sum(D[t ^ q] for q in masks if (q & low) and (q & ~t) == 0)
+    final = [D[m] > 0 and all(q & m for q in masks) for m in range(N)]
+    fcr = [0] * N
+    for m in range(N):
+        if D[m]:
+            free = (N - 1) & ~m
+            fcr[m] = sum(D[t] for t in range(N) if (t & ~free) == 0 and final[m | t])
+    return sum(D), sum(D[m] for m in range(N) if final[m]), fcr
+
+
+def geometry_masks(spec):
+    """Placement masks (bit i = memory slot i) of a geometry JSON spec."""
+    return [((1 << prof["memory_slots"]) - 1) << s for prof in spec["profiles"] for s in prof["starts"]]

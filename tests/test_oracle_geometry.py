@@ -234,3 +234,28 @@ def test_geometry_validation_errors():
     bad["profiles"][1]["starts"] = [7]  # 2-slot profile starting at slot 7 of 8
     with pytest.raises(ValueError):
         orc.Geometry(bad)
+
+
+def test_reach_counts_reference_pins():
+    # the brute-force Alg. 1 on occupancy masks (tests/bruteforce.py reach_counts, the reference of the device
+    # mig_reachability) reproduces the instance-set enumeration's |S| / |F| and Appendix A on the vendor tables
+    import bruteforce as bf
+
+    for name, nS, nF in [("a30-24gb", 26, 5), ("a100-40gb", 298, 19), ("a100-40gb-1g10", 723, 78)]:
+        spec = json.load(open(geom_path(name)))
+        S, F, fcr = bf.reach_counts(spec["total_memory_slots"], bf.geometry_masks(spec))
+        assert (S, F, fcr[0]) == (nS, nF, nF), name
+    spec = json.load(open(geom_path("a100-40gb")))
+    _, _, fcr = bf.reach_counts(8, bf.geometry_masks(spec))
+    for line in open(os.path.join(GOLDEN_DIR, "a100_fcr_table.txt")):
+        if line.startswith("#"):
+            continue
+        for tok in line.split():
+            if ":" in tok:
+                k, v = tok.split(":")
+                assert fcr[int(k, 16)] == int(v), tok
+    # binary-aligned slots (lengths 1, 2, 4, ..., n at aligned starts): |S| = f(n) = f(n/2)^2 + 1, f(1) = 2 and
+    # |F| = g(n) = g(n/2)^2 + 1, g(1) = 1 (a block is one instance, or two independent halves)
+    masks = [((1 << L) - 1) << s for L in (1, 2, 4, 8) for s in range(0, 8, L)]
+    S, F, fcr = bf.reach_counts(8, masks)
+    assert (S, F, fcr[0], fcr[255]) == (677, 26, 26, 1)
