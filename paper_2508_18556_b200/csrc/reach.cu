@@ -188,7 +188,7 @@ extern "C" mig_status mig_reachability(uint32_t n_slots, const uint32_t* placeme
     const size_t b_off = al((n_slots + 1) * 4), b_masks = al(n_placements * 4), b_stats = al(4 * 8),
                  b_flags = state_flags ? 0 : al(N), b_heavy = al(N * 4), b_D = al(N * 4);
     uint8_t* scr = nullptr;
-    cudaError_t e = mig_scratch_alloc((void**)&scr, b_off + b_masks + b_stats + b_flags + b_heavy, s);
+    cudaError_t e = mig_scratch_alloc((void**)&scr, b_off + b_masks + b_stats + b_flags + b_heavy + b_D, s);
     if (e != cudaSuccess) return mig_set_error(MIG_E_CUDA, std::string("mig_reachability scratch: ") + cudaGetErrorString(e));
     ReachParams P;
     P.n_slots = n_slots;
