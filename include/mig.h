@@ -259,6 +259,18 @@ mig_status mig_simulate_host(const mig_geometry* g, const mig_traces* traces, co
  * (SPEC.md:228-236). Host only. MIG_E_PARSE on a malformed string. */
 mig_status mig_workspace_bytes(const char* cublas_workspace_config, uint32_t n_layers, uint64_t* bytes);
 
+/* Recorded per-iteration samples of one job (the predictor on recorded traces; the samples
+ * Alg. 3 appends each iteration) from a CSV trace file in SPEC.md's format: header
+ * `iteration,requested_bytes,reuse_ratio`, one row per iteration, iterations 1, 2, 3, ... in order. Each row becomes
+ * one mig_traces sample {req_mib, inv_reuse_q16}: req_mib = ceil(requested_bytes / 2^20) (the requested memory in
+ * MiB, R35), inv_reuse_q16 = round(65536 / reuse_ratio) (the inverse reuse ratio in Q16, R22: physical = requested
+ * / inverse reuse, so a reuse_ratio in (0, 1] gives inv_reuse >= 1.0). Host only. samples: HOST u32[2 * cap]
+ * ({req_mib, inv_reuse_q16} per sample) or NULL to count; *n_out = the number of rows (the samples written when
+ * n_out <= cap). MIG_E_IO if the file cannot be read; MIG_E_PARSE (message: line number) on a bad header or row, an
+ * iteration out of order, requested_bytes >= 2^52, a reuse_ratio not in (2^-10, 2^10) or a value beyond u32;
+ * MIG_E_CAPACITY when samples != NULL and the file has more than cap rows. */
+mig_status mig_samples_load_csv(const char* path, uint32_t* samples, uint64_t cap, uint64_t* n_out);
+
 /* Test hook (DEVICE buffers, stream-ordered): out[i] = floor(y[i] * 2^16 / q[i]) computed the way k_estimate maps a
  * requested MiB to physical MiB under inverse reuse q (reading R22) on its fast path: a float estimate corrected
  * by one integer remainder test. Defined for y < 2^18 and 2^16 <= q < 2^26 (the estimator's in-range inputs);

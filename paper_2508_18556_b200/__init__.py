@@ -356,3 +356,29 @@ def mig_workspace_bytes(cublas_workspace_config: str, n_layers: int = 1) -> int:
 
 
 _lib.mig_workspace_bytes.argtypes = [C.c_char_p, C.c_uint32, C.POINTER(C.c_uint64)]
+_lib.mig_samples_load_csv.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+
+
+def mig_samples_load_csv(path: str):
+    """One job's recorded per-iteration samples from a CSV trace file (include/mig.h): uint32 [n, 2] rows
+    {req_mib, inv_reuse_q16}, the mig_traces.samples format."""
+    n = C.c_uint64()
+    _check(_lib.mig_samples_load_csv(str(path).encode(), None, 0, C.byref(n)))
+    out = np.zeros((max(n.value, 1), 2), np.uint32)
+    _check(_lib.mig_samples_load_csv(str(path).encode(), out.ctypes.data, n.value, C.byref(n)))
+    return out[: n.value]
+
+
+def samples_from_series(jobs, series):
+    """Assemble mig_traces.samples / sample_off (host arrays) from per-job recorded series: series[k] = uint32
+    [n_k, 2] samples of job k, or None for a job without samples. Argument marshalling only."""
+    off = [0]
+    parts = []
+    for k in range(len(jobs)):
+        s = series[k] if k < len(series) else None
+        n = 0 if s is None else len(s)
+        if n:
+            parts.append(np.ascontiguousarray(s, np.uint32).reshape(-1, 2))
+        off.append(off[-1] + n)
+    smp = np.concatenate(parts) if parts else np.zeros((1, 2), np.uint32)
+    return smp, np.array(off, np.uint64)

@@ -1,8 +1,11 @@
 // capi.cu — the extern "C" entry points of libmig.so (include/mig.h): argument validation, per-device geometry
 // upload, stream-ordered scratch, kernel launches, and the host-buffer pipeline of mig_simulate_host.
+#include <errno.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+
+#include <cmath>
 
 #include <algorithm>
 #include <vector>
@@ -310,6 +313,55 @@ mig_status mig_workspace_bytes(const char* cfg, uint32_t n_layers, uint64_t* byt
 }
 
 uint32_t mig_last_launch_count(void) { return t_launches; }
+
+mig_status mig_samples_load_csv(const char* path, uint32_t* samples, uint64_t cap, uint64_t* n_out) {
+    if (!path || !n_out) return mig_set_error(MIG_E_INVALID_ARG, "mig_samples_load_csv: null argument");
+    FILE* f = fopen(path, "r");
+    if (!f) return mig_set_error(MIG_E_IO, std::string("mig_samples_load_csv: cannot open ") + path);
+    char line[512];
+    uint64_t n = 0, lineno = 1;
+    mig_status st = MIG_OK;
+    auto bad = [&](const char* why) {
+        st = mig_set_error(MIG_E_PARSE, std::string(path) + ":" + std::to_string(lineno) + ": " + why);
+    };
+    if (!fgets(line, sizeof(line), f)) {
+        bad("empty file (expected the header iteration,requested_bytes,reuse_ratio)");
+    } else {
+        std::string h(line);
+        while (!h.empty() && (h.back() == '\n' || h.back() == '\r' || h.back() == ' ')) h.pop_back();
+        if (h != "iteration,requested_bytes,reuse_ratio") bad("header must be iteration,requested_bytes,reuse_ratio");
+    }
+    while (st == MIG_OK && fgets(line, sizeof(line), f)) {
+        ++lineno;
+        char* p = line;
+        while (*p == ' ' || *p == '\t') ++p;
+        if (*p == '\n' || *p == '\r' || *p == 0) continue;  // blank line
+        char* e = nullptr;
+        errno = 0;
+        const unsigned long long it = strtoull(p, &e, 10);
+        if (e == p || *e != ',' || errno) { bad("bad iteration"); break; }
+        if (it != n + 1) { bad("iterations must be 1, 2, 3, ... in order"); break; }
+        p = e + 1;
+        const double bytes = strtod(p, &e);
+        if (e == p || *e != ',' || !(bytes >= 0.0) || bytes >= 4503599627370496.0) { bad("bad requested_bytes"); break; }
+        p = e + 1;
+        const double r = strtod(p, &e);
+        while (*e == ' ' || *e == '\r' || *e == '\n') ++e;
+        if (e == p || *e != 0 || !(r > 1.0 / 1024.0 && r < 1024.0)) { bad("bad reuse_ratio"); break; }
+        const double mib = std::ceil(bytes / 1048576.0), q = std::nearbyint(65536.0 / r);
+        if (mib > 4294967295.0 || q > 4294967295.0) { bad("value beyond u32"); break; }
+        if (samples && n < cap) {
+            samples[2 * n] = (uint32_t)mib;
+            samples[2 * n + 1] = (uint32_t)q;
+        }
+        ++n;
+    }
+    fclose(f);
+    if (st != MIG_OK) return st;
+    *n_out = n;
+    if (samples && n > cap) return mig_set_error(MIG_E_CAPACITY, "mig_samples_load_csv: more rows than cap");
+    return MIG_OK;
+}
 
 mig_status mig_release_scratch(void) {
     std::lock_guard<std::mutex> lock(g_pool_mu);

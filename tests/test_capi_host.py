@@ -183,3 +183,22 @@ def test_c_example_reproduces_example_w(tmp_path):
     assert got["BASELINE"][2] == "450" and got["STATIC"][2] == "210"
     assert got["DYNAMIC"][2] == "220" and got["FUSION_FISSION"][2] == "220"
     assert got["FUSION_FISSION"][12] == "27100" and got["BASELINE"][12] == "58500"
+
+
+def test_samples_load_csv(tmp_path):
+    # the recorded-trace loader (include/mig.h mig_samples_load_csv, SPEC.md S:260 format): bytes -> MiB rounded up,
+    # reuse_ratio -> inverse reuse in Q16 (round(65536 / r)); iterations must be 1, 2, 3, ...
+    import paper_2508_18556_b200 as mig
+
+    p = tmp_path / "job.csv"
+    p.write_text("iteration,requested_bytes,reuse_ratio\n1,1048576,1.0\n2,1048577,0.5\n3,3145728,0.8\n\n")
+    s = mig.mig_samples_load_csv(str(p))
+    assert s.tolist() == [[1, 65536], [2, 131072], [3, 81920]]
+    for body, why in [("iteration,bytes,reuse_ratio\n1,1,1\n", "header"), ("iteration,requested_bytes,reuse_ratio\n2,1,1\n", "order"),
+                      ("iteration,requested_bytes,reuse_ratio\n1,x,1\n", "requested_bytes"),
+                      ("iteration,requested_bytes,reuse_ratio\n1,1,0\n", "reuse_ratio")]:
+        p.write_text(body)
+        with pytest.raises(mig.MigError, match="MIG_E_PARSE"):
+            mig.mig_samples_load_csv(str(p))
+    with pytest.raises(mig.MigError, match="MIG_E_IO"):
+        mig.mig_samples_load_csv(str(tmp_path / "missing.csv"))

@@ -493,3 +493,34 @@ def test_threads_and_scratch_release():
     for res, tot in outs:
         assert torch.equal(res, ref) and torch.equal(tot, rtot)
     mig.mig_release_scratch()
+
+
+def test_recorded_trace_files(tmp_path):
+    # the predictor and scheduler on recorded traces read from CSV trace files (SPEC.md S:260 format, loaded by
+    # mig_samples_load_csv): every DYNAMIC job's series written as bytes and reuse ratios, read back, assembled into
+    # mig_traces.samples, and simulated; identical to the oracle on the same recorded samples
+    cfg, n = 3, 120
+    jobs, ext, off = tg.generate_host(cfg, n)
+    seed = tg.seed_of(cfg)
+    smp, soff = tg.explicit_samples(jobs, ext, off, seed)
+    series = []
+    for j in range(len(jobs)):
+        a, b = int(soff[j]), int(soff[j + 1])
+        if b == a:
+            series.append(None)
+            continue
+        p = tmp_path / f"job{j}.csv"
+        rows = ["iteration,requested_bytes,reuse_ratio"]
+        rows += [f"{i + 1},{int(y) * 1048576},{65536.0 / int(q)!r}" for i, (y, q) in enumerate(smp[a:b])]
+        p.write_text("\n".join(rows) + "\n")
+        series.append(mig.mig_samples_load_csv(str(p)))
+    smp2, soff2 = mig.samples_from_series(jobs, series)
+    assert np.array_equal(soff2, soff) and np.array_equal(smp2, smp[: len(smp2)])
+    geo = tg.CONFIG_GEOMETRY[cfg]
+    g = mig.mig_geometry_load(f"builtin:{geo}")
+    og = orc.Geometry(geom_path(geo))
+    tr = mig.traces_from_numpy(jobs, ext, off, seed=1, samples=smp2, sample_off=soff2)
+    pols = [mig.policy(g, **s) for s in SPECS]
+    res, _ = mig.mig_simulate(g, tr, pols)
+    want = orc.simulate(og, jobs, ext, off, [orc.policy(**s) for s in SPECS], seed=1, samples=smp2, sample_off=soff2)
+    assert_same(mig.results_numpy(res, len(pols)), want)
