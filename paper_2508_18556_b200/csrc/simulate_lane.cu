@@ -1188,11 +1188,14 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
         }
         __syncwarp();
         // ---- PASS: evaluate the head of the queue (Alg. 4, one decision) ----
-        // P1 decides (kd, s, pr, nd); the warp reconverges; P2 records, creates and starts the run, and pops, so
-        // every decision kind shares one copy of P2
+        // P1 decides (kd, s, pr, nd) without branches on the common paths: the reuse candidates, the Alg. 2 answer and
+        // the fusion/fission candidates are all looked up, then selected (REUSE before ALLOC before A7 before WAIT);
+        // only the rare A7 table probe and the first evaluation of a job branch. The warp reconverges; P2 records,
+        // creates, starts the run and pops, one copy for every decision kind.
         if (mode == 0 && hj == kNoJob) mode = 1;
         const bool pass = mode == 0;
         uint32_t kd = 0, s = 0, pr = 0, nd = 0;
+        bool a7try = false;
         if (pass) {
             if (hneed == kUnk) {  // first evaluation of an initial queue entry: record checks + tight fit
                 const uint32_t cls = (hr.z >> 16) & 0xFFu, T = hr.z & 0xFFFFu;
@@ -1200,59 +1203,50 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 hneed = FF_FIT_S(cls == kClassDynamic ? S.mem0 : hr.x + ctx);  // R16 / est + ctx (a2)
             }
             const uint32_t need = hneed;
-            pr = need;
-            if (need == kNoNeed) {  // no profile can ever hold the job: REJECT
-                kd = K_REJECT;
-            } else {
-                const uint64_t x = IPM & S.reuse_sel[need];  // an idle slice that tightly fits (R7)
-                uint32_t y = (uint32_t)x | (uint32_t)(x >> 32);
-                y |= y >> 16;
-                y |= y >> 8;
-                const uint32_t cand = y & 0xFFu;
-                if (cand) {
-                    s = 31u - __clz(cand);
-                    pr = (prof4 >> (4 * s)) & 0xFu;
-                    kd = K_REUSE;
-                } else {
-                    const uint32_t a = S.alloc[(occ << 3) | need];  // Alg. 2: its start
-                    if (a != 0xFFu) {
-                        s = a;
-                        kd = K_ALLOC;
-                    } else {
-                        const uint32_t cm = (SM & ~BS) ? S.nobusy[(BM << 3) | need] : 0u;
-                        kd = K_WAIT;  // sleep() until a running job finishes, unless A7 finds one
-                        if (cm) {  // A7 fusion / fission (R8), host-built answer table
-                            const uint32_t sid = __ldg(P.sid + (occ | (SM << 8)));
-                            const uint2 e = __ldg(P.a7 + (sid * P.n_a7 + S.cbase[need] + cm));
-                            if (e.x) {
-                                s = e.x & 0xFFu;
-                                nd = 15u - ((e.x >> 8) & 0xFFu);
-                                const uint32_t rm = e.y & 0xFFu;
-                                IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
-                                occ &= ~rm;
-                                SM &= ~rm;
-                                kd = K_RECONF;
-                            }
-                        }
-                    }
+            const bool rej = need == kNoNeed;  // no profile can ever hold the job: REJECT
+            const uint32_t nq = rej ? 0u : need;
+            const uint64_t x = IPM & S.reuse_sel[nq];  // idle slices that tightly fit (R7)
+            uint32_t y = (uint32_t)x | (uint32_t)(x >> 32);
+            y |= y >> 16;
+            y |= y >> 8;
+            const uint32_t cand = y & 0xFFu;
+            const uint32_t a = S.alloc[(occ << 3) | nq];  // Alg. 2: its start, 0xFF = FAIL
+            const uint32_t rsl = 31u - __clz(cand | 1u);
+            pr = rej ? kNoNeed : cand ? (prof4 >> (4 * rsl)) & 0xFu : need;
+            s = cand ? rsl : a;
+            kd = rej ? K_REJECT : cand ? K_REUSE : a != 0xFFu ? K_ALLOC : K_WAIT;
+            a7try = kd == K_WAIT && (SM & ~BS);  // fusion / fission may place it (idle instances exist)
+        }
+        if (a7try) {  // A7 (R8): candidates touching no busy slot, the host-built answer table
+            const uint32_t need = hneed;
+            const uint32_t cm = S.nobusy[(BM << 3) | need];
+            if (cm) {
+                const uint32_t sid = __ldg(P.sid + (occ | (SM << 8)));
+                const uint2 e = __ldg(P.a7 + (sid * P.n_a7 + S.cbase[need] + cm));
+                if (e.x) {
+                    s = e.x & 0xFFu;
+                    nd = 15u - ((e.x >> 8) & 0xFFu);
+                    const uint32_t rm = e.y & 0xFFu;
+                    IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
+                    occ &= ~rm;
+                    SM &= ~rm;
+                    kd = K_RECONF;
                 }
             }
         }
         __syncwarp();
         if (pass) {
             const uint32_t j = hj;
-            const bool place = kd <= K_RECONF;
-            if (!place) {  // WAIT / REJECT: slot 0xF, the tight fit (REJECT: 0xF)
-                lrec(hl, hh, t, (j << 16) | (kd << 12) | 0xF00u | (pr << 4));
-                if (kd == K_WAIT) {
-                    K1 += 1u << 16;
-                    mode = 1;
-                } else {
-                    K2 += 1u;
-                }
-            } else {
-                // ---- create (ALLOC / RECONF, try_new_mig_slice PAPER.md:609), record, run start ----
-                const bool created = kd != K_REUSE;
+            const bool place = kd <= K_RECONF, created = kd >= K_ALLOC && place;
+            // the decision record: placements carry (slot, profile, #destroyed); WAIT / REJECT slot 0xF and the tight
+            // fit (REJECT: 0xF)
+            lrec(hl, hh, t, (j << 16) | (kd << 12) | (place ? (s << 8) | (pr << 4) | nd : 0xF00u | (pr << 4)));
+            K0 += place ? (created ? 0x10001u : 1u) : 0u;
+            K1 += kd == K_WAIT ? 1u << 16 : nd;
+            K2 += kd == K_REJECT ? 1u : 0u;
+            if (kd == K_WAIT) mode = 1;
+            if (place) {
+                // ---- create (ALLOC / RECONF, try_new_mig_slice PAPER.md:609) or take the idle slice, run start ----
                 const uint32_t si = S.pinfo[pr];
                 const uint32_t lm8 = (si >> 8) & 0xFFu;
                 if (created) {
@@ -1262,9 +1256,6 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 } else {
                     IPM &= ~(1ull << (8 * pr + s));
                 }
-                lrec(hl, hh, t, (j << 16) | (kd << 12) | (s << 8) | (pr << 4) | nd);
-                K0 += created ? 0x10001u : 1u;
-                K1 += nd;
                 // start_run: end tick and kind (OOM > COMPLETE in one iteration, R29)
                 const uint32_t rs = t + (created ? reconfig : 0u);
                 const uint32_t lev = si & 0xFu, comp = (si >> 4) & 0xFu, T = hr.z & 0xFFFFu, ticks = hr.w;

@@ -21,7 +21,7 @@ def obj(src, out, extra=()):
 def main():
     os.makedirs(os.path.join(ROOT, "build/obj"), exist_ok=True)
     os.makedirs(os.path.join(ROOT, "build/var"), exist_ok=True)
-    for f in os.listdir(os.path.join(ROOT, "build/var")):
+    for f in ([] if os.environ.get("VAR_KEEP") else os.listdir(os.path.join(ROOT, "build/var"))):
         os.remove(os.path.join(ROOT, "build/var", f))
     var_src = os.environ.get("VAR_SRC", "paper_2508_18556_b200/csrc/simulate_lane.cu")
     others = [s for s in ge.MIG_SOURCES if s != var_src]
