@@ -355,7 +355,9 @@ def roofline(wl, ktimes, steps, totals, world, peaks, peak_src, ncu):
         byts = ((JOB_BYTES + ext_b) * wl.n_jobs + RESULT_BYTES * wl.n) * len(even) / n_l
         ops_desc = f"{OPS_PER_DECISION}/decision + {OPS_PER_EVENT}/event (SURVEY.md §8(d))"
         bytes_desc = f"{JOB_BYTES + ext_b} B/job read + {RESULT_BYTES} B/trace result written"
-        kname = f"k_simulate_lane ({dom})"
+        fast = not wl.has_ext and all(wl.pol_keys[i][1] == 0 for i in even) and os.environ.get("MIG_FF_FAST", "1") != "0"
+        kname = {("sim_ff", True): "k_ff_lane", ("sim_baseline", True): "k_base_lane"}.get(
+            (dom, fast), f"k_simulate_lane ({dom})")
     a_ops = ops / (ms * 1e-3)
     a_bytes = byts / (ms * 1e-3)
     intensity = ops / byts if byts else float("inf")
