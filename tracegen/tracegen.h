@@ -75,7 +75,9 @@ TG_HD uint32_t tg_octave(uint64_t r, uint32_t a, uint32_t b) {
 TG_HD int32_t tg_irwin_hall(uint64_t r, uint32_t sigma) {
     int32_t s = (int32_t)(r & 0xFFFF) + (int32_t)((r >> 16) & 0xFFFF) + (int32_t)((r >> 32) & 0xFFFF) +
                 (int32_t)((r >> 48) & 0xFFFF);
-    return (int32_t)(((int64_t)(s - 131070) * (int64_t)(int32_t)((sigma & 0xFFFFu) * 7094u)) >> 28);
+    /* floor((s - 131070) * m / 2^28) written as the high word of 16 (s - 131070) * m (|16 (s - 131070)| < 2^21):
+     * the same integer, one multiply-high on 32-bit ALUs */
+    return (int32_t)(((int64_t)((s - 131070) * 16) * (int64_t)(int32_t)((sigma & 0xFFFFu) * 7094u)) >> 32);
 }
 
 /* 32-bit integer hash ("lowbias32", C. Wellons 2018: two multiplies, three xorshifts). */
