@@ -1021,6 +1021,8 @@ __device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
 #ifndef FF_MINB
 #define FF_MINB 8
 #endif
+// NS: the start slots scanned for the next event (every placement of the geometry starts below NS; A100: 7).
+template <int NS>
 __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) FFShared S;
     const uint32_t tid = threadIdx.x;
@@ -1134,7 +1136,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
         occ = SM = BS = BM = prof4 = 0;
         IPM = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) key[k * kLaneThreads] = kIdle;
+        for (int k = 0; k < NS; ++k) key[k * kLaneThreads] = kIdle;
         kmin = kIdle;
         K0 = K1 = K2 = K3 = 0;
         a_turn = a_busy = a_mem = a_waste = 0;
@@ -1181,7 +1183,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 IPM |= 1ull << (8 * epr + es);  // the instance is idle
                 unsigned long long m = key[0];
 #pragma unroll
-                for (int k = 1; k < 8; ++k) m = min(m, key[k * kLaneThreads]);
+                for (int k = 1; k < NS; ++k) m = min(m, key[k * kLaneThreads]);
                 kmin = m;
                 if ((uint32_t)(m >> 32) != t || m == kIdle) mode = 0;  // the tick is over: one scheduler pass
             }
@@ -1677,11 +1679,16 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
         }
         static int ff_per_sm = 0;
         if (!ff_per_sm) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ff_per_sm, k_ff_lane, kLaneThreads, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ff_per_sm, k_ff_lane<8>, kLaneThreads, 0);
             if (ff_per_sm < 1) ff_per_sm = 1;
         }
         const dim3 g2((unsigned)std::min<uint64_t>(blocks, lane_blocks(ff_per_sm, tr.n_traces, sm_count)));
-        k_ff_lane<<<g2, block, 0, stream>>>(Gdev, P);
+        uint32_t ns = 0;  // one past the highest start slot of any placement
+        for (uint32_t p = 0; p < Gh->n_prof; ++p)
+            for (uint32_t k = 0; k < Gh->n_place[p]; ++k) ns = std::max(ns, (Gh->place[p][k] & 0xFFu) + 1u);
+        if (ns <= 4) k_ff_lane<4><<<g2, block, 0, stream>>>(Gdev, P);
+        else if (ns <= 7) k_ff_lane<7><<<g2, block, 0, stream>>>(Gdev, P);
+        else k_ff_lane<8><<<g2, block, 0, stream>>>(Gdev, P);
         return cudaGetLastError();
     }
     switch (pol.kind) {
