@@ -60,6 +60,12 @@ struct LaneParams {
     // operands, and the first profile of each level as nibbles (0xF = none)
     uint32_t lm[kMaxLevels];
     uint32_t lfirst;
+    // Scheme A, grouped by k_sa_group before the launch (or NULL: the lane kernel's own grouping pass): the trace's
+    // job records in group order (record x replaced by the job index) and per trace {5 group lengths, REJECT count,
+    // error bits} + the decision hash after the t = 0 REJECT records
+    const uint4* sa_desc;
+    const uint4* sa_dext;
+    const uint4* sa_hdr;
 };
 
 constexpr int kLaneThreads = 128;
@@ -242,11 +248,15 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     uint16_t* ring = KIND == MIG_SCHEME_A
                          ? P.ring + (size_t)blockIdx.x * kLaneThreads * P.ring_cap * kMaxLevels + tid
                          : P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap;
-    // Scheme A: [0..7] group lengths by memory level, [8..15] next group-list index of the slice at slot s
-    __shared__ uint16_t s_sa[KIND == MIG_SCHEME_A ? 16 : 1][kLaneThreads];
+    // Scheme A: [0..7] group lengths by memory level, [8..15] next group-list index of the slice at slot s, [16..23]
+    // the group's entries grouped before the launch (sa_desc; the rest are requeues in the ring)
+    __shared__ uint16_t s_sa[KIND == MIG_SCHEME_A ? 24 : 1][kLaneThreads];
     uint16_t* glen = &s_sa[0][tid];
     uint16_t* nx = &s_sa[KIND == MIG_SCHEME_A ? 8 : 0][tid];
+    uint16_t* plen = &s_sa[KIND == MIG_SCHEME_A ? 16 : 0][tid];
     uint32_t cur = 0xFFu, ns = 0, PM = 0, ready = 0;  // Scheme A: current group, its slices, pending-slice mask
+    uint32_t pbase = 0;  // Scheme A with sa_desc: the current group's first record in the trace's grouped records
+    const bool sa_pre = KIND == MIG_SCHEME_A && !EXT && P.sa_desc != nullptr;
     // PCIe contention (R39): slot s run state at pcs[2s] = {W lo, W hi, tk, rs}, pcs[2s+1] = {D, mem, iters,
     // F | started << 8 | dynamic << 9}; c_eff = transferring runs since the last retime; tick_end = an end event
     // was applied at the current tick (a tick with only starts has no scheduler pass)
@@ -346,9 +356,9 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
         c_eff = 0;
         if (KIND == MIG_SCHEME_A) {
             cur = 0xFFu;
-            ns = PM = ready = 0;
+            ns = PM = ready = pbase = 0;
 #pragma unroll
-            for (int l = 0; l < 8; ++l) glen[l * kLaneThreads] = 0;
+            for (int l = 0; l < 8; ++l) glen[l * kLaneThreads] = plen[l * kLaneThreads] = 0;
         }
         K0 = K1 = K2 = K3 = 0;
         a_turn = a_busy = a_mem = a_waste = 0;
@@ -362,6 +372,18 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             na = alast = 0;
             hj = kNoJob;
             admit();
+        }
+        if (KIND == MIG_SCHEME_A && sa_pre) {  // grouped before the launch (k_sa_group): no grouping pass
+            const uint4 h0 = __ldg(P.sa_hdr + 2 * tr), h1 = __ldg(P.sa_hdr + 2 * tr + 1);
+            const uint32_t lens[5] = {h0.x & 0xFFFFu, h0.x >> 16, h0.y & 0xFFFFu, h0.y >> 16, h0.z & 0xFFFFu};
+#pragma unroll
+            for (int l = 0; l < 5; ++l) glen[l * kLaneThreads] = plen[l * kLaneThreads] = (uint16_t)lens[l];
+            K2 = h0.z >> 16;  // the REJECTs at t = 0
+            err |= h0.w;
+            hl = h1.x;
+            hh = h1.y;
+            hj = kNoJob;
+            return;
         }
         fetch_head();
         if (KIND == MIG_SCHEME_A && hj != kNoJob) mode = 4;  // the grouping pass first
@@ -576,10 +598,18 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                 if (cand) {  // the lowest idle slice with pending jobs takes its next one
                     const uint32_t s = (uint32_t)__ffs(cand) - 1u;
                     const uint32_t k = nx[s * kLaneThreads];
-                    const uint32_t j = ring[(cur * P.ring_cap + k) * kRs];
+                    const uint32_t pl = sa_pre ? plen[cur * kLaneThreads] : 0u;
+                    uint32_t j;
+                    if (sa_pre && k < pl) {  // a grouped record (its x holds the job index)
+                        hr = __ldg(P.sa_desc + j0 + pbase + k);
+                        he = pext ? __ldg(P.sa_dext + j0 + pbase + k) : make_uint4(0, 0, 0, 0);
+                        j = hr.x;
+                    } else {  // a requeued job (OOM / early restart), from the ring
+                        j = ring[(cur * P.ring_cap + k - pl) * kRs];
+                        hr = __ldg(P.jobs + j0 + j);
+                        he = pext ? __ldg(pext + j0 + j) : make_uint4(0, 0, 0, 0);
+                    }
                     const uint32_t pr = (prof4 >> (4 * s)) & 0xFu;
-                    hr = __ldg(P.jobs + j0 + j);
-                    he = pext ? __ldg(pext + j0 + j) : make_uint4(0, 0, 0, 0);
                     lrec(hl, hh, t, (j << 16) | (K_PLACE_GROUP << 12) | (s << 8) | (pr << 4));
                     K0 += 1u;
                     uint32_t end, ek;
@@ -610,6 +640,10 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                         K0 += ns << 16;
                         ready = t + reconfig;
                         cur = l;
+                        if (sa_pre) {  // the group's grouped records follow those of the smaller levels
+                            pbase = 0;
+                            for (uint32_t q = 0; q < l; ++q) pbase += plen[q * kLaneThreads];
+                        }
                     } else {
                         mode = 1;  // nothing left: EVT finds no running job and finishes the unit
                     }
@@ -676,7 +710,8 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                                 K2 += 1u;
                             } else {
                                 const uint32_t lv = G.level[nn], c = glen[lv * kLaneThreads];
-                                ring[(lv * P.ring_cap + c) * kRs] = (uint16_t)job;
+                                ring[(lv * P.ring_cap + c - (sa_pre ? plen[lv * kLaneThreads] : 0u)) * kRs] =
+                                    (uint16_t)job;
                                 glen[lv * kLaneThreads] = (uint16_t)(c + 1u);
                             }
                         }
@@ -1578,6 +1613,142 @@ __global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const Dev
     }
 }
 
+// ================================================================================================================
+// k_sa_group: Scheme A's grouping pass (sorted_by_mig_group, reading R38) as its own launch before
+// the Scheme A lane launch. One lane per trace, a warp takes 32 consecutive traces and walks their job records in
+// lockstep (coalesced enough, no event loop): the t = 0 REJECT records (queue order) go into the trace's decision
+// hash, and the records are written in group order (ascending memory level of the tight fit, queue order within a
+// level) with their x word replaced by the job index, so the lane kernel dispatches each group by reading the next
+// record of the group sequentially instead of re-reading records by job index. Per trace: sa_hdr[2t]
+// = {len0 | len1 << 16, len2 | len3 << 16, len4 | rejected << 16, error bits}, sa_hdr[2t + 1] = {hash lo, hash hi}.
+// Pass 1 counts the groups (and the REJECT hash), pass 2 scatters (the trace's records are re-read from L2).
+// ================================================================================================================
+template <bool XR>
+__global__ void __launch_bounds__(kLaneThreads) k_sa_group(const DevGeom* __restrict__ Gg, const LaneParams P,
+                                                          uint4* desc, uint4* dext, uint4* hdr) {
+    __shared__ uint32_t s_lmem[8];
+    __shared__ uint8_t s_first[8];
+    __shared__ DevGeom sG;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&sG);
+        for (uint32_t i = tid; i < sizeof(DevGeom) / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const DevGeom& G = sG;
+    if (tid < 8) {
+        uint32_t f = 0xFFu;
+        for (uint32_t p = G.n_prof; p-- > 0;)
+            if (G.level[p] == tid) f = p;
+        s_first[tid] = (uint8_t)(tid < G.n_levels ? f : 0xFFu);
+        s_lmem[tid] = tid < G.n_levels ? G.level_mem[tid] : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const bool fold = (P.pol.flags & MIG_WARP_FOLD) != 0;
+    // the tight fit of lane_tight_fit<MIG_SCHEME_A> (R6, R30)
+    auto fit = [&](uint32_t req, uint32_t warps) -> uint32_t {
+        if (!fold || warps == 0) {
+            uint32_t L = s_lmem[3] < req ? 4u : 0u;
+            L += s_lmem[L + 1] < req ? 2u : 0u;
+            L += s_lmem[L] < req ? 1u : 0u;
+            return s_first[L];
+        }
+        const uint32_t cf = G.wave_cap[G.full_prof];
+        for (uint32_t p = 0; p < G.n_prof; ++p) {
+            if (G.mem[p] < req) continue;
+            const uint32_t cp = G.wave_cap[p];
+            if ((warps + cp - 1) / cp != (warps + cf - 1) / cf) continue;
+            return p;
+        }
+        return kNoNeed;
+    };
+    const uint64_t jbase = P.off[0];
+    const uint32_t ctx = P.ctx, mem0 = G.mem[0];
+    const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
+    // one warp per trace: its records 32 at a time (coalesced), the tight fits in parallel, the group positions by
+    // ballots; the REJECT records (rare) folded into the hash in queue order by lane 0
+    for (unsigned long long tr = blockIdx.x * (kLaneThreads / 32) + (tid >> 5); tr < P.n_traces;
+         tr += (unsigned long long)gridDim.x * (kLaneThreads / 32)) {
+        const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1], j0 = o0 - jbase;
+        uint32_t n = (uint32_t)(o1 - o0), err = 0;
+        if (o1 - o0 > P.max_jobs) {
+            err = (uint32_t)MIG_ERR_TRACE_TOO_LONG;
+            n = 0;
+        }
+        uint32_t hl = (uint32_t)kFnvOffset, hh = (uint32_t)(kFnvOffset >> 32), rej = 0;
+        uint32_t cnt[5] = {0, 0, 0, 0, 0};
+        auto need_of = [&](uint32_t k, uint4& r, uint4& e) -> uint32_t {
+            r = __ldg(P.jobs + j0 + k);
+            e = XR ? __ldg(P.ext + j0 + k) : make_uint4(0, 0, 0, 0);
+            const uint32_t cls = (r.z >> 16) & 0xFFu;
+            return fit(cls == kClassDynamic ? mem0 : r.x + e.x + ctx, e.y);  // R16 / est + ws + ctx
+        };
+        for (uint32_t c = 0; c < n; c += 32) {  // pass 1: REJECTs in queue order, group sizes
+            const uint32_t k = c + lane;
+            uint32_t lv = 0xFFu;
+            bool rj = false;
+            if (k < n) {
+                uint4 r, e;
+                const uint32_t need = need_of(k, r, e);
+                const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
+                if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
+                rj = need == kNoNeed;
+                if (!rj) lv = G.level[need];
+            }
+            uint32_t rm = __ballot_sync(FULL, rj);
+            rej += __popc(rm);
+            while (rm) {  // lane-uniform loop over this chunk's REJECTs, in queue order
+                const uint32_t q = (uint32_t)__ffs(rm) - 1u;
+                rm &= rm - 1u;
+                lrec(hl, hh, 0u, ((c + q) << 16) | (K_REJECT << 12) | 0xFF0u);
+            }
+#pragma unroll
+            for (int l = 0; l < 5; ++l) cnt[l] += __popc(__ballot_sync(FULL, lv == (uint32_t)l));
+        }
+        uint32_t pos[5];
+        pos[0] = 0;
+#pragma unroll
+        for (int l = 1; l < 5; ++l) pos[l] = pos[l - 1] + cnt[l - 1];
+        for (uint32_t c = 0; c < n; c += 32) {  // pass 2: the records in group order, x = the job index
+            const uint32_t k = c + lane;
+            uint4 r = make_uint4(0, 0, 0, 0), e = r;
+            uint32_t lv = 0xFFu;
+            if (k < n) {
+                const uint32_t need = need_of(k, r, e);
+                if (need != kNoNeed) lv = G.level[need];
+            }
+            uint32_t at = 0;
+#pragma unroll
+            for (int l = 0; l < 5; ++l) {
+                const uint32_t m = __ballot_sync(FULL, lv == (uint32_t)l);
+                if (lv == (uint32_t)l) at = pos[l] + __popc(m & lt);
+                pos[l] += __popc(m);
+            }
+            if (lv != 0xFFu) {
+                r.x = k;
+                desc[j0 + at] = r;
+                if (XR) dext[j0 + at] = e;
+            }
+        }
+        err = __reduce_or_sync(FULL, err);
+        if (lane == 0) {
+            hdr[2 * tr] = make_uint4(cnt[0] | (cnt[1] << 16), cnt[2] | (cnt[3] << 16), cnt[4] | (rej << 16), err);
+            hdr[2 * tr + 1] = make_uint4(hl, hh, 0u, 0u);
+        }
+    }
+}
+
+// MIG_SA_PREGROUP=0: Scheme A's grouping pass inside the lane kernel instead of k_sa_group (A/B and parity).
+static bool sa_pregroup_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* env = getenv("MIG_SA_PREGROUP");
+        on = env ? atoi(env) != 0 : 1;
+    }
+    return on != 0;
+}
+
 // MIG_FF_FAST=0 selects k_simulate_lane for the FUSION_FISSION fast case too (A/B and parity of both kernels).
 static bool ff_fast_enabled() {
     static int on = -1;
@@ -1718,6 +1889,32 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
             break;
         case MIG_SCHEME_A:
             if (P.arr) return cudaErrorInvalidValue;  // Scheme A groups the whole queue at t = 0
+            if (!ext && sa_pregroup_enabled() && tr.n_traces && tr.n_jobs) {
+                // the grouping pass as its own launch (k_sa_group), its outputs in stream-ordered scratch
+                const size_t nj = tr.n_jobs, nt = tr.n_traces;
+                const size_t b_desc = nj * 16, b_dext = P.ext ? nj * 16 : 0, b_hdr = nt * 32;
+                uint8_t* sa = nullptr;
+                cudaError_t e2 = mig_scratch_alloc((void**)&sa, b_desc + b_dext + b_hdr, stream);
+                if (e2 != cudaSuccess) return e2;
+                P.sa_desc = reinterpret_cast<const uint4*>(sa);
+                P.sa_dext = P.ext ? reinterpret_cast<const uint4*>(sa + b_desc) : nullptr;
+                P.sa_hdr = reinterpret_cast<const uint4*>(sa + b_desc + b_dext);
+                const unsigned gg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sm_count * 16,
+                                                                                     (nt + 3) / 4));
+                if (P.ext)
+                    k_sa_group<true><<<gg, block, 0, stream>>>(Gdev, P, (uint4*)P.sa_desc, (uint4*)P.sa_dext, (uint4*)P.sa_hdr);
+                else
+                    k_sa_group<false><<<gg, block, 0, stream>>>(Gdev, P, (uint4*)P.sa_desc, nullptr, (uint4*)P.sa_hdr);
+                e2 = cudaGetLastError();
+                if (e2 == cudaSuccess) {
+                    if (P.ext) k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
+                    else if (pf) k_simulate_lane<MIG_SCHEME_A, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);
+                    else k_simulate_lane<MIG_SCHEME_A, false, false><<<grid, block, 0, stream>>>(Gdev, P);
+                    e2 = cudaGetLastError();
+                }
+                mig_scratch_free(sa, stream);
+                return e2;
+            }
             if (ext) k_simulate_lane<MIG_SCHEME_A, true><<<grid, block, 0, stream>>>(Gdev, P);
             else if (P.ext) k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
             else if (pf) k_simulate_lane<MIG_SCHEME_A, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);
