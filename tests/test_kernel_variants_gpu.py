@@ -1,4 +1,5 @@
-"""Every k_simulate variant (one lane per trace: k_simulate_lane; or a group of 8 | 32 lanes per trace with job
+"""Every k_simulate variant (one lane per trace: k_ff_lane / k_base_lane / k_sa_group + k_simulate_lane, or
+k_simulate_lane alone; or a group of 8 | 32 lanes per trace with job
 staging layout wide | narrow; policy launches on two streams (default) or serialised, MIG_CONCURRENT_POLICIES) is
 parity-checked against the oracle. The variant is chosen per process from MIG_LANES_PER_TRACE / MIG_JOB_LAYOUT, so each runs in a
 subprocess."""
@@ -35,10 +36,15 @@ print("variant OK")
 '''
 
 
-@pytest.mark.parametrize("lanes,layout,conc", [("1", "narrow", "1"), ("1", "narrow", "0"), ("8", "wide", "1"),
-                                               ("8", "narrow", "1"), ("32", "wide", "1"), ("32", "narrow", "1")])
-def test_variant_parity(lanes, layout, conc):
-    env = dict(os.environ, MIG_LANES_PER_TRACE=lanes, MIG_JOB_LAYOUT=layout, MIG_CONCURRENT_POLICIES=conc)
+@pytest.mark.parametrize("lanes,layout,conc,fast", [("1", "narrow", "1", "1"), ("1", "narrow", "0", "1"),
+                                                    ("1", "narrow", "1", "0"), ("8", "wide", "1", "1"),
+                                                    ("8", "narrow", "1", "1"), ("32", "wide", "1", "1"),
+                                                    ("32", "narrow", "1", "1")])
+def test_variant_parity(lanes, layout, conc, fast):
+    # fast = "0": the generic k_simulate_lane for FUSION_FISSION and BASELINE (MIG_FF_FAST=0) and Scheme A's grouping
+    # pass inside the lane kernel (MIG_SA_PREGROUP=0) instead of k_ff_lane / k_base_lane / k_sa_group
+    env = dict(os.environ, MIG_LANES_PER_TRACE=lanes, MIG_JOB_LAYOUT=layout, MIG_CONCURRENT_POLICIES=conc,
+               MIG_FF_FAST=fast, MIG_SA_PREGROUP=fast)
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "variant OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
