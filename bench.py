@@ -370,6 +370,15 @@ def roofline(wl, ktimes, steps, totals, world, peaks, peak_src, ncu):
          "hbm": {"achieved": a_bytes / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s", "frac": a_bytes / hbm_peak,
                  "bytes_per_launch": byts, "model": bytes_desc, "peak_source": f"{peak_src} hbm_gbs"},
          "intensity_ops_per_byte": intensity, "ridge_ops_per_byte": ridge}
+    if dom != "k_estimate":  # the whole step: every simulation launch's algorithmic units / the step's time
+        dec_all = sum(int(t["placements"]) + int(t["waits"]) + int(t["rejected"]) for t in totals) / world
+        ev_all = sum(int(t["placements"]) for t in totals) / world
+        step_ms = sum(per_step[k] for k in per_step if k == "k_simulate") or ms
+        ops_s = OPS_PER_DECISION * dec_all + OPS_PER_EVENT * ev_all
+        bytes_s = ((JOB_BYTES + ext_b) * wl.n_jobs + RESULT_BYTES * wl.n) * len(wl.pol_keys)
+        r["step"] = {"ms": step_ms, "launches": len(wl.pol_keys), "hbm_frac": bytes_s / (step_ms * 1e-3) / hbm_peak,
+                     "alu_frac": ops_s / (step_ms * 1e-3) / alu_peak,
+                     "note": "all policy launches of the step (they co-run on two streams) over the k_simulate span"}
     side = r["hbm"] if bound == "hbm" else r["alu"]
     r.update({"achieved": side["achieved"], "peak": side["peak"], "unit": side["unit"], "frac": side["frac"],
               "traffic": traffic})
