@@ -61,6 +61,7 @@ KIND_OF = {"sim_baseline": 0, "sim_static": 1, "sim_dynamic": 2, "sim_ff": 3, "s
 OPS_PER_DECISION = 25    # <= 7 legality ANDs + <= 7 fcr lookups + 1 argmax (15-25 integer ops)
 OPS_PER_EVENT = 12       # <= 7 compares + queue op + 2 energy ops + 2 hash ops
 OPS_PER_DYN_ITER = 23    # RNG + Irwin-Hall ~15, <= 5 level compares, 3 moment updates
+OPS_PER_FIT = 25         # per fit until convergence: ~25 FP64 ops incl. 3 divisions and 1 sqrt (+ int128 products)
 JOB_BYTES = 16           # job record read once per launch (+16 with an extension record)
 RESULT_BYTES = 96        # per-trace result row written once per launch (mig_trace_result)
 EST_BYTES = 80           # mig_job_estimate written per DYNAMIC job by k_estimate
@@ -214,10 +215,19 @@ class Workload:
             self.dyn_samples = int(((zf & 0xFFFF) * dyn.to(torch.int64)).sum().item())
             self.n_dyn_jobs = int(dyn.sum().item())
             self.n_jobs = self.tr.n_jobs
+            self.fits = 0
+            if self.n_dyn_jobs:  # fits until convergence (§8(d)), from one estimator call outside the timed region
+                est = mig.mig_estimate_memory(self.g, self.tr, self.pols[0])
+                conv = est.view(-1, 80)[:, 8:10].contiguous().view(torch.int16).to(torch.int64).view(-1) & 0xFFFF
+                T = zf & 0xFFFF
+                min_n = int(self.pols[0].min_n)
+                f = torch.where(conv > 0, conv - min_n + 1, (T - min_n + 1).clamp(min=0))
+                self.fits = int((f * dyn.to(torch.int64)).sum().item())
+                del est, conv, T, f
         else:  # the units the roofline counts, from one pass of the generator over the shard (not timed)
             self.res = None
             self.n_jobs = n * self.J
-            self.dyn_samples = self.n_dyn_jobs = 0
+            self.dyn_samples = self.n_dyn_jobs = self.fits = 0
             for c0 in range(0, n, chunk):
                 m = min(chunk, n - c0)
                 j, _, _ = tg.generate_device(cfg, m, trace_id0=t_id0 + c0, seed=self.seed, device=dev)
@@ -339,9 +349,10 @@ def roofline(wl, ktimes, steps, totals, world, peaks, peak_src, ncu):
     if dom == "k_estimate":
         # every job record (+ ext) read once, an estimate written per DYNAMIC job; 23 ops per sample scanned
         dyn_samples = wl.dyn_samples or 0
-        ops = OPS_PER_DYN_ITER * dyn_samples / n_l
+        ops = (OPS_PER_DYN_ITER * dyn_samples + OPS_PER_FIT * (wl.fits or 0)) / n_l
         byts = ((JOB_BYTES + ext_b) * wl.n_jobs + EST_BYTES * (wl.n_dyn_jobs or 0)) / n_l
-        ops_desc = f"{OPS_PER_DYN_ITER} ops per DYNAMIC-job sample scanned (fits not counted)"
+        ops_desc = (f"{OPS_PER_DYN_ITER} ops per DYNAMIC-job sample scanned + {OPS_PER_FIT} per fit until "
+                    f"convergence ({wl.fits} fits; chunked shards: samples only)")
         bytes_desc = f"{JOB_BYTES + ext_b} B/job read + {EST_BYTES} B per DYNAMIC job written"
         kname = "k_estimate"
     else:
