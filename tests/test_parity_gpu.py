@@ -524,3 +524,23 @@ def test_recorded_trace_files(tmp_path):
     res, _ = mig.mig_simulate(g, tr, pols)
     want = orc.simulate(og, jobs, ext, off, [orc.policy(**s) for s in SPECS], seed=1, samples=smp2, sample_off=soff2)
     assert_same(mig.results_numpy(res, len(pols)), want)
+
+
+@pytest.mark.parametrize("geo", ["a30-24gb", "a100-40gb", "a100-40gb-1g10", "h100-80gb", "b200-180gb"])
+def test_fast_kernels_random_traces_without_ext(geo):
+    # traces without extension records take k_ff_lane (FUSION_FISSION), k_base_lane (BASELINE) and, for Scheme A,
+    # k_sa_group: empty traces, ragged lengths, zero-iteration jobs, rejections, failures on the whole GPU, DYNAMIC
+    # jobs (estimates read in the run start), every geometry (start-slot scans of 4, 7 and 8 slots)
+    spec = json.load(open(geom_path(geo)))
+    rng = np.random.default_rng(41)
+    jobs, _, off = random_tiny_traces(rng, spec, 600, 40, dyn_frac=0.2)
+    for common in [dict(ctx_mib=0, reconfig_ticks=0), dict(ctx_mib=512, reconfig_ticks=500)]:
+        got, want, tot = run_pair(geo, jobs, None, off, SPECS, seed=31, common=common)
+        assert_same(got, want)
+        check_totals(got, tot)
+    rng = np.random.default_rng(9)  # a maximum-length trace, an empty one and a short one
+    tr = [tg.pack_job(int(rng.integers(1, spec["slot_mib"] * 3)), int(rng.integers(1, spec["slot_mib"] * 3)), 1, 0,
+                      int(rng.integers(1, 100))) for _ in range(mig.MIG_MAX_JOBS_PER_TRACE)]
+    jobs, _, off = tg.pack_traces([tr, [], tr[:17]])
+    got, want, tot = run_pair(geo, jobs, None, off, SPECS, max_jobs=mig.MIG_MAX_JOBS_PER_TRACE)
+    assert_same(got, want)
