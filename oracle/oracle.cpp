@@ -27,6 +27,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <deque>
 #include <map>
@@ -1070,6 +1071,55 @@ void* or_geometry_new(const OrGeomDesc* d) {
 }
 
 void or_geometry_free(void* g) { delete (Geometry*)g; }
+
+// Alg. 1 for an arbitrary slot geometry given as placement masks (bit i = memory slot i), by its
+// literal definition: the valid partition states are the sets of pairwise disjoint placements (enumerated
+// exhaustively), the final states those to which no placement can be added (R2), and fcr(s) = the number of final
+// states that contain s (every superset of s that is a state is reached by adding its missing placements). The
+// per-occupancy table fcr_out[m] (2^n_slots entries, 0 where no state has occupancy m) asserts R3: every state with
+// occupancy m has the same fcr. Returns 0, -1 (more than 2 000 000 states), -2 (R3 violated), -3 (bad input).
+int or_reach(uint32_t n_slots, const uint32_t* masks, uint32_t n_pl, uint32_t* fcr_out, uint64_t* n_states,
+             uint64_t* n_finals) {
+    if (n_slots < 1 || n_slots > 20 || n_pl < 1) return -3;
+    std::vector<std::vector<int>> states;
+    std::vector<uint32_t> occ;
+    std::vector<int> cur;
+    // every set of pairwise disjoint placements, each once (placements added in increasing index order)
+    std::function<bool(int, uint32_t)> rec = [&](int from, uint32_t m) -> bool {
+        states.push_back(cur);
+        occ.push_back(m);
+        if (states.size() > 2000000) return false;
+        for (int q = from; q < (int)n_pl; ++q) {
+            if (masks[q] & m) continue;
+            cur.push_back(q);
+            if (!rec(q + 1, m | masks[q])) return false;
+            cur.pop_back();
+        }
+        return true;
+    };
+    if (!rec(0, 0u)) return -1;
+    std::vector<int> finals;
+    for (size_t i = 0; i < states.size(); ++i) {
+        bool fits = false;
+        for (uint32_t q = 0; q < n_pl && !fits; ++q) fits = (masks[q] & occ[i]) == 0;
+        if (!fits) finals.push_back((int)i);
+    }
+    const uint32_t N = 1u << n_slots;
+    std::vector<int64_t> table(N, -1);
+    for (size_t i = 0; i < states.size(); ++i) {
+        uint32_t c = 0;
+        for (int f : finals) {  // s is a subset of F (both sorted placement lists)
+            if ((occ[i] & ~occ[f]) != 0) continue;
+            c += std::includes(states[f].begin(), states[f].end(), states[i].begin(), states[i].end()) ? 1u : 0u;
+        }
+        if (table[occ[i]] >= 0 && table[occ[i]] != (int64_t)c) return -2;
+        table[occ[i]] = c;
+    }
+    for (uint32_t m = 0; m < N; ++m) fcr_out[m] = table[m] < 0 ? 0u : (uint32_t)table[m];
+    *n_states = states.size();
+    *n_finals = finals.size();
+    return 0;
+}
 
 void or_geometry_counts(void* gp, uint32_t* n_states, uint32_t* n_finals, uint32_t* n_placements) {
     Geometry* g = (Geometry*)gp;

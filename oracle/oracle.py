@@ -76,6 +76,8 @@ def lib():
         L.or_state_fcr.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32]
         L.or_allocate.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32]
         L.or_tight_fit.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(OrPolicy)]
+        L.or_reach.argtypes = [C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64),
+                               C.POINTER(C.c_uint64)]
         L.or_predict_series.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(OrPolicy), C.c_uint32,
                                         C.c_void_p]
         L.or_fit_once.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(OrPolicy), C.c_uint32,
@@ -186,6 +188,18 @@ def predict_series(y, q, pol=None, ws=0):
     out = np.zeros(1, ESTIMATE_DTYPE)
     lib().or_predict_series(_ptr(y), _ptr(q), len(y), C.byref(pol), ws, _ptr(out))
     return out[0]
+
+
+def reach(n_slots, masks):
+    """Alg. 1 by its literal definition for a slot geometry of placement masks (oracle.cpp or_reach): returns
+    (fcr per occupancy, uint32 [2^n_slots]; |S|; |F|)."""
+    m = np.ascontiguousarray(masks, np.uint32)
+    out = np.zeros(1 << n_slots, np.uint32)
+    ns, nf = C.c_uint64(), C.c_uint64()
+    rc = lib().or_reach(n_slots, _ptr(m), len(m), _ptr(out), C.byref(ns), C.byref(nf))
+    if rc != 0:
+        raise RuntimeError(f"or_reach failed ({rc})")
+    return out, ns.value, nf.value
 
 
 def fit_once(y, q, T, pol=None, ws=0):

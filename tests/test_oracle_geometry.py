@@ -13,6 +13,7 @@ import itertools
 import json
 import os
 
+import numpy as np
 import pytest
 
 from conftest import GOLDEN_DIR, geom_path
@@ -259,3 +260,37 @@ def test_reach_counts_reference_pins():
     masks = [((1 << L) - 1) << s for L in (1, 2, 4, 8) for s in range(0, 8, L)]
     S, F, fcr = bf.reach_counts(8, masks)
     assert (S, F, fcr[0], fcr[255]) == (677, 26, 26, 1)
+
+
+def test_oracle_reach_pins():
+    # the oracle's literal Alg. 1 on placement masks (or_reach: every set of disjoint placements, finals, fcr =
+    # finals containing the state) against the vendor tables' |S| / |F| / fcr(s0), Appendix A, the closed forms of
+    # aligned power-of-two slots, and the independent pure-Python definition (tests/bruteforce.py) on random
+    # geometries
+    import bruteforce as bf
+
+    for name, nS, nF in [("a30-24gb", 26, 5), ("a100-40gb", 298, 19), ("a100-40gb-1g10", 723, 78)]:
+        spec = json.load(open(geom_path(name)))
+        fcr, S, F = orc.reach(spec["total_memory_slots"], bf.geometry_masks(spec))
+        assert (S, F, int(fcr[0])) == (nS, nF, nF), name
+    spec = json.load(open(geom_path("a100-40gb")))
+    fcr, _, _ = orc.reach(8, bf.geometry_masks(spec))
+    for line in open(os.path.join(GOLDEN_DIR, "a100_fcr_table.txt")):
+        if line.startswith("#"):
+            continue
+        for tok in line.split():
+            if ":" in tok:
+                k, v = tok.split(":")
+                assert int(fcr[int(k, 16)]) == int(v), tok
+    for n, S, F in [(8, 677, 26), (16, 458330, 677)]:
+        masks = [((1 << L) - 1) << s for L in [1 << k for k in range(5)] if L <= n for s in range(0, n, L)]
+        fcr, s_, f_ = orc.reach(n, masks)
+        assert (s_, f_, int(fcr[0]), int(fcr[(1 << n) - 1])) == (S, F, F, 1)
+    rng = np.random.default_rng(2)
+    for _ in range(10):
+        n = int(rng.integers(4, 10))
+        masks = sorted({((1 << L) - 1) << s for L, s in
+                        [(L, int(rng.integers(0, n - L + 1))) for L in rng.integers(1, min(n, 5) + 1, 3 * n)]})
+        S, F, ref = bf.reach_counts(n, masks)
+        fcr, s_, f_ = orc.reach(n, masks)
+        assert (s_, f_) == (S, F) and fcr.tolist() == ref

@@ -1,6 +1,7 @@
 """Alg. 1 on the device (mig_reachability: on-device reachability for larger state spaces),
-against the host tables of the loaded geometries, the pure-Python definition (tests/bruteforce.py reach_counts) on
-random slot geometries, closed forms, and the invariants of Alg. 1 at 16-24 slots."""
+against the host tables of the loaded geometries, the oracle's literal Alg. 1 (oracle.reach, itself pinned by the
+pure-Python definition in tests/bruteforce.py) on random slot geometries, closed forms, and the invariants of Alg. 1
+at 16-24 slots."""
 import json
 import time
 
@@ -10,6 +11,7 @@ import torch
 
 import bruteforce as bf
 from conftest import geom_path
+from oracle import oracle as orc
 
 import paper_2508_18556_b200 as mig
 
@@ -31,7 +33,7 @@ def test_matches_loaded_geometry_tables(name):
     assert np.array_equal((fl & 1) != 0, host > 0) and np.array_equal(dev[(fl & 2) != 0], np.ones(((fl & 2) != 0).sum()))
 
 
-def test_random_geometries_equal_bruteforce():
+def test_random_geometries_equal_oracle():
     rng = np.random.default_rng(11)
     for trial in range(12):
         n = int(rng.integers(5, 12))
@@ -41,10 +43,10 @@ def test_random_geometries_equal_bruteforce():
             s = int(rng.integers(0, n - L + 1))
             masks.add(((1 << L) - 1) << s)
         masks = sorted(masks)
-        S, F, ref = bf.reach_counts(n, masks)
+        ref, S, F = orc.reach(n, masks)  # the oracle's literal Alg. 1 (pinned on the CPU by the brute force)
         fcr, _, info = mig.mig_reachability(n, masks)
-        assert np.array_equal(fcr.cpu().numpy().astype(np.int64), np.array(ref, np.int64)), (n, masks)
-        assert (info["n_states"], info["n_finals"], info["fcr_s0"]) == (S, F, ref[0])
+        assert np.array_equal(fcr.cpu().numpy().astype(np.int64), ref.astype(np.int64)), (n, masks)
+        assert (info["n_states"], info["n_finals"], info["fcr_s0"]) == (S, F, int(ref[0]))
 
 
 def _binary(n):
