@@ -19,9 +19,11 @@
 //                     OOM restart (R12-R15), early restart (R25),
 //                     baseline, static slices (R11), dynamic (create/free)
 //   Metrics ......... makespan, completions, energy (R26), turnaround, decision hash
+//   or_reach ........ Alg. 1 for an arbitrary slot geometry given by placement masks (up to 20 slots), by the same
+//                     literal definition (R42), the reference of mig_reachability
 //
-// Parity status of each function: see DESIGN.md §"Oracle pins". Nothing here is "parity unpinned" except the
-// EWMA variant (R36), which the paper does not describe at all.
+// Parity status of each function: see DESIGN.md §"Oracle pins". Nothing here is "parity unpinned": the EWMA variant
+// (R36), which the paper does not describe, is pinned by hand-worked level sequences.
 
 #include <stdint.h>
 #include <string.h>
