@@ -33,71 +33,9 @@
 
 #include <algorithm>
 
-#include "device_common.cuh"
+#include "lane_common.cuh"
 
 namespace mig {
-
-struct LaneParams {
-    const uint4* jobs;
-    const uint4* ext;
-    const uint64_t* off;
-    const mig_job_estimate* est;
-    uint64_t n_traces;
-    mig_trace_result* out;
-    mig_policy_totals* totals;
-    unsigned long long* counter;
-    const unsigned long long* est_err;  // error word of k_estimate (merged into this policy's totals)
-    uint16_t* ring;                     // requeue FIFOs (job | need << 10) / Scheme A group lists, per lane
-    const uint16_t* sid;                // mig_geometry::sid16: slot-level state id by occ | SM << 8 (FUSION_FISSION)
-    const uint2* a7;                    // mig_geometry::a7, [state][n_a7] (FUSION_FISSION)
-    uint4* pc;                          // PCIe contention: per lane and start slot, 2 x uint4 of run state (R39)
-    unsigned long long* part;           // per-lane partial 64-bit totals, [CTA][kT64][kLaneThreads] (global scratch)
-    const uint32_t* arr;                // arrival ticks aligned with jobs (R40), or NULL (batch)
-    uint32_t n_a7;
-    uint32_t ring_cap, max_jobs, ctx, n_pol_all, pol_idx;
-    mig_policy pol;
-    // k_ff_lane: tight fit against the ascending level memories (padded with 0xFFFFFFFF) read as constant-bank
-    // operands, and the first profile of each level as nibbles (0xF = none)
-    uint32_t lm[kMaxLevels];
-    uint32_t lfirst;
-    // Scheme A, grouped by k_sa_group before the launch (or NULL: the lane kernel's own grouping pass): the trace's
-    // job records in group order (record x replaced by the job index) and per trace {5 group lengths, REJECT count,
-    // error bits} + the decision hash after the t = 0 REJECT records
-    const uint4* sa_desc;
-    const uint4* sa_dext;
-    const uint4* sa_hdr;
-};
-
-constexpr int kLaneThreads = 128;
-// Resident CTAs per SM (launch bounds) and where the u64 accumulators live: the Scheme B kernels (STATIC, DYNAMIC,
-// FUSION_FISSION) keep them in shared memory, BASELINE and Scheme A in registers; every kind runs 8 CTAs (64
-// registers). The per-lane partial totals live in global scratch, so 8 CTAs x 19.8 KB of shared memory still leave
-// the L1 the table and record loads need. Measured A/B, config 2 / config 5 k_simulate: 4.84 / 250.7
-// ms at 7 CTAs (BASELINE 6) with the partials in shared memory; 5.25 / 299 at 8 with them there (28 KB of L1); 4.80 /
-// 240.6 at 8 with the partials in global scratch; 4.70 / 238.1 with BASELINE at 8 too (at 10 / 12 it spills: 4.87 /
-// 5.66 on config 2); Scheme A at 7 / 8: 238.6 / 238.0 on config 5.
-template <int KIND>
-__host__ __device__ constexpr bool lane_acc_smem() { return KIND != MIG_BASELINE && KIND != MIG_SCHEME_A; }
-template <int KIND>
-__host__ __device__ constexpr int lane_min_blocks() { return 8; }
-constexpr uint32_t kNoNeed = 0xFFu, kUnk = 0xFEu, kNoJob = 0xFFFFu;
-constexpr uint32_t kNoEnd = 0xFFFFFFFFu;
-
-// mig_policy_totals fields accumulated per CTA: 32-bit counts (index -> totals field; shared atomics, at most
-// 2^32 / MIG_MAX_JOBS_PER_TRACE units per CTA) and 64-bit sums (per-lane partials). completed,
-// restarts and energy are linear in these (n - rejected - failed; ooms - failed + preempts; idle_w * makespan +
-// w_per_slice * busy) and are derived once per CTA.
-constexpr int kT32 = 12, kT64 = 6;
-// The per-trace counters are packed two per u32 (K0..K3: placements | creates, destroys | waits, rejected | ooms,
-// preempts | failed), so each must stay below 2^16. A job runs at most 1 + 2 * kMaxLevels times (every OOM restart
-// moves to a strictly larger memory level, R14; an early restart moves to a slice holding the converged forecast,
-// R25, where it cannot preempt again before an OOM moves it up), so placements <= jobs * (1 + 2 * kMaxLevels);
-// creates <= placements, destroys <= creates (only created instances are destroyed), and every WAIT is followed by
-// an event or an arrival before the head is evaluated again, so waits <= placements + jobs.
-static_assert((uint64_t)MIG_MAX_JOBS_PER_TRACE * (2 + 2 * kMaxLevels) < 65536,
-              "packed 16-bit per-trace counters could overflow");
-__constant__ const uint8_t kF32[kT32] = {0, 1, 3, 4, 5, 6, 8, 9, 10, 11, 13, 20};
-__constant__ const uint8_t kF64[kT64] = {12, 15, 16, 17, 18, 19};
 
 struct LaneShared {
     DevGeom G;
@@ -114,14 +52,6 @@ struct LaneShared {
     uint32_t c32[kT32];            // per-CTA 32-bit counts (shared atomics)
     // the per-lane partial 64-bit totals live in global scratch (LaneParams::part)
 };
-
-// FNV-1a-64 step on the two 32-bit halves of h (same as simulate.cu).
-__device__ __forceinline__ void lrec(uint32_t& hl, uint32_t& hh, uint32_t tick, uint32_t lo) {
-    const uint32_t x = hl ^ lo, y = hh ^ tick;
-    const uint64_t p = (uint64_t)x * 0x1b3u;
-    hl = (uint32_t)p;
-    hh = (uint32_t)(p >> 32) + y * 0x1b3u + (x << 8);
-}
 
 // Tight fit (R6, R30): the smallest-memory profile holding req (ties -> fewer compute
 // slices; profiles are sorted by (memory, compute)), with warp folding the same wave count as the whole GPU.
@@ -976,767 +906,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             }
         }
     }
-    __syncthreads();
-    if (P.totals) {
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);
-        if (tid == 0 && blockIdx.x == 0 && P.est_err && *P.est_err) atomicOr(dst + 20, *P.est_err);
-        __shared__ unsigned long long red[24];
-        if (tid < kT32 + kT64) {  // one thread per field reduces the CTA's lanes
-            unsigned long long v = 0;
-            if (tid < kT32) {
-                v = S.c32[tid];
-            } else {
-                const unsigned long long* row = P.part + ((size_t)blockIdx.x * kT64 + (tid - kT32)) * kLaneThreads;
-                for (int k = 0; k < kLaneThreads; ++k) v += row[k];
-            }
-            red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
-        }
-        __syncthreads();
-        if (tid < 21) {
-            unsigned long long v;
-            if (tid == 2) v = red[1] - red[3] - red[4];  // completed
-            else if (tid == 7) v = red[5] - red[4] + red[6];  // restarts
-            else if (tid == 14) v = (unsigned long long)pol.idle_w * red[12] + (unsigned long long)pol.w_per_slice * red[16];
-            else v = red[tid];
-            if (v) {
-                if (tid == 13) atomicMax(dst + 13, v);
-                else if (tid == 20) atomicOr(dst + 20, v);
-                else atomicAdd(dst + tid, v);
-            }
-        }
-    }
-}
-
-// ================================================================================================================
-// k_ff_lane: the FUSION_FISSION launch of the common case (no extension records, no early restart / warp folding /
-// wave time, no arrival streams or PCIe contention) written for the fewest issued instructions per step. Same
-// method, records, counters and results as k_simulate_lane<MIG_FUSION_FISSION, false, false, true> (parity-tested
-// against the oracle by the same suites); what differs is the bookkeeping:
-//  - the running instances' next events are 64-bit keys {end tick, kind, job, slot} in shared memory, so the next
-//    event of a lane (R28: tick, then COMPLETE < OOM < PREEMPT, then job id) is one unrolled minimum over the 8
-//    start slots, kept in a register (kmin) and refreshed only when an event retires; a tick's remaining events
-//    and the move to the scheduler pass need no per-tick event mask or tie loop;
-//  - each iteration is EVT (one event) then PASS (one head evaluation), so the pass that follows a tick's last
-//    event runs in the same iteration;
-//  - the tight fit compares against the level memories in the kernel's constant bank (no table loads);
-//  - the four u64 accumulators stay in registers.
-// ================================================================================================================
-struct FFShared {
-    uint32_t pinfo[16];                 // level | comp << 4 | lenmask << 8 (DevGeom::pinfo)
-    uint32_t level_mem[8], level_next[8];
-    uint32_t mem0;
-    uint8_t place_s[8][8];              // start slot of placement k of profile p
-    uint8_t alloc[256 * 8];             // Alg. 2 by (occupancy, profile): start slot of the placement, 0xFF = FAIL
-    uint32_t lmem[8];                   // level memories, padded with 0xFFFFFFFF (tight-fit binary search)
-    uint8_t lvl_first[8];               // first profile of each level ([n_levels..] = 0xFF = none)
-    uint8_t nobusy[256 * 8];            // placements of p touching no busy slot, by busy-slot mask
-    unsigned long long reuse_sel[16];   // idle instances that tightly fit profile p (R7), over the IPM bytes
-    uint16_t cbase[8];                  // fusion/fission-table column of candidate mask 0 of profile p
-    unsigned long long key[8][kLaneThreads];  // per lane and start slot: end << 32 | (job | kind << 16) << 3 | slot
-    uint32_t c32[kT32];
-};
-
-// Tight fit by a branch-free binary search over the 8 padded level memories in shared memory (3 loads).
-#define FF_FIT_S(req)                                                  \
-    ([&](uint32_t r_) {                                                \
-        uint32_t L_ = S.lmem[3] < r_ ? 4u : 0u;                        \
-        L_ += S.lmem[L_ + 1] < r_ ? 2u : 0u;                           \
-        L_ += S.lmem[L_] < r_ ? 1u : 0u;                               \
-        return (uint32_t)S.lvl_first[L_];                              \
-    }(req))
-
-__device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
-    uint32_t L = 0;
-#pragma unroll
-    for (int l = 0; l < kMaxLevels; ++l) L += req > P.lm[l] ? 1u : 0u;
-    const uint32_t p = (P.lfirst >> (4 * L)) & 0xFu;
-    return p == 0xFu ? kNoNeed : p;
-}
-
-#ifndef FF_MINB
-#define FF_MINB 8
-#endif
-// NS: the start slots scanned for the next event (every placement of the geometry starts below NS; A100: 7).
-template <int NS>
-__global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
-    __shared__ __align__(16) FFShared S;
-    const uint32_t tid = threadIdx.x;
-    {
-        const DevGeom* G = Gg;
-        for (uint32_t i = tid; i < 256 * 8; i += blockDim.x) {  // Alg. 2 for every (occupancy, profile)
-            const uint32_t occ = i >> 3, p = i & 7u;
-            const uint32_t np = __ldg(&G->n_prof), ns = __ldg(&G->n_slots);
-            uint32_t best = 0, bk = 0xFFu, nb = 0;
-            if (p < np) {
-                const uint32_t npl = __ldg(&G->n_place[p]);
-                for (uint32_t k = 0; k < npl; ++k) {
-                    const uint32_t pl = __ldg(&G->place[p][k]), qm = pl >> 8;
-                    if (occ < (1u << ns)) {
-                        const uint32_t score =
-                            (pl && !(occ & qm)) ? ((uint32_t)__ldg(&G->fcr[occ | qm]) << 8) | (pl & 0xFFu) : 0u;
-                        if (score > best) {
-                            best = score;
-                            bk = pl & 0xFFu;  // the start slot of the best placement
-                        }
-                    }
-                    nb |= (qm & occ) ? 0u : 1u << k;  // here occ plays the busy-slot mask
-                }
-            }
-            S.alloc[i] = (uint8_t)bk;
-            S.nobusy[i] = (uint8_t)nb;
-        }
-        if (tid < 16) {
-            const uint32_t np = __ldg(&G->n_prof);
-            uint32_t ok = 0;
-            if (tid < np)
-                for (uint32_t q = 0; q < np; ++q)
-                    if (__ldg(&G->level[q]) == __ldg(&G->level[tid]) && __ldg(&G->comp[q]) >= __ldg(&G->comp[tid]))
-                        ok |= 1u << q;
-            unsigned long long sel = 0;
-            for (uint32_t q = 0; q < 8; ++q)
-                if ((ok >> q) & 1u) sel |= 0xFFull << (8 * q);
-            S.reuse_sel[tid] = sel;
-            S.pinfo[tid] = __ldg(&G->pinfo[tid]);
-        }
-        if (tid < 64) S.place_s[tid >> 3][tid & 7] = (uint8_t)__ldg(&G->place[tid >> 3][tid & 7]);
-        if (tid < 8) {
-            const uint32_t nl = __ldg(&G->n_levels), np = __ldg(&G->n_prof);
-            S.level_mem[tid] = __ldg(&G->level_mem[tid]);
-            S.level_next[tid] = __ldg(&G->level_next[tid]);
-            S.lmem[tid] = tid < nl ? __ldg(&G->level_mem[tid]) : 0xFFFFFFFFu;
-            uint32_t f = 0xFFu;
-            for (uint32_t p = np; p-- > 0;)
-                if (__ldg(&G->level[p]) == tid) f = p;
-            S.lvl_first[tid] = (uint8_t)(tid < nl ? f : 0xFFu);
-        }
-        if (tid == 0) {
-            uint32_t cb = 0;
-            const uint32_t np = __ldg(&G->n_prof);
-            for (uint32_t p = 0; p < 8; ++p) {
-                S.cbase[p] = (uint16_t)cb;
-                cb += p < np ? 1u << __ldg(&G->n_place[p]) : 0u;
-            }
-            S.mem0 = __ldg(&G->mem[0]);
-        }
-        if (tid < kT32) S.c32[tid] = 0;
-#pragma unroll
-        for (int f = 0; f < kT64; ++f) P.part[((size_t)blockIdx.x * kT64 + f) * kLaneThreads + tid] = 0;
-    }
-    __syncthreads();
-
-    const uint32_t reconfig = P.pol.reconfig_ticks, ctx = P.ctx;
-    const uint64_t jbase = P.off[0];
-#define FF_RING (P.ring + (size_t)(blockIdx.x * kLaneThreads + tid) * P.ring_cap)
-    unsigned long long* const key = &S.key[0][tid];
-    constexpr unsigned long long kIdle = ~0ull;
-
-    unsigned long long tr = atomicAdd(P.counter, 1ull);
-    __shared__ unsigned long long s_next[kLaneThreads];  // the lane's next unit (taken one ahead)
-    s_next[tid] = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
-    uint64_t j0 = 0;  // index of the unit's first job record
-    uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
-    uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0;
-    uint64_t IPM = 0;  // idle instances by profile: byte p bit s = an idle instance of profile p starts at s
-    uint32_t K0 = 0, K1 = 0, K2 = 0, K3 = 0, hl = 0, hh = 0;
-    unsigned long long a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0, kmin = kIdle;
-    uint32_t hj = kNoJob, hneed = kUnk;
-    uint4 hr = make_uint4(0, 0, 0, 0);
-
-    auto fetch_head = [&]() {  // queue = jobs[qh..n) ++ requeue FIFO
-        if (qh < n) {
-            hj = qh;
-            hneed = kUnk;
-        } else if (rn) {
-            const uint32_t v = FF_RING[rh];
-            hj = v & 0x3FFu;
-            hneed = v >> 10;
-            if (hneed == 15u) hneed = kNoNeed;
-        } else {
-            hj = kNoJob;
-            return;
-        }
-        hr = __ldg(P.jobs + j0 + hj);
-    };
-    auto init_unit = [&]() {
-        const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
-        j0 = o0 - jbase;
-        const uint64_t n64 = o1 - o0;
-        err = 0;
-        n = (uint32_t)n64;
-        if (n64 > P.max_jobs) {
-            err = (uint32_t)MIG_ERR_TRACE_TOO_LONG;
-            n = 0;
-        }
-        t = qh = rh = rn = 0;
-        occ = SM = BS = BM = prof4 = 0;
-        IPM = 0;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) key[k * kLaneThreads] = kIdle;
-        kmin = kIdle;
-        K0 = K1 = K2 = K3 = 0;
-        a_turn = a_busy = a_mem = a_waste = 0;
-        hl = (uint32_t)kFnvOffset;
-        hh = (uint32_t)(kFnvOffset >> 32);
-        mode = 0;
-        fetch_head();
-    };
-
-    bool active = tr < P.n_traces;
-    if (active) init_unit();
-    else mode = 3;
-    while (__any_sync(FULL, active)) {
-        // ---- EVT: apply the event of kmin (R28 order), then refresh kmin ----
-        if (mode == 1) {
-            if (kmin == kIdle) {
-                mode = 2;  // nothing running and nothing placeable: the unit is done
-            } else {
-                const uint32_t lo = (uint32_t)kmin, es = lo & 7u, job = (lo >> 3) & 0xFFFFu, ek = lo >> 19;
-                t = (uint32_t)(kmin >> 32);
-                const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = S.pinfo[epr];
-                const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
-                lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7
-                if (ek == 0) {
-                    a_turn += t;
-                } else {  // OOM: next larger slice (R14) or FAILED on the whole GPU
-                    K2 += 1u << 16;
-                    const uint32_t req = S.level_next[si & 0xFu];
-                    if (req == 0) {
-                        lrec(hl, hh, t, elo | (K_FAILED << 12));
-                        K3 += 1u << 16;
-                    } else {  // back to the queue tail (R13) with the new tight fit
-                        const uint32_t nn = ff_fit(P, req);
-                        uint32_t pos = rh + rn;
-                        if (pos >= P.ring_cap) pos -= P.ring_cap;
-                        FF_RING[pos] = (uint16_t)(job | ((nn == kNoNeed ? 15u : nn) << 10));
-                        ++rn;
-                        if (hj == kNoJob) fetch_head();
-                    }
-                }
-                key[es * kLaneThreads] = kIdle;
-                BS &= ~(1u << es);
-                BM &= ~(((si >> 8) & 0xFFu) << es);
-                IPM |= 1ull << (8 * epr + es);  // the instance is idle
-                unsigned long long m = key[0];
-#pragma unroll
-                for (int k = 1; k < NS; ++k) m = min(m, key[k * kLaneThreads]);
-                kmin = m;
-                if ((uint32_t)(m >> 32) != t || m == kIdle) mode = 0;  // the tick is over: one scheduler pass
-            }
-        }
-        __syncwarp();
-        // ---- PASS: evaluate the head of the queue (Alg. 4, one decision) ----
-        // P1 decides (kd, s, pr, nd) without branches on the common paths: the reuse candidates, the Alg. 2 answer and
-        // the fusion/fission candidates are all looked up, then selected (REUSE before ALLOC before A7 before WAIT);
-        // only the rare A7 table probe and the first evaluation of a job branch. The warp reconverges; P2 records,
-        // creates, starts the run and pops, one copy for every decision kind.
-        if (mode == 0 && hj == kNoJob) mode = 1;
-        const bool pass = mode == 0;
-        uint32_t kd = 0, s = 0, pr = 0, nd = 0;
-        bool a7try = false;
-        if (pass) {
-            if (hneed == kUnk) {  // first evaluation of an initial queue entry: record checks + tight fit
-                const uint32_t cls = (hr.z >> 16) & 0xFFu, T = hr.z & 0xFFFFu;
-                if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
-                hneed = FF_FIT_S(cls == kClassDynamic ? S.mem0 : hr.x + ctx);  // R16 / est + ctx (a2)
-            }
-            const uint32_t need = hneed;
-            const bool rej = need == kNoNeed;  // no profile can ever hold the job: REJECT
-            const uint32_t nq = rej ? 0u : need;
-            const uint64_t x = IPM & S.reuse_sel[nq];  // idle slices that tightly fit (R7)
-            uint32_t y = (uint32_t)x | (uint32_t)(x >> 32);
-            y |= y >> 16;
-            y |= y >> 8;
-            const uint32_t cand = y & 0xFFu;
-            const uint32_t a = S.alloc[(occ << 3) | nq];  // Alg. 2: its start, 0xFF = FAIL
-            const uint32_t rsl = 31u - __clz(cand | 1u);
-            pr = rej ? kNoNeed : cand ? (prof4 >> (4 * rsl)) & 0xFu : need;
-            s = cand ? rsl : a;
-            kd = rej ? K_REJECT : cand ? K_REUSE : a != 0xFFu ? K_ALLOC : K_WAIT;
-            a7try = kd == K_WAIT && (SM & ~BS);  // fusion / fission may place it (idle instances exist)
-        }
-        if (a7try) {  // A7 (R8): candidates touching no busy slot, the host-built answer table
-            const uint32_t need = hneed;
-            const uint32_t cm = S.nobusy[(BM << 3) | need];
-            if (cm) {
-                const uint32_t sid = __ldg(P.sid + (occ | (SM << 8)));
-                const uint2 e = __ldg(P.a7 + (sid * P.n_a7 + S.cbase[need] + cm));
-                if (e.x) {
-                    s = e.x & 0xFFu;
-                    nd = 15u - ((e.x >> 8) & 0xFFu);
-                    const uint32_t rm = e.y & 0xFFu;
-                    IPM &= ~(0x0101010101010101ull * (SM & rm));  // destroyed (idle) instances
-                    occ &= ~rm;
-                    SM &= ~rm;
-                    kd = K_RECONF;
-                }
-            }
-        }
-        __syncwarp();
-        if (pass) {
-            const uint32_t j = hj;
-            const bool place = kd <= K_RECONF, created = kd >= K_ALLOC && place;
-            // the decision record: placements carry (slot, profile, #destroyed); WAIT / REJECT slot 0xF and the tight
-            // fit (REJECT: 0xF)
-            lrec(hl, hh, t, (j << 16) | (kd << 12) | (place ? (s << 8) | (pr << 4) | nd : 0xF00u | (pr << 4)));
-            K0 += place ? (created ? 0x10001u : 1u) : 0u;
-            K1 += kd == K_WAIT ? 1u << 16 : nd;
-            K2 += kd == K_REJECT ? 1u : 0u;
-            if (kd == K_WAIT) mode = 1;
-            if (place) {
-                // ---- create (ALLOC / RECONF, try_new_mig_slice PAPER.md:609) or take the idle slice, run start ----
-                const uint32_t si = S.pinfo[pr];
-                const uint32_t lm8 = (si >> 8) & 0xFFu;
-                if (created) {
-                    occ |= lm8 << s;
-                    SM |= 1u << s;
-                    prof4 = (prof4 & ~(0xFu << (4 * s))) | (pr << (4 * s));
-                } else {
-                    IPM &= ~(1ull << (8 * pr + s));
-                }
-                // start_run: end tick and kind (OOM > COMPLETE in one iteration, R29)
-                const uint32_t rs = t + (created ? reconfig : 0u);
-                const uint32_t lev = si & 0xFu, comp = (si >> 4) & 0xFu, T = hr.z & 0xFFFFu, ticks = hr.w;
-                uint32_t dur, ek, it;
-                if (((hr.z >> 16) & 0xFFu) != kClassDynamic) {
-                    const uint32_t phys = hr.y + ctx < hr.y ? 0xFFFFFFFFu : hr.y + ctx;
-                    ek = (T >= 1 && phys > S.level_mem[lev]) ? 1u : 0u;  // R12: static jobs OOM at iteration 1
-                    it = ek ? 1u : T;
-                    dur = it * ticks;
-                    a_mem += (uint64_t)phys * dur;
-                } else if (P.est) {
-                    const mig_job_estimate* ej = P.est + j0 + j;
-                    const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
-                    ek = fe <= T ? 1u : 0u;
-                    it = ek ? fe : T;
-                    dur = it * ticks;
-                    a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? lev : 6u)) * ticks;
-                } else {  // a DYNAMIC record under MIG_TRACES_NO_DYNAMIC (no estimates): flagged, no forecast
-                    err |= (uint32_t)MIG_ERR_BAD_RECORD;
-                    ek = 0;
-                    it = T;
-                    dur = T * ticks;
-                }
-                if (((uint64_t)it * ticks + rs) >> 32) err |= (uint32_t)MIG_ERR_TICK_OVERFLOW;  // u32 ticks (mig.h)
-                a_busy += (uint64_t)comp * dur;
-                if (ek) a_waste += dur;
-                const unsigned long long kk = ((unsigned long long)(rs + dur) << 32) | (((j | (ek << 16)) << 3) | s);
-                key[s * kLaneThreads] = kk;
-                kmin = min(kmin, kk);
-                BS |= 1u << s;
-                BM |= lm8 << s;
-            }
-            if (kd != K_WAIT) {  // pop the head
-                if (qh < n) {
-                    ++qh;
-                } else {
-                    rh = rh + 1 == P.ring_cap ? 0u : rh + 1u;
-                    --rn;
-                }
-                fetch_head();
-            }
-        }
-        __syncwarp();
-        // ---- FIN: the unit's result (96 B) and totals; take the next unit ----
-        if (mode == 2) {
-            const uint32_t placements = K0 & 0xFFFFu, creates = K0 >> 16, destroys = K1 & 0xFFFFu, waits = K1 >> 16,
-                           rejected = K2 & 0xFFFFu, ooms = K2 >> 16, preempts = K3 & 0xFFFFu, failed = K3 >> 16;
-            const uint32_t completed = n - rejected - failed, restarts = ooms - failed + preempts;
-            const uint32_t makespan = t;
-            const uint64_t energy = (uint64_t)P.pol.idle_w * makespan + (uint64_t)P.pol.w_per_slice * a_busy;
-            if (P.out) {
-                uint4* o = reinterpret_cast<uint4*>(P.out + tr * P.n_pol_all + P.pol_idx);
-                o[0] = make_uint4(makespan, n, completed, rejected);
-                o[1] = make_uint4(failed, ooms, preempts, restarts);
-                o[2] = make_uint4(placements, waits, creates, destroys);
-                o[3] = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)a_turn,
-                                  (uint32_t)(a_turn >> 32));
-                o[4] = make_uint4((uint32_t)a_busy, (uint32_t)(a_busy >> 32), hl, hh);
-                o[5] = make_uint4((uint32_t)a_mem, (uint32_t)(a_mem >> 32), (uint32_t)a_waste,
-                                  (uint32_t)(a_waste >> 32));
-            }
-            {  // a12: 32-bit counts by shared atomics, 64-bit sums in this lane's partial slots
-                uint32_t* c = S.c32;
-                atomicAdd(c + 0, 1u);
-                atomicAdd(c + 1, n);
-                if (rejected) atomicAdd(c + 2, rejected);
-                if (failed) atomicAdd(c + 3, failed);
-                if (ooms) atomicAdd(c + 4, ooms);
-                if (preempts) atomicAdd(c + 5, preempts);
-                atomicAdd(c + 6, placements);
-                if (waits) atomicAdd(c + 7, waits);
-                if (creates) atomicAdd(c + 8, creates);
-                if (destroys) atomicAdd(c + 9, destroys);
-                atomicMax(c + 10, makespan);
-                if (err) atomicOr(c + 11, err);
-                unsigned long long* d = P.part + (size_t)blockIdx.x * kT64 * kLaneThreads + tid;
-                d[0 * kLaneThreads] += makespan;
-                d[1 * kLaneThreads] += a_turn;
-                d[2 * kLaneThreads] += a_busy;
-                d[3 * kLaneThreads] += ((unsigned long long)hh << 32) | hl;
-                d[4 * kLaneThreads] += a_mem;
-                d[5 * kLaneThreads] += a_waste;
-            }
-            tr = s_next[tid];
-            if (tr < P.n_traces) {
-                s_next[tid] = atomicAdd(P.counter, 1ull);
-                init_unit();
-            } else {
-                active = false;
-                mode = 3;
-            }
-        }
-    }
-#undef FF_RING
-    __syncthreads();
-    if (P.totals) {
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);
-        if (tid == 0 && blockIdx.x == 0 && P.est_err && *P.est_err) atomicOr(dst + 20, *P.est_err);
-        __shared__ unsigned long long red[24];
-        if (tid < kT32 + kT64) {
-            unsigned long long v = 0;
-            if (tid < kT32) {
-                v = S.c32[tid];
-            } else {
-                const unsigned long long* row = P.part + ((size_t)blockIdx.x * kT64 + (tid - kT32)) * kLaneThreads;
-                for (int k = 0; k < kLaneThreads; ++k) v += row[k];
-            }
-            red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
-        }
-        __syncthreads();
-        if (tid < 21) {
-            unsigned long long v;
-            if (tid == 2) v = red[1] - red[3] - red[4];
-            else if (tid == 7) v = red[5] - red[4] + red[6];
-            else if (tid == 14) v = (unsigned long long)P.pol.idle_w * red[12] + (unsigned long long)P.pol.w_per_slice * red[16];
-            else v = red[tid];
-            if (v) {
-                if (tid == 13) atomicMax(dst + 13, v);
-                else if (tid == 20) atomicOr(dst + 20, v);
-                else atomicAdd(dst + tid, v);
-            }
-        }
-    }
-}
-
-// ================================================================================================================
-// k_base_lane: the BASELINE launch of the common case (no extension records, no policy flags, no arrival streams).
-// BASELINE is an in-order fold over the queue: each job waits for the previous one on the whole
-// GPU, so a trace is one pass over its records with no event queue. One lane per trace; a warp takes 32 consecutive
-// traces and advances them one job per iteration in lockstep (the record of job k+1 is loaded while job k is
-// folded). Records, counters and results are those of k_simulate_lane<MIG_BASELINE> (same parity suites):
-//   per job j, at tick t:  REJECT(j) if no profile holds it; else [WAIT(j) at t, the previous run's end at its end
-//   tick (COMPLETE, or OOM + FAILED on the whole GPU), t = that tick] then PLACE_BASELINE(j) at t.
-// ================================================================================================================
-#ifndef BASE_MINB
-#define BASE_MINB 8
-#endif
-__global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
-    __shared__ uint32_t c32[kT32];
-    const uint32_t tid = threadIdx.x, lane = tid & 31u;
-    if (tid < kT32) c32[tid] = 0;
-#pragma unroll
-    for (int f = 0; f < kT64; ++f) P.part[((size_t)blockIdx.x * kT64 + f) * kLaneThreads + tid] = 0;
-    const uint32_t fp = __ldg(&Gg->full_prof);
-    const uint32_t fsi = __ldg(&Gg->pinfo[fp]);
-    const uint32_t flev = fsi & 0xFu, fcomp = (fsi >> 4) & 0xFu, fcap = __ldg(&Gg->level_mem[flev]);
-    const uint32_t mem0 = __ldg(&Gg->mem[0]);
-    const uint32_t ctx = P.ctx;
-    const uint64_t jbase = P.off[0];
-    __syncthreads();
-    unsigned long long p_make = 0, p_turn = 0, p_busy = 0, p_hash = 0, p_mem = 0, p_waste = 0;
-    for (;;) {
-        unsigned long long w0 = 0;
-        if (lane == 0) w0 = atomicAdd(P.counter, 32ull);
-        w0 = __shfl_sync(FULL, w0, 0);
-        if (w0 >= P.n_traces) break;
-        const unsigned long long tr = w0 + lane;
-        const bool act = tr < P.n_traces;
-        uint64_t j0 = 0;
-        uint32_t n = 0, err = 0;
-        if (act) {
-            const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
-            j0 = o0 - jbase;
-            n = (uint32_t)(o1 - o0);
-            if (o1 - o0 > P.max_jobs) {
-                err = (uint32_t)MIG_ERR_TRACE_TOO_LONG;
-                n = 0;
-            }
-        }
-        const uint32_t nmax = __reduce_max_sync(FULL, n);
-        uint32_t t = 0, bend = 0, bjob = 0, hl = (uint32_t)kFnvOffset, hh = (uint32_t)(kFnvOffset >> 32);
-        uint32_t placements = 0, waits = 0, rejected = 0, failed = 0;
-        bool busy = false, boom = false;
-        unsigned long long a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
-        const uint4* rec = P.jobs + j0;
-        uint4 r = n ? __ldg(rec) : make_uint4(0, 0, 0, 0);
-        for (uint32_t k = 0; k < nmax; ++k) {
-            const uint4 rn = (k + 1 < n) ? __ldg(rec + k + 1) : make_uint4(0, 0, 0, 0);  // one ahead
-            if (k < n) {
-                const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu, j = k;
-                if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
-                const uint32_t need = ff_fit(P, cls == kClassDynamic ? mem0 : r.x + ctx);  // R16 / est + ctx
-                if (need == kNoNeed) {  // no profile can ever hold the job: REJECT (no wait)
-                    lrec(hl, hh, t, (j << 16) | (K_REJECT << 12) | 0xFF0u);
-                    ++rejected;
-                } else {
-                    if (busy) {  // the head waits for the running job, then its end event
-                        lrec(hl, hh, t, (j << 16) | (K_WAIT << 12) | 0xF00u | (need << 4));
-                        ++waits;
-                        t = bend;
-                        const uint32_t lo = (bjob << 16) | (fp << 4);
-                        if (boom) {  // OOM on the whole GPU = FAILED
-                            lrec(hl, hh, t, lo | (K_OOM << 12));
-                            lrec(hl, hh, t, lo | (K_FAILED << 12));
-                            ++failed;
-                        } else {
-                            lrec(hl, hh, t, lo | (K_COMPLETE << 12));
-                            a_turn += t;
-                        }
-                    }
-                    lrec(hl, hh, t, (j << 16) | (K_PLACE_BASELINE << 12) | (fp << 4));
-                    ++placements;
-                    // start_run on the whole GPU (OOM > COMPLETE in one iteration, R29)
-                    const uint32_t ticks = r.w;
-                    uint32_t dur, ek, it;
-                    if (cls != kClassDynamic) {
-                        const uint32_t phys = r.y + ctx < r.y ? 0xFFFFFFFFu : r.y + ctx;
-                        ek = (T >= 1 && phys > fcap) ? 1u : 0u;  // R12: static jobs OOM at iteration 1
-                        it = ek ? 1u : T;
-                        dur = it * ticks;
-                        a_mem += (uint64_t)phys * dur;
-                    } else if (P.est) {
-                        const mig_job_estimate* ej = P.est + j0 + j;
-                        const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + flev);
-                        ek = fe <= T ? 1u : 0u;
-                        it = ek ? fe : T;
-                        dur = it * ticks;
-                        a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? flev : 6u)) * ticks;
-                    } else {  // DYNAMIC under MIG_TRACES_NO_DYNAMIC: flagged, no forecast
-                        err |= (uint32_t)MIG_ERR_BAD_RECORD;
-                        ek = 0;
-                        it = T;
-                        dur = T * ticks;
-                    }
-                    if (((uint64_t)it * ticks + t) >> 32) err |= (uint32_t)MIG_ERR_TICK_OVERFLOW;  // u32 ticks
-                    a_busy += (uint64_t)fcomp * dur;
-                    if (ek) a_waste += dur;
-                    bend = t + dur;
-                    bjob = j;
-                    boom = ek != 0;
-                    busy = true;
-                }
-            }
-            r = rn;
-        }
-        if (busy) {  // the last run's end
-            t = bend;
-            const uint32_t lo = (bjob << 16) | (fp << 4);
-            if (boom) {
-                lrec(hl, hh, t, lo | (K_OOM << 12));
-                lrec(hl, hh, t, lo | (K_FAILED << 12));
-                ++failed;
-            } else {
-                lrec(hl, hh, t, lo | (K_COMPLETE << 12));
-                a_turn += t;
-            }
-        }
-        if (act) {
-            const uint32_t ooms = failed, completed = n - rejected - failed, makespan = t;
-            const uint64_t energy = (uint64_t)P.pol.idle_w * makespan + (uint64_t)P.pol.w_per_slice * a_busy;
-            if (P.out) {
-                uint4* o = reinterpret_cast<uint4*>(P.out + tr * P.n_pol_all + P.pol_idx);
-                o[0] = make_uint4(makespan, n, completed, rejected);
-                o[1] = make_uint4(failed, ooms, 0u, ooms - failed);
-                o[2] = make_uint4(placements, waits, 0u, 0u);
-                o[3] = make_uint4((uint32_t)energy, (uint32_t)(energy >> 32), (uint32_t)a_turn,
-                                  (uint32_t)(a_turn >> 32));
-                o[4] = make_uint4((uint32_t)a_busy, (uint32_t)(a_busy >> 32), hl, hh);
-                o[5] = make_uint4((uint32_t)a_mem, (uint32_t)(a_mem >> 32), (uint32_t)a_waste,
-                                  (uint32_t)(a_waste >> 32));
-            }
-            atomicAdd(c32 + 0, 1u);
-            atomicAdd(c32 + 1, n);
-            if (rejected) atomicAdd(c32 + 2, rejected);
-            if (failed) {
-                atomicAdd(c32 + 3, failed);
-                atomicAdd(c32 + 4, ooms);
-            }
-            atomicAdd(c32 + 6, placements);
-            if (waits) atomicAdd(c32 + 7, waits);
-            atomicMax(c32 + 10, makespan);
-            if (err) atomicOr(c32 + 11, err);
-            p_make += makespan;
-            p_turn += a_turn;
-            p_busy += a_busy;
-            p_hash += ((unsigned long long)hh << 32) | hl;
-            p_mem += a_mem;
-            p_waste += a_waste;
-        }
-    }
-    {
-        unsigned long long* d = P.part + (size_t)blockIdx.x * kT64 * kLaneThreads + tid;
-        d[0 * kLaneThreads] = p_make;
-        d[1 * kLaneThreads] = p_turn;
-        d[2 * kLaneThreads] = p_busy;
-        d[3 * kLaneThreads] = p_hash;
-        d[4 * kLaneThreads] = p_mem;
-        d[5 * kLaneThreads] = p_waste;
-    }
-    __syncthreads();
-    if (P.totals) {
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(P.totals + P.pol_idx);
-        if (tid == 0 && blockIdx.x == 0 && P.est_err && *P.est_err) atomicOr(dst + 20, *P.est_err);
-        __shared__ unsigned long long red[24];
-        if (tid < kT32 + kT64) {
-            unsigned long long v = 0;
-            if (tid < kT32) {
-                v = c32[tid];
-            } else {
-                const unsigned long long* row = P.part + ((size_t)blockIdx.x * kT64 + (tid - kT32)) * kLaneThreads;
-                for (int k = 0; k < kLaneThreads; ++k) v += row[k];
-            }
-            red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
-        }
-        __syncthreads();
-        if (tid < 21) {
-            unsigned long long v;
-            if (tid == 2) v = red[1] - red[3] - red[4];
-            else if (tid == 7) v = red[5] - red[4] + red[6];
-            else if (tid == 14) v = (unsigned long long)P.pol.idle_w * red[12] + (unsigned long long)P.pol.w_per_slice * red[16];
-            else v = red[tid];
-            if (v) {
-                if (tid == 13) atomicMax(dst + 13, v);
-                else if (tid == 20) atomicOr(dst + 20, v);
-                else atomicAdd(dst + tid, v);
-            }
-        }
-    }
-}
-
-// ================================================================================================================
-// k_sa_group: Scheme A's grouping pass (sorted_by_mig_group, reading R38) as its own launch before
-// the Scheme A lane launch. One lane per trace, a warp takes 32 consecutive traces and walks their job records in
-// lockstep (coalesced enough, no event loop): the t = 0 REJECT records (queue order) go into the trace's decision
-// hash, and the records are written in group order (ascending memory level of the tight fit, queue order within a
-// level) with their x word replaced by the job index, so the lane kernel dispatches each group by reading the next
-// record of the group sequentially instead of re-reading records by job index. Per trace: sa_hdr[2t]
-// = {len0 | len1 << 16, len2 | len3 << 16, len4 | rejected << 16, error bits}, sa_hdr[2t + 1] = {hash lo, hash hi}.
-// Pass 1 counts the groups (and the REJECT hash), pass 2 scatters (the trace's records are re-read from L2).
-// ================================================================================================================
-template <bool XR>
-__global__ void __launch_bounds__(kLaneThreads) k_sa_group(const DevGeom* __restrict__ Gg, const LaneParams P,
-                                                          uint4* desc, uint4* dext, uint4* hdr) {
-    __shared__ uint32_t s_lmem[8];
-    __shared__ uint8_t s_first[8];
-    __shared__ DevGeom sG;
-    const uint32_t tid = threadIdx.x, lane = tid & 31u;
-    {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(Gg);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(&sG);
-        for (uint32_t i = tid; i < sizeof(DevGeom) / 4; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
-    __syncthreads();
-    const DevGeom& G = sG;
-    if (tid < 8) {
-        uint32_t f = 0xFFu;
-        for (uint32_t p = G.n_prof; p-- > 0;)
-            if (G.level[p] == tid) f = p;
-        s_first[tid] = (uint8_t)(tid < G.n_levels ? f : 0xFFu);
-        s_lmem[tid] = tid < G.n_levels ? G.level_mem[tid] : 0xFFFFFFFFu;
-    }
-    __syncthreads();
-    const bool fold = (P.pol.flags & MIG_WARP_FOLD) != 0;
-    // the tight fit of lane_tight_fit<MIG_SCHEME_A> (R6, R30)
-    auto fit = [&](uint32_t req, uint32_t warps) -> uint32_t {
-        if (!fold || warps == 0) {
-            uint32_t L = s_lmem[3] < req ? 4u : 0u;
-            L += s_lmem[L + 1] < req ? 2u : 0u;
-            L += s_lmem[L] < req ? 1u : 0u;
-            return s_first[L];
-        }
-        const uint32_t cf = G.wave_cap[G.full_prof];
-        for (uint32_t p = 0; p < G.n_prof; ++p) {
-            if (G.mem[p] < req) continue;
-            const uint32_t cp = G.wave_cap[p];
-            if ((warps + cp - 1) / cp != (warps + cf - 1) / cf) continue;
-            return p;
-        }
-        return kNoNeed;
-    };
-    const uint64_t jbase = P.off[0];
-    const uint32_t ctx = P.ctx, mem0 = G.mem[0];
-    const uint32_t lt = (1u << lane) - 1u;  // lanes below this one
-    // one warp per trace: its records 32 at a time (coalesced), the tight fits in parallel, the group positions by
-    // ballots; the REJECT records (rare) folded into the hash in queue order by lane 0
-    for (unsigned long long tr = blockIdx.x * (kLaneThreads / 32) + (tid >> 5); tr < P.n_traces;
-         tr += (unsigned long long)gridDim.x * (kLaneThreads / 32)) {
-        const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1], j0 = o0 - jbase;
-        uint32_t n = (uint32_t)(o1 - o0), err = 0;
-        if (o1 - o0 > P.max_jobs) {
-            err = (uint32_t)MIG_ERR_TRACE_TOO_LONG;
-            n = 0;
-        }
-        uint32_t hl = (uint32_t)kFnvOffset, hh = (uint32_t)(kFnvOffset >> 32), rej = 0;
-        uint32_t cnt[5] = {0, 0, 0, 0, 0};
-        auto need_of = [&](uint32_t k, uint4& r, uint4& e) -> uint32_t {
-            r = __ldg(P.jobs + j0 + k);
-            e = XR ? __ldg(P.ext + j0 + k) : make_uint4(0, 0, 0, 0);
-            const uint32_t cls = (r.z >> 16) & 0xFFu;
-            return fit(cls == kClassDynamic ? mem0 : r.x + e.x + ctx, e.y);  // R16 / est + ws + ctx
-        };
-        for (uint32_t c = 0; c < n; c += 32) {  // pass 1: REJECTs in queue order, group sizes
-            const uint32_t k = c + lane;
-            uint32_t lv = 0xFFu;
-            bool rj = false;
-            if (k < n) {
-                uint4 r, e;
-                const uint32_t need = need_of(k, r, e);
-                const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu;
-                if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
-                rj = need == kNoNeed;
-                if (!rj) lv = G.level[need];
-            }
-            uint32_t rm = __ballot_sync(FULL, rj);
-            rej += __popc(rm);
-            while (rm) {  // lane-uniform loop over this chunk's REJECTs, in queue order
-                const uint32_t q = (uint32_t)__ffs(rm) - 1u;
-                rm &= rm - 1u;
-                lrec(hl, hh, 0u, ((c + q) << 16) | (K_REJECT << 12) | 0xFF0u);
-            }
-#pragma unroll
-            for (int l = 0; l < 5; ++l) cnt[l] += __popc(__ballot_sync(FULL, lv == (uint32_t)l));
-        }
-        uint32_t pos[5];
-        pos[0] = 0;
-#pragma unroll
-        for (int l = 1; l < 5; ++l) pos[l] = pos[l - 1] + cnt[l - 1];
-        for (uint32_t c = 0; c < n; c += 32) {  // pass 2: the records in group order, x = the job index
-            const uint32_t k = c + lane;
-            uint4 r = make_uint4(0, 0, 0, 0), e = r;
-            uint32_t lv = 0xFFu;
-            if (k < n) {
-                const uint32_t need = need_of(k, r, e);
-                if (need != kNoNeed) lv = G.level[need];
-            }
-            uint32_t at = 0;
-#pragma unroll
-            for (int l = 0; l < 5; ++l) {
-                const uint32_t m = __ballot_sync(FULL, lv == (uint32_t)l);
-                if (lv == (uint32_t)l) at = pos[l] + __popc(m & lt);
-                pos[l] += __popc(m);
-            }
-            if (lv != 0xFFu) {
-                r.x = k;
-                desc[j0 + at] = r;
-                if (XR) dext[j0 + at] = e;
-            }
-        }
-        err = __reduce_or_sync(FULL, err);
-        if (lane == 0) {
-            hdr[2 * tr] = make_uint4(cnt[0] | (cnt[1] << 16), cnt[2] | (cnt[3] << 16), cnt[4] | (rej << 16), err);
-            hdr[2 * tr + 1] = make_uint4(hl, hh, 0u, 0u);
-        }
-    }
+    lane_flush_totals(P, S.c32);
 }
 
 // MIG_SA_PREGROUP=0: Scheme A's grouping pass inside the lane kernel instead of k_sa_group (A/B and parity).
@@ -1765,14 +935,6 @@ static int lane_per_sm() {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_simulate_lane<KIND, false>, kLaneThreads, 0);
     return per_sm < 1 ? 1 : per_sm;
-}
-
-// Grid: resident CTAs per SM x SMs (persistent; units are taken from the counter), capped by the unit count.
-static uint64_t lane_blocks(int per_sm, uint64_t n_traces, int sm_count) {
-    uint64_t blocks = (uint64_t)per_sm * sm_count;
-    const uint64_t want = (n_traces + kLaneThreads - 1) / kLaneThreads;
-    if (want < blocks) blocks = want;
-    return blocks < 1 ? 1 : blocks;
 }
 
 // The largest grid of any kind (sizes the per-lane scratch shared by the launches of one call).
@@ -1838,29 +1000,11 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
             lf |= f << (4 * l);
         }
         P.lfirst = lf;
-        if (pol.kind == MIG_BASELINE) {
-            static int b_per_sm = 0;
-            if (!b_per_sm) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b_per_sm, k_base_lane, kLaneThreads, 0);
-                if (b_per_sm < 1) b_per_sm = 1;
-            }
-            const dim3 g3((unsigned)std::min<uint64_t>(blocks, lane_blocks(b_per_sm, tr.n_traces, sm_count)));
-            k_base_lane<<<g3, block, 0, stream>>>(Gdev, P);
-            return cudaGetLastError();
-        }
-        static int ff_per_sm = 0;
-        if (!ff_per_sm) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ff_per_sm, k_ff_lane<8>, kLaneThreads, 0);
-            if (ff_per_sm < 1) ff_per_sm = 1;
-        }
-        const dim3 g2((unsigned)std::min<uint64_t>(blocks, lane_blocks(ff_per_sm, tr.n_traces, sm_count)));
+        if (pol.kind == MIG_BASELINE) return launch_base_lane(Gdev, P, blocks, sm_count, stream);
         uint32_t ns = 0;  // one past the highest start slot of any placement
         for (uint32_t p = 0; p < Gh->n_prof; ++p)
             for (uint32_t k = 0; k < Gh->n_place[p]; ++k) ns = std::max(ns, (Gh->place[p][k] & 0xFFu) + 1u);
-        if (ns <= 4) k_ff_lane<4><<<g2, block, 0, stream>>>(Gdev, P);
-        else if (ns <= 7) k_ff_lane<7><<<g2, block, 0, stream>>>(Gdev, P);
-        else k_ff_lane<8><<<g2, block, 0, stream>>>(Gdev, P);
-        return cudaGetLastError();
+        return launch_ff_lane(Gdev, P, ns, blocks, sm_count, stream);
     }
     switch (pol.kind) {
         case MIG_BASELINE:
@@ -1899,13 +1043,7 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                 P.sa_desc = reinterpret_cast<const uint4*>(sa);
                 P.sa_dext = P.ext ? reinterpret_cast<const uint4*>(sa + b_desc) : nullptr;
                 P.sa_hdr = reinterpret_cast<const uint4*>(sa + b_desc + b_dext);
-                const unsigned gg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sm_count * 16,
-                                                                                     (nt + 3) / 4));
-                if (P.ext)
-                    k_sa_group<true><<<gg, block, 0, stream>>>(Gdev, P, (uint4*)P.sa_desc, (uint4*)P.sa_dext, (uint4*)P.sa_hdr);
-                else
-                    k_sa_group<false><<<gg, block, 0, stream>>>(Gdev, P, (uint4*)P.sa_desc, nullptr, (uint4*)P.sa_hdr);
-                e2 = cudaGetLastError();
+                e2 = launch_sa_group(Gdev, P, (uint4*)P.sa_desc, (uint4*)P.sa_dext, (uint4*)P.sa_hdr, sm_count, stream);
                 if (e2 == cudaSuccess) {
                     if (P.ext) k_simulate_lane<MIG_SCHEME_A, false><<<grid, block, 0, stream>>>(Gdev, P);
                     else if (pf) k_simulate_lane<MIG_SCHEME_A, false, false, true><<<grid, block, 0, stream>>>(Gdev, P);

@@ -1,5 +1,6 @@
 """Build A/B variants of libmig.so into build/var/<name>.so: every source compiled once (build/obj), and
-simulate_lane.cu recompiled per variant with extra -D flags. Usage:
+one source (VAR_SRC, default simulate_lane.cu; simulate_ff.cu for k_ff_lane / k_base_lane) recompiled per variant
+with extra -D flags. Usage:
   python tools/build_variants.py name1='-DFOO=1' name2='-DFOO=2' ...   (then: gpurun -- 'bash tools/gpu_ab.sh')"""
 import os
 import subprocess
