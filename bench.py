@@ -215,29 +215,36 @@ class Workload:
             self.dyn_samples = int(((zf & 0xFFFF) * dyn.to(torch.int64)).sum().item())
             self.n_dyn_jobs = int(dyn.sum().item())
             self.n_jobs = self.tr.n_jobs
-            self.fits = 0
-            if self.n_dyn_jobs:  # fits until convergence (§8(d)), from one estimator call outside the timed region
-                est = mig.mig_estimate_memory(self.g, self.tr, self.pols[0])
-                conv = est.view(-1, 80)[:, 8:10].contiguous().view(torch.int16).to(torch.int64).view(-1) & 0xFFFF
-                T = zf & 0xFFFF
-                min_n = int(self.pols[0].min_n)
-                f = torch.where(conv > 0, conv - min_n + 1, (T - min_n + 1).clamp(min=0))
-                self.fits = int((f * dyn.to(torch.int64)).sum().item())
-                del est, conv, T, f
+            self.fits = self._fits(self.jobs, self.ext, self.off, n, t_id0, zf, dyn) if self.n_dyn_jobs else 0
         else:  # the units the roofline counts, from one pass of the generator over the shard (not timed)
             self.res = None
             self.n_jobs = n * self.J
             self.dyn_samples = self.n_dyn_jobs = self.fits = 0
             for c0 in range(0, n, chunk):
                 m = min(chunk, n - c0)
-                j, _, _ = tg.generate_device(cfg, m, trace_id0=t_id0 + c0, seed=self.seed, device=dev)
+                j, e, o = tg.generate_device(cfg, m, trace_id0=t_id0 + c0, seed=self.seed, device=dev)
                 zf = j[:, 2].to(torch.int64)
                 dyn = ((zf >> 16) & 0xFF) == 2
                 self.dyn_samples += int(((zf & 0xFFFF) * dyn.to(torch.int64)).sum().item())
                 self.n_dyn_jobs += int(dyn.sum().item())
-                del j, zf, dyn
+                if bool(dyn.any()):
+                    self.fits += self._fits(j, e, o, m, t_id0 + c0, zf, dyn)
+                del j, e, o, zf, dyn
         self.launches = 0
         self.gen_ms = 0.0
+
+    def _fits(self, jobs, ext, off, n, t_id0, zf, dyn):
+        """Fits until convergence (§8(d)) of the shard's DYNAMIC jobs, from one estimator call outside the timed
+        region: conv - min_n + 1 for a converged job, T - min_n + 1 otherwise."""
+        import torch
+
+        tr = self.mig.Traces(jobs, ext, off, n, seed=self.seed, trace_id0=t_id0, max_jobs=self.J)
+        est = self.mig.mig_estimate_memory(self.g, tr, self.pols[0])
+        conv = est.view(-1, 80)[:, 8:10].contiguous().view(torch.int16).to(torch.int64).view(-1) & 0xFFFF
+        T = zf & 0xFFFF
+        min_n = int(self.pols[0].min_n)
+        f = torch.where(conv > 0, conv - min_n + 1, (T - min_n + 1).clamp(min=0))
+        return int((f * dyn.to(torch.int64)).sum().item())
 
     def step(self, world, dist):
         import torch
@@ -352,7 +359,7 @@ def roofline(wl, ktimes, steps, totals, world, peaks, peak_src, ncu):
         ops = (OPS_PER_DYN_ITER * dyn_samples + OPS_PER_FIT * (wl.fits or 0)) / n_l
         byts = ((JOB_BYTES + ext_b) * wl.n_jobs + EST_BYTES * (wl.n_dyn_jobs or 0)) / n_l
         ops_desc = (f"{OPS_PER_DYN_ITER} ops per DYNAMIC-job sample scanned + {OPS_PER_FIT} per fit until "
-                    f"convergence ({wl.fits} fits; chunked shards: samples only)")
+                    f"convergence ({wl.fits} fits)")
         bytes_desc = f"{JOB_BYTES + ext_b} B/job read + {EST_BYTES} B per DYNAMIC job written"
         kname = "k_estimate"
     else:
