@@ -228,7 +228,8 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     bool done_pred = T < P.min_n;
     bool bad = false;
     // generated series whose range bounds already satisfy the predictor's input limits skip the per-sample checks
-    // (y < 2^18, 0 < q < 2^26): y <= b + slope*T/256 + the largest Irwin-Hall draw + 1, q grows from q0 by qs
+    // (y < 2^18, 0 < q < 2^26): y <= b + slope*T/256 + the largest Irwin-Hall draw + 1, q grows from q0 by qs (the
+    // draw is at most 510 * sigma * 7094 / 2^20; 131070 / 2^28 = 511.99 / 2^20 bounds it)
     const uint64_t y_hi = (uint64_t)b + (((uint64_t)slope * T) >> 8) +
                           (((uint64_t)131070u * ((sigma_n & 0xFFFFu) * 7094u)) >> 28) + 2u;
     const bool check = rec_samples || y_hi >= (1u << 18) || q0 == 0 || (uint64_t)q0 + (uint64_t)qs * T >= (1u << 26);

@@ -67,7 +67,7 @@ def test_config_has_dynamic_table():
 
 
 def test_dyn_sample_noise_shape():
-    # the per-iteration draw (tg_iter_bits: two 32-bit counter hashes) gives Irwin-Hall(4) noise: symmetric, with
+    # the per-iteration draw (tg_iter_bits: one 32-bit counter hash, Irwin-Hall(4) over its bytes) gives noise: symmetric, with
     # the normal's central masses (68.3% within 1 sigma, 95.4% within 2; Irwin-Hall(4): 67.8% / 95.8%), and no
     # lag-1 correlation between consecutive iterations
     sig = 1000

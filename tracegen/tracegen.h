@@ -69,17 +69,6 @@ TG_HD uint32_t tg_octave(uint64_t r, uint32_t a, uint32_t b) {
     return (1u << e) + (uint32_t)(((r & 0xFFFFFFFFull) * (uint64_t)(1u << e)) >> 32);
 }
 
-/* Irwin-Hall(4) noise with standard deviation ~sigma: (sum of four 16-bit uniforms - 131070) has standard
- * deviation 37837.6 = 2^28 / 7094.3, so noise = floor((sum - 131070) * (sigma * 7094) / 2^28) (one 32x32->64
- * multiply and an arithmetic shift; sigma < 2^16). No log/cos/division, so host and device are bit-identical. */
-TG_HD int32_t tg_irwin_hall(uint64_t r, uint32_t sigma) {
-    int32_t s = (int32_t)(r & 0xFFFF) + (int32_t)((r >> 16) & 0xFFFF) + (int32_t)((r >> 32) & 0xFFFF) +
-                (int32_t)((r >> 48) & 0xFFFF);
-    /* floor((s - 131070) * m / 2^28) written as the high word of 16 (s - 131070) * m (|16 (s - 131070)| < 2^21):
-     * the same integer, one multiply-high on 32-bit ALUs */
-    return (int32_t)(((int64_t)((s - 131070) * 16) * (int64_t)(int32_t)((sigma & 0xFFFFu) * 7094u)) >> 32);
-}
-
 /* 32-bit integer hash ("lowbias32", C. Wellons 2018: two multiplies, three xorshifts). */
 TG_HD uint32_t tg_hash32(uint32_t x) {
     x ^= x >> 16;
@@ -90,15 +79,25 @@ TG_HD uint32_t tg_hash32(uint32_t x) {
     return x;
 }
 
-/* The 64 random bits of iteration i of a DYNAMIC job's sample stream: two 32-bit counter hashes keyed by the two
- * halves of the job's splitmix64 key. The per-iteration draw is the hot part of generating a series in-kernel
- * (SURVEY.md §8(d) budgets ~15 ops for RNG + Irwin-Hall per iteration); splitmix64's 64-bit multiplies cost ~30
- * 32-bit instructions, these two hashes ~16. */
-TG_HD uint64_t tg_iter_bits(uint64_t job_key, uint32_t i) {
-    const uint32_t c = i * 0x9E3779B9u;
-    const uint32_t h1 = tg_hash32((uint32_t)job_key ^ c);
-    const uint32_t h2 = tg_hash32((uint32_t)(job_key >> 32) + c);
-    return ((uint64_t)h2 << 32) | h1;
+/* The 32 random bits of iteration i of a DYNAMIC job's sample stream: one counter hash keyed by both halves of the
+ * job's splitmix64 key. The per-iteration draw is the hot part of generating a series in-kernel (SURVEY.md §8(d)
+ * budgets ~15 ops for RNG + Irwin-Hall per iteration): one hash, ~10 32-bit instructions. */
+TG_HD uint32_t tg_iter_bits(uint64_t job_key, uint32_t i) {
+    return tg_hash32(((uint32_t)job_key ^ (i * 0x9E3779B9u)) + (uint32_t)(job_key >> 32));
+}
+
+/* Irwin-Hall(4) noise with standard deviation ~sigma from the four bytes of r: (sum of four 8-bit uniforms - 510)
+ * * 256 has standard deviation 37837.6 = 2^28 / 7094.3, so noise = floor((sum - 510) * 256 * (sigma * 7094) / 2^28),
+ * written as the high word of 4096 (sum - 510) * (sigma * 7094) (|4096 (sum - 510)| < 2^21; sigma < 2^16): one
+ * 32x32->64 multiply. |noise| <= 510 * 65535 * 7094 / 2^20 < 2^18. The byte sum is one dp4a on the device. No
+ * log/cos/division, so host and device are bit-identical. */
+TG_HD int32_t tg_irwin_hall(uint32_t r, uint32_t sigma) {
+#ifdef __CUDA_ARCH__
+    const int32_t s = (int32_t)__dp4a(r, 0x01010101u, 0u);
+#else
+    const int32_t s = (int32_t)((r & 0xFFu) + ((r >> 8) & 0xFFu) + ((r >> 16) & 0xFFu) + (r >> 24));
+#endif
+    return (int32_t)(((int64_t)((s - 510) * 4096) * (int64_t)(int32_t)((sigma & 0xFFFFu) * 7094u)) >> 32);
 }
 
 /* Per-iteration sample i (1-based) of a DYNAMIC job: requested MiB y_i (allocator-rounded up to 2 MiB, >= 2) and
