@@ -1,8 +1,9 @@
-// simulate_ff.cu — the two specialised lane kernels of the common case (no extension records, no early restart /
-// warp folding / wave time, no arrival streams or PCIe contention): k_ff_lane (FUSION_FISSION) and k_base_lane
-// (BASELINE), SURVEY.md §8(a) rows a1, a4-a12. Same method, decision records, counters and results as the generic
-// k_simulate_lane (simulate_lane.cu), which keeps every other case; launch_simulate_lane picks these when they
-// apply (MIG_FF_FAST=0 disables them for A/B runs and parity of both paths).
+// simulate_ff.cu — the two specialised lane kernels of the common cases (no warp folding / wave time, no arrival
+// streams or PCIe contention): k_ff_lane (FUSION_FISSION, with or without early restart) and k_base_lane
+// (BASELINE), SURVEY.md §8(a) rows a1, a4-a12 (a9, a10). Both take extension records (XR: the workspace field joins
+// the estimate and the true footprint) as a template option. Same method, decision records, counters and results as
+// the generic k_simulate_lane (simulate_lane.cu), which keeps every other case; launch_simulate_lane picks these when
+// they apply (MIG_FF_FAST=0 disables them for A/B runs and parity of both paths).
 #include <algorithm>
 
 #include "lane_common.cuh"
@@ -10,10 +11,12 @@
 namespace mig {
 
 // ================================================================================================================
-// k_ff_lane: the FUSION_FISSION launch of the common case (no extension records, no early restart / warp folding /
-// wave time, no arrival streams or PCIe contention) written for the fewest issued instructions per step. Same
-// method, records, counters and results as k_simulate_lane<MIG_FUSION_FISSION, false, false, true> (parity-tested
-// against the oracle by the same suites); what differs is the bookkeeping:
+// k_ff_lane: the FUSION_FISSION launch of the common cases (no warp folding / wave time, no arrival streams or PCIe
+// contention) written for the fewest issued instructions per step. XR: extension records (their workspace field is
+// added to the record's estimate and true footprint when the record is fetched, R17); ER: MIG_EARLY_RESTART (a10,
+// a DYNAMIC job whose converged forecast exceeds its slice is preempted at the convergence iteration
+// and requeued for the forecast, R25). Same method, records, counters and results as k_simulate_lane
+// <MIG_FUSION_FISSION> (parity-tested against the oracle by the same suites); what differs is the bookkeeping:
 //  - the running instances' next events are 64-bit keys {end tick, kind, job, slot} in shared memory, so the next
 //    event of a lane (R28: tick, then COMPLETE < OOM < PREEMPT, then job id) is one unrolled minimum over the 8
 //    start slots, kept in a register (kmin) and refreshed only when an event retires; a tick's remaining events
@@ -26,7 +29,7 @@ namespace mig {
 struct FFShared {
     uint32_t pinfo[16];                 // level | comp << 4 | lenmask << 8 (DevGeom::pinfo)
     uint32_t level_mem[8], level_next[8];
-    uint32_t mem0;
+    uint32_t mem0, full_mem;
     uint8_t place_s[8][8];              // start slot of placement k of profile p
     uint8_t alloc[256 * 8];             // Alg. 2 by (occupancy, profile): start slot of the placement, 0xFF = FAIL
     uint32_t lmem[8];                   // level memories, padded with 0xFFFFFFFF (tight-fit binary search)
@@ -59,7 +62,7 @@ __device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
 #define FF_MINB 8
 #endif
 // NS: the start slots scanned for the next event (every placement of the geometry starts below NS; A100: 7).
-template <int NS>
+template <int NS, bool XR, bool ER>
 __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ __align__(16) FFShared S;
     const uint32_t tid = threadIdx.x;
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 cb += p < np ? 1u << __ldg(&G->n_place[p]) : 0u;
             }
             S.mem0 = __ldg(&G->mem[0]);
+            S.full_mem = __ldg(&G->full_mem);
         }
         if (tid < kT32) S.c32[tid] = 0;
 #pragma unroll
@@ -158,6 +162,11 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
             return;
         }
         hr = __ldg(P.jobs + j0 + hj);
+        if (XR) {  // est + ws and true + ws (the context is added where they are used; true saturates, mig.h)
+            const uint32_t ws = __ldg(&P.ext[j0 + hj].x);
+            hr.x += ws;
+            hr.y = hr.y + ws < hr.y ? 0xFFFFFFFFu : hr.y + ws;
+        }
     };
     auto init_unit = [&]() {
         const uint64_t o0 = P.off[tr], o1 = P.off[tr + 1];
@@ -196,12 +205,19 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 t = (uint32_t)(kmin >> 32);
                 const uint32_t epr = (prof4 >> (4 * es)) & 0xFu, si = S.pinfo[epr];
                 const uint32_t elo = (job << 16) | (es << 8) | (epr << 4);
-                lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7
+                lrec(hl, hh, t, elo | ((K_COMPLETE + ek) << 12));  // COMPLETE 6 / OOM 7 / PREEMPT 8
                 if (ek == 0) {
                     a_turn += t;
-                } else {  // OOM: next larger slice (R14) or FAILED on the whole GPU
-                    K2 += 1u << 16;
-                    const uint32_t req = S.level_next[si & 0xFu];
+                } else {  // OOM: next larger slice (R14) or FAILED on the whole GPU; PREEMPT (ER): the
+                          // converged forecast, at most the whole GPU (R25)
+                    uint32_t req;
+                    if (ER && ek == 2) {
+                        K3 += 1u;
+                        req = min(__ldg(&P.est[j0 + job].pred_mib), S.full_mem);
+                    } else {
+                        K2 += 1u << 16;
+                        req = S.level_next[si & 0xFu];
+                    }
                     if (req == 0) {
                         lrec(hl, hh, t, elo | (K_FAILED << 12));
                         K3 += 1u << 16;
@@ -308,10 +324,20 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 } else if (P.est) {
                     const mig_job_estimate* ej = P.est + j0 + j;
                     const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
-                    ek = fe <= T ? 1u : 0u;
-                    it = ek ? fe : T;
+                    if (ER) {  // a10: preempt at the convergence iteration when the forecast exceeds this slice
+                        const uint2 pc = __ldg(reinterpret_cast<const uint2*>(ej) + 0);  // (req0, pred)
+                        const uint32_t conv = __ldg(reinterpret_cast<const unsigned short*>(ej) + 4);
+                        const uint32_t cap = S.level_mem[lev];
+                        const uint32_t i_pre = (conv > 0 && pc.y > cap && cap < S.full_mem) ? conv : 0xFFFFFFFFu;
+                        ek = fe <= min(T, i_pre) ? 1u : i_pre < T ? 2u : 0u;  // R29: OOM > COMPLETE > PREEMPT
+                        it = ek == 1 ? fe : ek == 2 ? i_pre : T;
+                    } else {
+                        ek = fe <= T ? 1u : 0u;
+                        it = ek ? fe : T;
+                    }
                     dur = it * ticks;
-                    a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? lev : 6u)) * ticks;
+                    a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek == 1 ? lev : ek ? 5u : 6u)) *
+                             ticks;
                 } else {  // a DYNAMIC record under MIG_TRACES_NO_DYNAMIC (no estimates): flagged, no forecast
                     err |= (uint32_t)MIG_ERR_BAD_RECORD;
                     ek = 0;
@@ -404,6 +430,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
 #ifndef BASE_MINB
 #define BASE_MINB 8
 #endif
+template <bool XR>
 __global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     __shared__ uint32_t c32[kT32];
     const uint32_t tid = threadIdx.x, lane = tid & 31u;
@@ -442,9 +469,16 @@ __global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const Dev
         bool busy = false, boom = false;
         unsigned long long a_turn = 0, a_busy = 0, a_mem = 0, a_waste = 0;
         const uint4* rec = P.jobs + j0;
+        const uint4* xrec = XR ? P.ext + j0 : nullptr;
         uint4 r = n ? __ldg(rec) : make_uint4(0, 0, 0, 0);
+        uint32_t w = XR && n ? __ldg(&xrec[0].x) : 0u;  // the job's workspace MiB (extension record)
         for (uint32_t k = 0; k < nmax; ++k) {
             const uint4 rn = (k + 1 < n) ? __ldg(rec + k + 1) : make_uint4(0, 0, 0, 0);  // one ahead
+            const uint32_t wn = XR && k + 1 < n ? __ldg(&xrec[k + 1].x) : 0u;
+            if (XR) {  // est + ws, true + ws (saturating, as k_simulate_lane's 64-bit sum)
+                r.x += w;
+                r.y = r.y + w < r.y ? 0xFFFFFFFFu : r.y + w;
+            }
             if (k < n) {
                 const uint32_t cls = (r.z >> 16) & 0xFFu, T = r.z & 0xFFFFu, j = k;
                 if (cls > 2 || T > 4096) err |= (uint32_t)MIG_ERR_BAD_RECORD;
@@ -501,6 +535,7 @@ __global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const Dev
                 }
             }
             r = rn;
+            w = wn;
         }
         if (busy) {  // the last run's end
             t = bend;
@@ -564,14 +599,25 @@ cudaError_t launch_ff_lane(const DevGeom* Gdev, const LaneParams& P, uint32_t ns
                            cudaStream_t stream) {
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_lane<8>, kLaneThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_lane<8, true, true>, kLaneThreads, 0);
         if (per_sm < 1) per_sm = 1;
     }
     const dim3 grid((unsigned)std::min<uint64_t>(max_blocks, lane_blocks(per_sm, P.n_traces, sm_count))),
         block(kLaneThreads);
-    if (ns <= 4) k_ff_lane<4><<<grid, block, 0, stream>>>(Gdev, P);
-    else if (ns <= 7) k_ff_lane<7><<<grid, block, 0, stream>>>(Gdev, P);
-    else k_ff_lane<8><<<grid, block, 0, stream>>>(Gdev, P);
+    const bool xr = P.ext != nullptr, er = (P.pol.flags & MIG_EARLY_RESTART) != 0;
+#define FF_LAUNCH(NS_)                                                                     \
+    if (xr && er) k_ff_lane<NS_, true, true><<<grid, block, 0, stream>>>(Gdev, P);         \
+    else if (xr) k_ff_lane<NS_, true, false><<<grid, block, 0, stream>>>(Gdev, P);         \
+    else if (er) k_ff_lane<NS_, false, true><<<grid, block, 0, stream>>>(Gdev, P);         \
+    else k_ff_lane<NS_, false, false><<<grid, block, 0, stream>>>(Gdev, P);
+    if (ns <= 4) {
+        FF_LAUNCH(4)
+    } else if (ns <= 7) {
+        FF_LAUNCH(7)
+    } else {
+        FF_LAUNCH(8)
+    }
+#undef FF_LAUNCH
     return cudaGetLastError();
 }
 
@@ -579,11 +625,12 @@ cudaError_t launch_base_lane(const DevGeom* Gdev, const LaneParams& P, uint64_t 
                              cudaStream_t stream) {
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_base_lane, kLaneThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_base_lane<true>, kLaneThreads, 0);
         if (per_sm < 1) per_sm = 1;
     }
     const dim3 grid((unsigned)std::min<uint64_t>(max_blocks, lane_blocks(per_sm, P.n_traces, sm_count)));
-    k_base_lane<<<grid, kLaneThreads, 0, stream>>>(Gdev, P);
+    if (P.ext) k_base_lane<true><<<grid, kLaneThreads, 0, stream>>>(Gdev, P);
+    else k_base_lane<false><<<grid, kLaneThreads, 0, stream>>>(Gdev, P);
     return cudaGetLastError();
 }
 

@@ -988,7 +988,9 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     if (con && !P.pc) return cudaErrorInvalidValue;
     const bool ext = con || P.arr;  // the EXT instantiation: contention and / or arrival streams
     const bool pf = (pol.flags & (MIG_WARP_FOLD | MIG_EARLY_RESTART | MIG_WAVE_TIME)) == 0;
-    const bool fast = (pol.kind == MIG_FUSION_FISSION || pol.kind == MIG_BASELINE) && !ext && !P.ext && pf && Gh &&
+    // the fast kernels (simulate_ff.cu) take extension records and early restart, not warp folding or wave time
+    const bool ff_pf = (pol.flags & (MIG_WARP_FOLD | MIG_WAVE_TIME)) == 0;
+    const bool fast = (pol.kind == MIG_FUSION_FISSION || pol.kind == MIG_BASELINE) && !ext && ff_pf && Gh &&
                       ff_fast_enabled();
     if (fast) {
         for (int l = 0; l < kMaxLevels; ++l) P.lm[l] = l < (int)Gh->n_levels ? Gh->level_mem[l] : 0xFFFFFFFFu;
