@@ -44,7 +44,7 @@ struct FitOut {
 // exactly 1.0 at every sample, so its forecast is exactly 65536 and V = 1 (the canonical sequence gives the same).
 __device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int64_t Syy, int64_t Sq, int64_t Stq,
                                          int64_t T, double z, int64_t ws_ctx, bool q_unit, bool ewma, int64_t L,
-                                         bool small) {
+                                         bool small, bool n32) {
     const int64_t n2m1 = n * n - 1;
     const int64_t D = n * n2m1;
     const int64_t Ky = 2 * Sty - (n + 1) * Sy;
@@ -53,11 +53,15 @@ __device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int
     // conversion is the same single rounding as i128_to_double's
     const __int128 numY = small ? (__int128)0 : (__int128)Sy * n2m1 + (__int128)3 * Ky * h;
     const int64_t numY64 = small ? Sy * n2m1 + 3 * Ky * h : 0;
-    const __int128 ssrN = (__int128)n2m1 * (__int128)(n * Syy - Sy * Sy) - (__int128)3 * Ky * Ky;  // n*Syy, Sy^2 < 2^62
+    // n32 (small and n <= 32): Sy < 2^23, Syy < 2^41, |Ky| < 2^29, so every term of the residual sum is below 2^60 and
+    // it is exact in int64 (its conversion is the same single rounding as i128_to_double's)
+    const __int128 ssrN =
+        n32 ? (__int128)0 : (__int128)n2m1 * (__int128)(n * Syy - Sy * Sy) - (__int128)3 * Ky * Ky;  // n*Syy, Sy^2 < 2^62
+    const int64_t ssr64 = n32 ? n2m1 * (n * Syy - Sy * Sy) - 3 * Ky * Ky : 0;
     const double den = __ll2double_rn(D);
     FitOut f;
     const double yT = __ddiv_rn(small ? __ll2double_rn(numY64) : i128_to_double(numY), den);
-    const double var = __ddiv_rn(i128_to_double(ssrN), __ll2double_rn(D * (n - 2)));
+    const double var = __ddiv_rn(n32 ? __ll2double_rn(ssr64) : i128_to_double(ssrN), __ll2double_rn(D * (n - 2)));
     f.sigma = __dsqrt_rn(var);
     double u = __dadd_rn(yT, __dmul_rn(z, f.sigma));
     if (u < 0.0) u = 0.0;
@@ -146,8 +150,8 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
     uint64_t lvl = lnext < lend ? G.level_mem[lnext] : ~0ull;  // the level being watched (lnext)
     // W32 (no checks, ws + ctx < 2^31): every physical MiB is below 2^32, so the sums and tests run in 32 bits
     const uint32_t wc32 = (uint32_t)ws_ctx;
+    uint32_t n = base + lane + 1;  // this lane's iteration (carried, so the lane id is not re-read per chunk)
     auto chunk = [&](bool last) {
-        const uint32_t n = base + lane + 1;
         const bool valid = !last || n <= T;
         uint32_t y = 0, q = 0;
         if (valid) {
@@ -193,7 +197,7 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
         Smem += __reduce_add_sync(FULL, phys);
     };
     // full chunks need no per-lane bound test; the last (partial) chunk does
-    for (; base + 32 <= T; base += 32) chunk(false);
+    for (; base + 32 <= T; base += 32, n += 32) chunk(false);
     if (base < T) chunk(true);
 }
 
@@ -294,7 +298,9 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
         }
         const bool has = valid && n >= P.min_n;
         FitOut f = {0, 0.0, 0.0, 0.0};
-        if (has) f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit, ewma, myL, !check && T <= 4096);
+        if (has)
+            f = fit_at(ni, sy, sty, syy, sq, stq, T, P.z, ws_ctx, q_unit, ewma, myL, !check && T <= 4096,
+                       !check && T <= 4096 && base == 0);
         int64_t Pprev = __shfl_up_sync(FULL, f.P, 1);
         if (lane == 0) Pprev = Plast;
         const bool prev_has = n >= P.min_n + 1;
@@ -435,15 +441,10 @@ __global__ void __launch_bounds__(256, EST_MINB) k_estimate(const DevGeom G, con
                 // the batch trace holding job gL: the last trace whose first job is <= gL
                 const uint32_t tb = 31u - __clz(__ballot_sync(FULL, lane < nb && my_off <= gL));
                 const uint32_t jt = (uint32_t)(gL - __shfl_sync(FULL, my_off, tb));
-                uint4 rr, ee;
-                rr.x = __shfl_sync(FULL, r.x, L);
-                rr.y = __shfl_sync(FULL, r.y, L);
-                rr.z = __shfl_sync(FULL, r.z, L);
-                rr.w = __shfl_sync(FULL, r.w, L);
-                ee.x = __shfl_sync(FULL, e.x, L);
-                ee.y = __shfl_sync(FULL, e.y, L);
-                ee.z = __shfl_sync(FULL, e.z, L);
-                ee.w = __shfl_sync(FULL, e.w, L);
+                // the job's records again, one broadcast load each (L1 hits: the chunk just read them), so the chunk's
+                // records are not kept live across the job loop
+                const uint4 rr = __ldg(P.jobs + gL);
+                const uint4 ee = P.ext ? __ldg(P.ext + gL) : make_uint4(0, 0, 0, 0);
                 const uint2* rs = nullptr;
                 uint32_t rcount = 0;
                 if (P.samples) {

@@ -52,3 +52,43 @@ def test_phys_div_near_integer_quotients_and_edges():
     qs = np.array([1 << 16, (1 << 16) + 1, (1 << 26) - 1, (1 << 26) - 3, 1 << 16, 1 << 16, 65537, 196608, 65536,
                    65537], np.uint64)
     _check(ys, qs)
+
+
+def _wrap64(v):
+    """Two's-complement int64 wrap of a Python integer (what the device's int64 arithmetic yields)."""
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >= 1 << 63 else v
+
+
+def _ssr_int64_terms(y):
+    """The first chunk's residual sum (n <= 32) formed term by term in wrapping int64, as k_estimate's fit_at does
+    when n32 holds, next to the exact value: (n^2-1)(n Syy - Sy^2) - 3 Ky^2, Ky = 2 Sty - (n+1) Sy."""
+    out = []
+    Sy = Sty = Syy = 0
+    for i, v in enumerate(y, 1):
+        Sy += v
+        Sty += i * v
+        Syy += v * v
+        n = i
+        Ky = 2 * Sty - (n + 1) * Sy
+        exact = (n * n - 1) * (n * Syy - Sy * Sy) - 3 * Ky * Ky
+        a = _wrap64(n * Syy - Sy * Sy)
+        b = _wrap64((n * n - 1) * a)
+        c = _wrap64(3 * _wrap64(Ky * Ky))
+        out.append((exact, _wrap64(b - c)))
+    return out
+
+
+def test_first_chunk_residual_sum_fits_int64():
+    # estimate.cu fit_at(n32): for n <= 32 and samples y < 2^18 every term of the residual sum stays below 2^60, so
+    # the int64 evaluation equals the exact (int128) one. Edges: constant maximum, alternating 0 / maximum, ramps, and
+    # random series at the bound.
+    top = (1 << 18) - 1
+    series = [[top] * 32, [0, top] * 16, [top, 0] * 16, list(range(top - 31, top + 1)), [top - 40 * i for i in range(32)],
+              [0] * 31 + [top], [top] + [0] * 31]
+    rng = np.random.default_rng(7)
+    series += [list(rng.integers(0, 1 << 18, 32)) for _ in range(2000)]
+    series += [list(rng.integers(top - 64, 1 << 18, 32)) for _ in range(500)]
+    for y in series:
+        for exact, got in _ssr_int64_terms([int(v) for v in y]):
+            assert got == exact and abs(exact) < 1 << 61

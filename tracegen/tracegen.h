@@ -94,10 +94,12 @@ TG_HD uint32_t tg_iter_bits(uint64_t job_key, uint32_t i) {
 TG_HD int32_t tg_irwin_hall(uint32_t r, uint32_t sigma) {
 #ifdef __CUDA_ARCH__
     const int32_t s = (int32_t)__dp4a(r, 0x01010101u, 0u);
+    /* the high word of the signed 64-bit product: one IMAD.HI */
+    return __mulhi((s - 510) * 4096, (int32_t)((sigma & 0xFFFFu) * 7094u));
 #else
     const int32_t s = (int32_t)((r & 0xFFu) + ((r >> 8) & 0xFFu) + ((r >> 16) & 0xFFu) + (r >> 24));
-#endif
     return (int32_t)(((int64_t)((s - 510) * 4096) * (int64_t)(int32_t)((sigma & 0xFFFFu) * 7094u)) >> 32);
+#endif
 }
 
 /* Per-iteration sample i (1-based) of a DYNAMIC job: requested MiB y_i (allocator-rounded up to 2 MiB, >= 2) and
