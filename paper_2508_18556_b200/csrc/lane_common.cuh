@@ -77,6 +77,30 @@ __device__ __forceinline__ void lrec(uint32_t& hl, uint32_t& hh, uint32_t tick, 
     hh = (uint32_t)(p >> 32) + y * 0x1b3u + (x << 8);
 }
 
+// a12 per finished unit (k_ff_lane, k_simulate_lane): the lane's counts go to the CTA's 32-bit counters (c32, the
+// kF32 order) by one shared reduction each, and its 64-bit sums to the lane's own partial slots in global scratch by
+// one global reduction each. Plain RED instructions: no warp aggregation (lanes finish their units at different
+// iterations, often one or two at a time) and no load on the lane's path.
+__device__ __forceinline__ void lane_unit_totals(const LaneParams& P, uint32_t* c32, uint32_t n, uint32_t rejected,
+                                                 uint32_t failed, uint32_t ooms, uint32_t preempts,
+                                                 uint32_t placements, uint32_t waits, uint32_t creates,
+                                                 uint32_t destroys, uint32_t makespan, uint32_t err,
+                                                 unsigned long long turn, unsigned long long busy,
+                                                 unsigned long long hash, unsigned long long mem,
+                                                 unsigned long long waste) {
+    const uint32_t cb = (uint32_t)__cvta_generic_to_shared(c32);
+    const uint32_t v[10] = {1u, n, rejected, failed, ooms, preempts, placements, waits, creates, destroys};
+#pragma unroll
+    for (int k = 0; k < 10; ++k) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(cb + 4 * k), "r"(v[k]) : "memory");
+    asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(cb + 40), "r"(makespan) : "memory");
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(cb + 44), "r"(err) : "memory");
+    unsigned long long* d = P.part + (size_t)blockIdx.x * kT64 * kLaneThreads + threadIdx.x;
+    const unsigned long long w[kT64] = {makespan, turn, busy, hash, mem, waste};
+#pragma unroll
+    for (int k = 0; k < kT64; ++k)
+        asm volatile("red.global.add.u64 [%0], %1;" ::"l"(d + k * kLaneThreads), "l"(w[k]) : "memory");
+}
+
 // a12, once per CTA at the end of a launch: the policy's totals from the CTA's 32-bit counts (shared atomics,
 // c32[kT32]) and its lanes' 64-bit partial sums (global scratch, [CTA][kT64][lane]); one thread per field, one
 // atomic per field and CTA; completed, restarts and energy derived from them. Every thread of the CTA calls it.
@@ -93,7 +117,7 @@ __device__ __forceinline__ void lane_flush_totals(const LaneParams& P, const uin
             v = c32[tid];
         } else {
             const unsigned long long* row = P.part + ((size_t)blockIdx.x * kT64 + (tid - kT32)) * kLaneThreads;
-            for (int k = 0; k < kLaneThreads; ++k) v += row[k];
+            for (int k = 0; k < kLaneThreads; ++k) v += __ldcg(row + k);  // written by global reductions (L2)
         }
         red[tid < kT32 ? kF32[tid] : kF64[tid - kT32]] = v;
     }

@@ -874,28 +874,9 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                 o[5] = make_uint4((uint32_t)a_mem, (uint32_t)(a_mem >> 32), (uint32_t)a_waste,
                                   (uint32_t)(a_waste >> 32));
             }
-            {  // a12: 32-bit counts by shared atomics, 64-bit sums in this lane's partial slots
-                uint32_t* c = S.c32;
-                atomicAdd(c + 0, 1u);
-                atomicAdd(c + 1, n);
-                if (rejected) atomicAdd(c + 2, rejected);
-                if (failed) atomicAdd(c + 3, failed);
-                if (ooms) atomicAdd(c + 4, ooms);
-                if (preempts) atomicAdd(c + 5, preempts);
-                atomicAdd(c + 6, placements);
-                if (waits) atomicAdd(c + 7, waits);
-                if (creates) atomicAdd(c + 8, creates);
-                if (destroys) atomicAdd(c + 9, destroys);
-                atomicMax(c + 10, makespan);
-                if (err) atomicOr(c + 11, err);
-                unsigned long long* d = P.part + (size_t)blockIdx.x * kT64 * kLaneThreads + tid;
-                d[0 * kLaneThreads] += makespan;
-                d[1 * kLaneThreads] += a_turn;
-                d[2 * kLaneThreads] += a_busy;
-                d[3 * kLaneThreads] += ((unsigned long long)hh << 32) | hl;
-                d[4 * kLaneThreads] += a_mem;
-                d[5 * kLaneThreads] += a_waste;
-            }
+            // a12: the unit's counts and sums into the CTA's totals (lane_common.cuh)
+            lane_unit_totals(P, S.c32, n, rejected, failed, ooms, preempts, placements, waits, creates, destroys, makespan,
+                             err, a_turn, a_busy, ((unsigned long long)hh << 32) | hl, a_mem, a_waste);
             tr = tr_next;
             if (tr < P.n_traces) {
                 tr_next = atomicAdd(P.counter, 1ull);
