@@ -322,22 +322,29 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                     dur = it * ticks;
                     a_mem += (uint64_t)phys * dur;
                 } else if (P.est) {
+                    // every field the run needs is loaded up front (independent loads, one latency): the first
+                    // exceed at this level, the memory integral up to it / to convergence / to the end
                     const mig_job_estimate* ej = P.est + j0 + j;
+                    const uint32_t* ew = reinterpret_cast<const uint32_t*>(ej);
                     const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
+                    const uint32_t m_fe = __ldg(ew + 12 + lev), m_T = __ldg(ew + 18);
+                    uint32_t m_run;
                     if (ER) {  // a10: preempt at the convergence iteration when the forecast exceeds this slice
                         const uint2 pc = __ldg(reinterpret_cast<const uint2*>(ej) + 0);  // (req0, pred)
                         const uint32_t conv = __ldg(reinterpret_cast<const unsigned short*>(ej) + 4);
+                        const uint32_t m_conv = __ldg(ew + 17);
                         const uint32_t cap = S.level_mem[lev];
                         const uint32_t i_pre = (conv > 0 && pc.y > cap && cap < S.full_mem) ? conv : 0xFFFFFFFFu;
                         ek = fe <= min(T, i_pre) ? 1u : i_pre < T ? 2u : 0u;  // R29: OOM > COMPLETE > PREEMPT
                         it = ek == 1 ? fe : ek == 2 ? i_pre : T;
+                        m_run = ek == 1 ? m_fe : ek == 2 ? m_conv : m_T;
                     } else {
                         ek = fe <= T ? 1u : 0u;
                         it = ek ? fe : T;
+                        m_run = ek ? m_fe : m_T;
                     }
                     dur = it * ticks;
-                    a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek == 1 ? lev : ek ? 5u : 6u)) *
-                             ticks;
+                    a_mem += (uint64_t)m_run * ticks;
                 } else {  // a DYNAMIC record under MIG_TRACES_NO_DYNAMIC (no estimates): flagged, no forecast
                     err |= (uint32_t)MIG_ERR_BAD_RECORD;
                     ek = 0;
@@ -493,13 +500,15 @@ __global__ void __launch_bounds__(kLaneThreads, BASE_MINB) k_base_lane(const Dev
                         it = ek ? 1u : T;
                         dur = it * ticks;
                         a_mem += (uint64_t)phys * dur;
-                    } else if (P.est) {
+                    } else if (P.est) {  // independent loads: the first exceed and both memory integrals
                         const mig_job_estimate* ej = P.est + j0 + j;
+                        const uint32_t* ew = reinterpret_cast<const uint32_t*>(ej);
                         const uint32_t fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + flev);
+                        const uint32_t m_fe = __ldg(ew + 12 + flev), m_T = __ldg(ew + 18);
                         ek = fe <= T ? 1u : 0u;
                         it = ek ? fe : T;
                         dur = it * ticks;
-                        a_mem += (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(ej) + 12 + (ek ? flev : 6u)) * ticks;
+                        a_mem += (uint64_t)(ek ? m_fe : m_T) * ticks;
                     } else {  // DYNAMIC under MIG_TRACES_NO_DYNAMIC: flagged, no forecast
                         err |= (uint32_t)MIG_ERR_BAD_RECORD;
                         ek = 0;
