@@ -62,8 +62,11 @@ __device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
 #define FF_MINB 8
 #endif
 // NS: the start slots scanned for the next event (every placement of the geometry starts below NS; A100: 7).
-template <int NS, bool XR, bool ER>
+// KIND: MIG_FUSION_FISSION (Scheme B: idle instances persist and are reused, fused or split) or MIG_DYNAMIC (Alg. 2
+// creates a tight slice on demand and the run's end destroys it, R10: no reuse, no fusion / fission).
+template <int NS, bool XR, bool ER, int KIND>
 __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
+    constexpr bool FF = KIND == MIG_FUSION_FISSION;
     __shared__ __align__(16) FFShared S;
     const uint32_t tid = threadIdx.x;
     {
@@ -231,9 +234,15 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                     }
                 }
                 key[es * kLaneThreads] = kIdle;
+                const uint32_t ext = ((si >> 8) & 0xFFu) << es;
                 BS &= ~(1u << es);
-                BM &= ~(((si >> 8) & 0xFFu) << es);
-                IPM |= 1ull << (8 * epr + es);  // the instance is idle
+                BM &= ~ext;
+                if (FF) {
+                    IPM |= 1ull << (8 * epr + es);  // the instance is idle
+                } else {  // DYNAMIC: freed at the run's end (R10)
+                    occ &= ~ext;
+                    K1 += 1u;
+                }
                 unsigned long long m = key[0];
 #pragma unroll
                 for (int k = 1; k < NS; ++k) m = min(m, key[k * kLaneThreads]);
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
             const uint32_t need = hneed;
             const bool rej = need == kNoNeed;  // no profile can ever hold the job: REJECT
             const uint32_t nq = rej ? 0u : need;
-            const uint64_t x = IPM & S.reuse_sel[nq];  // idle slices that tightly fit (R7)
+            const uint64_t x = FF ? IPM & S.reuse_sel[nq] : 0ull;  // idle slices that tightly fit (R7)
             uint32_t y = (uint32_t)x | (uint32_t)(x >> 32);
             y |= y >> 16;
             y |= y >> 8;
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
             pr = rej ? kNoNeed : cand ? (prof4 >> (4 * rsl)) & 0xFu : need;
             s = cand ? rsl : a;
             kd = rej ? K_REJECT : cand ? K_REUSE : a != 0xFFu ? K_ALLOC : K_WAIT;
-            a7try = kd == K_WAIT && (SM & ~BS);  // fusion / fission may place it (idle instances exist)
+            a7try = FF && kd == K_WAIT && (SM & ~BS);  // fusion / fission may place it (idle instances exist)
         }
         if (a7try) {  // A7 (R8): candidates touching no busy slot, the host-built answer table
             const uint32_t need = hneed;
@@ -306,9 +315,9 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 const uint32_t lm8 = (si >> 8) & 0xFFu;
                 if (created) {
                     occ |= lm8 << s;
-                    SM |= 1u << s;
+                    if (FF) SM |= 1u << s;
                     prof4 = (prof4 & ~(0xFu << (4 * s))) | (pr << (4 * s));
-                } else {
+                } else if (FF) {
                     IPM &= ~(1ull << (8 * pr + s));
                 }
                 // start_run: end tick and kind (OOM > COMPLETE in one iteration, R29)
@@ -589,17 +598,25 @@ cudaError_t launch_ff_lane(const DevGeom* Gdev, const LaneParams& P, uint32_t ns
                            cudaStream_t stream) {
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_lane<8, true, true>, kLaneThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_lane<8, true, true, MIG_FUSION_FISSION>, kLaneThreads,
+                                                      0);
         if (per_sm < 1) per_sm = 1;
     }
     const dim3 grid((unsigned)std::min<uint64_t>(max_blocks, lane_blocks(per_sm, P.n_traces, sm_count))),
         block(kLaneThreads);
     const bool xr = P.ext != nullptr, er = (P.pol.flags & MIG_EARLY_RESTART) != 0;
-#define FF_LAUNCH(NS_)                                                                     \
-    if (xr && er) k_ff_lane<NS_, true, true><<<grid, block, 0, stream>>>(Gdev, P);         \
-    else if (xr) k_ff_lane<NS_, true, false><<<grid, block, 0, stream>>>(Gdev, P);         \
-    else if (er) k_ff_lane<NS_, false, true><<<grid, block, 0, stream>>>(Gdev, P);         \
-    else k_ff_lane<NS_, false, false><<<grid, block, 0, stream>>>(Gdev, P);
+    const bool dyn = P.pol.kind == MIG_DYNAMIC;
+#define FF_LAUNCH_K(NS_, K_)                                                                 \
+    if (xr && er) k_ff_lane<NS_, true, true, K_><<<grid, block, 0, stream>>>(Gdev, P);       \
+    else if (xr) k_ff_lane<NS_, true, false, K_><<<grid, block, 0, stream>>>(Gdev, P);       \
+    else if (er) k_ff_lane<NS_, false, true, K_><<<grid, block, 0, stream>>>(Gdev, P);       \
+    else k_ff_lane<NS_, false, false, K_><<<grid, block, 0, stream>>>(Gdev, P);
+#define FF_LAUNCH(NS_)                           \
+    if (dyn) {                                   \
+        FF_LAUNCH_K(NS_, MIG_DYNAMIC)            \
+    } else {                                     \
+        FF_LAUNCH_K(NS_, MIG_FUSION_FISSION)     \
+    }
     if (ns <= 4) {
         FF_LAUNCH(4)
     } else if (ns <= 7) {
@@ -608,6 +625,7 @@ cudaError_t launch_ff_lane(const DevGeom* Gdev, const LaneParams& P, uint32_t ns
         FF_LAUNCH(8)
     }
 #undef FF_LAUNCH
+#undef FF_LAUNCH_K
     return cudaGetLastError();
 }
 

@@ -971,8 +971,8 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
     const bool pf = (pol.flags & (MIG_WARP_FOLD | MIG_EARLY_RESTART | MIG_WAVE_TIME)) == 0;
     // the fast kernels (simulate_ff.cu) take extension records and early restart, not warp folding or wave time
     const bool ff_pf = (pol.flags & (MIG_WARP_FOLD | MIG_WAVE_TIME)) == 0;
-    const bool fast = (pol.kind == MIG_FUSION_FISSION || pol.kind == MIG_BASELINE) && !ext && ff_pf && Gh &&
-                      ff_fast_enabled();
+    const bool fast = (pol.kind == MIG_FUSION_FISSION || pol.kind == MIG_DYNAMIC || pol.kind == MIG_BASELINE) && !ext &&
+                      ff_pf && Gh && ff_fast_enabled();
     if (fast) {
         for (int l = 0; l < kMaxLevels; ++l) P.lm[l] = l < (int)Gh->n_levels ? Gh->level_mem[l] : 0xFFFFFFFFu;
         uint32_t lf = 0;
