@@ -122,6 +122,8 @@ mig_status mig_geometry_fusion(const mig_geometry* g, uint32_t occ_mask, uint32_
  *                     | PCIe transfer fraction F of an iteration in 1/256 (bits 24-31; MIG_PCIE_CONTENTION)
  *                 w = iter_ticks
  *   jobs_ext[j] = {ws_mib, warps, slope_q8, sigma_mib | qslope_q16 << 16} or NULL (all zero).
+ *   Domain: est_mib + ws_mib + ctx_mib is taken modulo 2^32 (u32, as the oracle's req0), and true_mib + ws_mib +
+ *   ctx_mib must stay below 2^32 MiB (the kernels saturate it there; the oracle keeps it exact).
  *   DYNAMIC jobs report per-iteration samples (requested MiB, inverse reuse Q16) drawn in-kernel from the
  *   counter-based generator of tracegen.h keyed by (seed, trace_id0 + trace, job index in trace).
  * ---------------------------------------------------------------------------------------------------------------- */
