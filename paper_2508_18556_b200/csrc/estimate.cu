@@ -203,15 +203,30 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
 
 // Whole-warp estimation of one DYNAMIC job (lanes over iterations).
 // PLAIN: generated samples and no EWMA variant (the common case), so those paths compile out.
+// A bound on every physical MiB of a DYNAMIC job's generated series, or ~0 when the series' range bounds do not
+// keep it inside the predictor's input limits (y < 2^18, 0 < q < 2^26: the checked path). y <= b + slope*T/256 + the
+// largest Irwin-Hall draw + 1, q grows from q0 by qs (the draw is at most 510 * sigma * 7094 / 2^20; 131070 / 2^28 =
+// 511.99 / 2^20 bounds it); the inverse reuse only grows, so q >= q0, and the division by q0 is bounded from above
+// by a shift by floor(log2 q0) (no 64-bit division).
+__device__ __forceinline__ uint64_t generated_phys_hi(uint4 r, uint4 e, uint32_t ctx) {
+    const uint32_t T = r.z & 0xFFFFu;
+    const uint32_t b = r.x, q0 = r.y, slope = e.z, sigma_n = e.w & 0xFFFFu, qs = e.w >> 16;
+    const uint64_t y_hi = (uint64_t)b + (((uint64_t)slope * T) >> 8) +
+                          (((uint64_t)131070u * ((sigma_n & 0xFFFFu) * 7094u)) >> 28) + 2u;
+    const bool check = y_hi >= (1u << 18) || q0 == 0 || (uint64_t)q0 + (uint64_t)qs * T >= (1u << 26);
+    const bool q_unit = q0 == 65536u && qs == 0;
+    return check ? ~0ull : (q_unit ? y_hi : (y_hi << 16) >> (31 - __clz(q0))) + (uint64_t)e.x + ctx;
+}
+
+// key: the job's sample-generator key (tracegen.h tg_job_key, formed for the chunk's jobs in parallel).
 template <bool PLAIN>
-__device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t trace_key, uint32_t jidx, uint4 r,
+__device__ __forceinline__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t key, uint4 r,
                                  uint4 e, uint32_t lane, mig_job_estimate* dst, const uint2* rec_samples,
                                  uint32_t rec_count) {
     if (PLAIN) rec_samples = nullptr;
     const bool ewma = !PLAIN && P.ewma != 0;
     const uint32_t T = r.z & 0xFFFFu;
     const uint32_t b = r.x, q0 = r.y, ws = e.x, slope = e.z, sigma_n = e.w & 0xFFFFu, qs = e.w >> 16;
-    const uint64_t key = tg_job_key(trace_key, jidx);  // = tg_key(seed, trace, jidx)
     const int64_t ws_ctx = (int64_t)ws + P.ctx;
     uint32_t fe[5] = {kNever, kNever, kNever, kNever, kNever};
     uint32_t mfe[5] = {0u, 0u, 0u, 0u, 0u};  // physical MiB summed over iterations 1..fe[l]
@@ -231,17 +246,12 @@ __device__ void estimate_dynamic(const DevGeom& G, const EstParams& P, uint64_t 
     double phi = 0.0, a = 0.0, sig = 0.0;
     bool done_pred = T < P.min_n;
     bool bad = false;
-    // generated series whose range bounds already satisfy the predictor's input limits skip the per-sample checks
-    // (y < 2^18, 0 < q < 2^26): y <= b + slope*T/256 + the largest Irwin-Hall draw + 1, q grows from q0 by qs (the
-    // draw is at most 510 * sigma * 7094 / 2^20; 131070 / 2^28 = 511.99 / 2^20 bounds it)
-    const uint64_t y_hi = (uint64_t)b + (((uint64_t)slope * T) >> 8) +
-                          (((uint64_t)131070u * ((sigma_n & 0xFFFFu) * 7094u)) >> 28) + 2u;
-    const bool check = rec_samples || y_hi >= (1u << 18) || q0 == 0 || (uint64_t)q0 + (uint64_t)qs * T >= (1u << 26);
+    // generated series whose range bounds already satisfy the predictor's input limits skip the per-sample checks;
+    // phys_hi bounds every physical MiB of the job
+    const uint64_t phys_hi_gen = generated_phys_hi(r, e, P.ctx);  // (formed here: a passed-in copy spills)
+    const bool check = rec_samples || phys_hi_gen == ~0ull;
     const bool fastq = !check && q0 >= 65536u;  // phys_div's range: generated q never decreases from q0
-    // a bound on every physical MiB of the job (generated series; q >= q0 since the inverse reuse only grows)
-    // (the division by q0 is bounded from above by a shift by floor(log2 q0): no 64-bit division here)
-    const uint64_t phys_hi = rec_samples || check ? ~0ull
-                                                  : (q_unit ? y_hi : (y_hi << 16) >> (31 - __clz(q0))) + (uint64_t)ws_ctx;
+    const uint64_t phys_hi = rec_samples ? ~0ull : phys_hi_gen;
     uint32_t base = 0;
     for (; base < T && !done_pred; base += 32) {  // until convergence; then scan_tail to T (memory integral)
         const uint32_t n = base + lane + 1;
@@ -380,6 +390,7 @@ __global__ void __launch_bounds__(256, EST_MINB) k_estimate(const DevGeom G, con
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t j_base = P.off[0];
     __shared__ uint64_t s_tkey[8][32];
+    __shared__ uint64_t s_jkey[8][32];  // the generator key of each of the chunk's jobs
     for (;;) {
         unsigned long long t0 = 0;
         if (lane == 0) t0 = atomicAdd(P.counter, (unsigned long long)kEstBatch);
@@ -434,13 +445,21 @@ __global__ void __launch_bounds__(256, EST_MINB) k_estimate(const DevGeom G, con
                                (uint32_t)phys * T);
             }
             uint32_t dm = __ballot_sync(FULL, valid && cls == kClassDynamic);
+            if (dm) {  // the generator keys of the chunk's 32 jobs at once (one lane each)
+                // the batch trace holding record g: the last trace whose first job is <= g (offsets non-decreasing)
+                uint32_t tb = 0;
+#pragma unroll
+                for (uint32_t step = 16; step; step >>= 1)
+                    if (__shfl_sync(FULL, my_off, tb + step) <= g) tb += step;
+                const uint32_t jt = (uint32_t)(g - __shfl_sync(FULL, my_off, tb));
+                const uint64_t key = tg_job_key(s_tkey[threadIdx.x >> 5][tb], jt);  // = tg_key(seed, trace, jt)
+                s_jkey[threadIdx.x >> 5][lane] = key;
+                __syncwarp();
+            }
             while (dm) {
                 const uint32_t L = (uint32_t)__ffs(dm) - 1;
                 dm &= dm - 1;
                 const uint64_t gL = c + L;
-                // the batch trace holding job gL: the last trace whose first job is <= gL
-                const uint32_t tb = 31u - __clz(__ballot_sync(FULL, lane < nb && my_off <= gL));
-                const uint32_t jt = (uint32_t)(gL - __shfl_sync(FULL, my_off, tb));
                 // the job's records again, one broadcast load each (L1 hits: the chunk just read them), so the chunk's
                 // records are not kept live across the job loop
                 const uint4 rr = __ldg(P.jobs + gL);
@@ -456,8 +475,7 @@ __global__ void __launch_bounds__(256, EST_MINB) k_estimate(const DevGeom G, con
                         if (rcount == 0) rs = nullptr;  // nothing recorded: fall back to the declared generator
                     }
                 }
-                const uint64_t tkey = s_tkey[threadIdx.x >> 5][tb];
-                estimate_dynamic<PLAIN>(G, P, tkey, jt, rr, ee, lane, P.out + gL, rs, rcount);
+                estimate_dynamic<PLAIN>(G, P, s_jkey[threadIdx.x >> 5][L], rr, ee, lane, P.out + gL, rs, rcount);
             }
         }
     }
