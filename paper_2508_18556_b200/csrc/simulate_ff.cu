@@ -339,8 +339,9 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                     const uint32_t m_fe = __ldg(ew + 12 + lev), m_T = __ldg(ew + 18);
                     uint32_t m_run;
                     if (ER) {  // a10: preempt at the convergence iteration when the forecast exceeds this slice
-                        const uint2 pc = __ldg(reinterpret_cast<const uint2*>(ej) + 0);  // (req0, pred)
-                        const uint32_t conv = __ldg(reinterpret_cast<const unsigned short*>(ej) + 4);
+                        const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(ej));  // (req0, pred, conv | n, fe0 | fe1)
+                        const uint2 pc = make_uint2(e0.x, e0.y);
+                        const uint32_t conv = e0.z & 0xFFFFu;
                         const uint32_t m_conv = __ldg(ew + 17);
                         const uint32_t cap = S.level_mem[lev];
                         const uint32_t i_pre = (conv > 0 && pc.y > cap && cap < S.full_mem) ? conv : 0xFFFFFFFFu;

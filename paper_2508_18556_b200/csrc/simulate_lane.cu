@@ -341,11 +341,18 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             err |= (uint32_t)MIG_ERR_BAD_RECORD;
             fe = kNever;
         } else if (__builtin_expect(dyn, 0)) {
+            // the estimate's first 16 B hold pred, conv and the first exceeds of levels 0-1; levels 2-4 follow
+            // (one request per 16 B block instead of one per field)
             ej = P.est + j0 + j;
             const uint4 e0 = __ldg(reinterpret_cast<const uint4*>(ej));
             pred = e0.y;
             conv = e0.z & 0xFFFFu;
-            fe = __ldg(reinterpret_cast<const unsigned short*>(ej) + 6 + lev);
+            if (lev < 2) {
+                fe = lev ? e0.w >> 16 : e0.w & 0xFFFFu;
+            } else {
+                const uint2 e1 = __ldg(reinterpret_cast<const uint2*>(ej) + 2);
+                fe = lev == 2 ? e1.x & 0xFFFFu : lev == 3 ? e1.x >> 16 : e1.y & 0xFFFFu;
+            }
         } else {
             const uint64_t phys64 = (uint64_t)hr.y + he.x + P.ctx;
             phys = phys64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)phys64;
@@ -532,7 +539,7 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
                     uint32_t j;
                     if (sa_pre && k < pl) {  // a grouped record (its x holds the job index)
                         hr = __ldg(P.sa_desc + j0 + pbase + k);
-                        he = pext ? __ldg(P.sa_dext + j0 + pbase + k) : make_uint4(0, 0, 0, 0);
+                        he = P.sa_dext ? __ldg(P.sa_dext + j0 + pbase + k) : make_uint4(0, 0, 0, 0);
                         j = hr.x;
                     } else {  // a requeued job (OOM / early restart), from the ring
                         j = ring[(cur * P.ring_cap + k - pl) * kRs];
@@ -1019,12 +1026,15 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
             if (!ext && sa_pregroup_enabled() && tr.n_traces && tr.n_jobs) {
                 // the grouping pass as its own launch (k_sa_group), its outputs in stream-ordered scratch
                 const size_t nj = tr.n_jobs, nt = tr.n_traces;
-                const size_t b_desc = nj * 16, b_dext = P.ext ? nj * 16 : 0, b_hdr = nt * 32;
+                // the grouped extension records only when the policy reads more than the workspace (warp folding,
+                // wave time); otherwise k_sa_group adds the workspace to the grouped record's true footprint
+                const bool dext_needed = P.ext && (pol.flags & (MIG_WARP_FOLD | MIG_WAVE_TIME)) != 0;
+                const size_t b_desc = nj * 16, b_dext = dext_needed ? nj * 16 : 0, b_hdr = nt * 32;
                 uint8_t* sa = nullptr;
                 cudaError_t e2 = mig_scratch_alloc((void**)&sa, b_desc + b_dext + b_hdr, stream);
                 if (e2 != cudaSuccess) return e2;
                 P.sa_desc = reinterpret_cast<const uint4*>(sa);
-                P.sa_dext = P.ext ? reinterpret_cast<const uint4*>(sa + b_desc) : nullptr;
+                P.sa_dext = dext_needed ? reinterpret_cast<const uint4*>(sa + b_desc) : nullptr;
                 P.sa_hdr = reinterpret_cast<const uint4*>(sa + b_desc + b_dext);
                 e2 = launch_sa_group(Gdev, P, (uint4*)P.sa_desc, (uint4*)P.sa_dext, (uint4*)P.sa_hdr, sm_count, stream);
                 if (e2 == cudaSuccess) {

@@ -12,7 +12,8 @@ namespace mig {
 // the Scheme A lane launch. One warp per trace (four per CTA): its job records 32 at a time (coalesced), the tight
 // fits in parallel, group positions by ballots (no event loop); the t = 0 REJECT records (queue order) go into the trace's decision
 // hash, and the records are written in group order (ascending memory level of the tight fit, queue order within a
-// level) with their x word replaced by the job index, so the lane kernel dispatches each group by reading the next
+// level) with their x word replaced by the job index (and, without a dext buffer, the workspace added to the true
+// footprint: only warp folding / wave time need the rest of the extension record), so the lane kernel dispatches each group by reading the next
 // record of the group sequentially instead of re-reading records by job index. Per trace: sa_hdr[2t]
 // = {len0 | len1 << 16, len2 | len3 << 16, len4 | rejected << 16, error bits}, sa_hdr[2t + 1] = {hash lo, hash hi}.
 // Pass 1 counts the groups (and the REJECT hash), pass 2 scatters (the trace's records are re-read from L2).
@@ -121,8 +122,10 @@ __global__ void __launch_bounds__(kLaneThreads) k_sa_group(const DevGeom* __rest
             }
             if (lv != 0xFFu) {
                 r.x = k;
+                if (XR && !dext && ((r.z >> 16) & 0xFFu) != kClassDynamic)  // true + ws (saturating, as the lane
+                    r.y = r.y + e.x < r.y ? 0xFFFFFFFFu : r.y + e.x;          // kernel's 64-bit sum): no dext needed
                 desc[j0 + at] = r;
-                if (XR) dext[j0 + at] = e;
+                if (XR && dext) dext[j0 + at] = e;
             }
         }
         err = __reduce_or_sync(FULL, err);
