@@ -373,9 +373,10 @@ def roofline(wl, ktimes, steps, totals, world, peaks, peak_src, ncu):
         byts = ((JOB_BYTES + ext_b) * wl.n_jobs + RESULT_BYTES * wl.n) * len(even) / n_l
         ops_desc = f"{OPS_PER_DECISION}/decision + {OPS_PER_EVENT}/event (SURVEY.md §8(d))"
         bytes_desc = f"{JOB_BYTES + ext_b} B/job read + {RESULT_BYTES} B/trace result written"
-        fast = not wl.has_ext and all(wl.pol_keys[i][1] == 0 for i in even) and os.environ.get("MIG_FF_FAST", "1") != "0"
-        kname = {("sim_ff", True): "k_ff_lane", ("sim_baseline", True): "k_base_lane"}.get(
-            (dom, fast), f"k_simulate_lane ({dom})")
+        # the fast kernels take extension records and early restart (flag 1), not warp folding / wave time
+        fast = all(wl.pol_keys[i][1] in (0, 1) for i in even) and os.environ.get("MIG_FF_FAST", "1") != "0"
+        kname = {("sim_ff", True): "k_ff_lane", ("sim_dynamic", True): "k_ff_lane",
+                 ("sim_baseline", True): "k_base_lane"}.get((dom, fast), f"k_simulate_lane ({dom})")
     a_ops = ops / (ms * 1e-3)
     a_bytes = byts / (ms * 1e-3)
     intensity = ops / byts if byts else float("inf")
@@ -627,7 +628,10 @@ def run_mine(args):
         "traces_per_s": m["traces_per_s"],
         "config": {"workload": spec["desc"], "traces_per_gpu": n_per, "total_traces": n_per * world if not total
                    else total, "jobs_per_trace": wl.J, "policies": [POLICY_NAMES[p] for p in wl.pol_keys],
-                   "decisions_per_step": m["dec_step"], "parallelism": f"trace-sharded x{world} ({scaling})",
+                   "decisions_per_step": m["dec_step"],
+                   "decisions_by_policy": {POLICY_NAMES[p]: int(t["placements"]) + int(t["waits"]) + int(t["rejected"])
+                                           for p, t in zip(wl.pol_keys, m["totals"])},
+                   "parallelism": f"trace-sharded x{world} ({scaling})",
                    "l2": (f"inputs ({wl.n_jobs * 16 / 1e9:.2f} GB/GPU) larger than L2; no flush" if not wl.chunked
                           else "inputs generated per chunk inside the step (chunks larger than L2); no flush")},
         "kernels": m["kernels"],
