@@ -75,7 +75,8 @@ __device__ __forceinline__ FitOut fit_at(int64_t n, int64_t Sy, int64_t Sty, int
         V = __dmul_rn(__ddiv_rn(i128_to_double(numQ), den), 1.0 / 65536.0);  // exact power-of-two scaling
         if (V < 1.0) V = 1.0;
     }
-    f.phi = __ddiv_rn(u, V);
+    // V = 1 exactly for a constant inverse reuse (no EWMA): the IEEE quotient u / 1 is u, so the division is skipped
+    f.phi = (q_unit && !ewma) ? u : __ddiv_rn(u, V);
     f.a = 0.0;
     f.P = (int64_t)ceil(f.phi) + ws_ctx;
     return f;
@@ -289,7 +290,9 @@ __device__ __forceinline__ void estimate_dynamic(const DevGeom& G, const EstPara
         // exact integer moments at n = base + lane + 1 (inclusive warp scans + carried totals)
         const int64_t yi = y, qi = q, ni = n;
         const int64_t sy = Sy + (int64_t)warp_scan_u32(y, lane);  // sum y <= 4096 * 2^18 fits 32 bits
-        const int64_t sty = Sty + warp_scan_i64(valid ? ni * yi : 0, lane);
+        // first chunk of an in-range series: n*y < 2^23 and the prefix sums stay below 2^28, so the scan runs in 32 bits
+        const int64_t sty = (base == 0 && !check) ? (int64_t)warp_scan_u32(valid ? n * y : 0u, lane)
+                                                  : Sty + warp_scan_i64(valid ? ni * yi : 0, lane);
         const int64_t syy = Syy + warp_scan_i64(yi * yi, lane);
         // constant inverse reuse: its fit is not needed (V = 1), so its moments are not formed
         const int64_t sq = q_unit ? 0 : Sq + warp_scan_i64(qi, lane);
