@@ -36,7 +36,14 @@ struct LaneParams {
     const uint4* sa_desc;
     const uint4* sa_dext;
     const uint4* sa_hdr;
+    // the order in which units are visited (trace_order.cu): unit u is trace order[u]; NULL = trace u
+    const uint32_t* order;
 };
+
+// The trace of unit u, or ~0 once the units are exhausted (u >= n_traces).
+__device__ __forceinline__ unsigned long long lane_unit_trace(const LaneParams& P, unsigned long long u) {
+    return u >= P.n_traces ? ~0ull : P.order ? (unsigned long long)__ldg(P.order + u) : u;
+}
 
 constexpr int kLaneThreads = 128;
 // Resident CTAs per SM (launch bounds) and where the u64 accumulators live: the Scheme B kernels (STATIC, DYNAMIC,
@@ -150,6 +157,9 @@ cudaError_t launch_ff_lane(const DevGeom* Gdev, const LaneParams& P, uint32_t ns
                            cudaStream_t stream);
 cudaError_t launch_base_lane(const DevGeom* Gdev, const LaneParams& P, uint64_t max_blocks, int sm_count,
                              cudaStream_t stream);
+size_t trace_order_scratch_bytes(uint64_t n_traces);
+cudaError_t launch_trace_order(const mig_traces& tr, const DevGeom* Gh, uint32_t ctx, void* buf, bool force,
+                               int sm_count, cudaStream_t s);
 cudaError_t launch_sa_group(const DevGeom* Gdev, const LaneParams& P, uint4* desc, uint4* dext, uint4* hdr,
                             int sm_count, cudaStream_t stream);
 

@@ -939,13 +939,16 @@ static cudaError_t launch_variant(const DevGeom* Gdev, const SimParams& P, const
 uint64_t simulate_lane_grid(uint64_t n_traces, int sm_count);
 uint32_t simulate_lane_threads();
 uint32_t simulate_lane_partials();
+size_t trace_order_scratch_bytes(uint64_t n_traces);  // trace_order.cu
+cudaError_t launch_trace_order(const mig_traces& tr, const DevGeom* Gh, uint32_t ctx, void* buf, bool force,
+                               int sm_count, cudaStream_t s);
 cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, const mig_policy& pol, uint32_t pol_idx,
                                  uint32_t n_pol_all, const mig_job_estimate* est, mig_trace_result* out,
                                  mig_policy_totals* totals, unsigned long long* counter,
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
                                  uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream,
-                                 const DevGeom* Gh);
+                                 const DevGeom* Gh, const uint32_t* order);
 
 // Scheme B policies run one lane per trace (simulate_lane.cu) unless MIG_LANES_PER_TRACE selects the group kernel
 // (8 or 32 lanes per trace).
@@ -956,6 +959,11 @@ bool simulate_use_lane() {
         forced = env ? atoi(env) : 1;
     }
     return forced == 1;
+}
+
+static int env_flag(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
 }
 
 // Policy launches on forked streams (launch_simulate): on unless MIG_CONCURRENT_POLICIES=0.
@@ -1073,6 +1081,34 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                 return e;
             }
         }
+        // the visit order of the traces (trace_order.cu): similar traces in neighbouring lanes, one pass for every
+        // policy launch (a schedule only: results do not depend on it). Default: calls of at least 4096 traces
+        // averaging at least 32 jobs (a lane's phases only matter over long queues: configs 3 and 4, 20 and 4 jobs
+        // per trace, ran slower ordered), and the pass itself keeps trace order unless a quarter of the queues look
+        // homogeneous (config 5's mixed queues ran slower ordered); MIG_TRACE_ORDER=0 keeps trace order, =2 orders
+        // every call (tests)
+        uint32_t* order = nullptr;
+        const int ord = env_flag("MIG_TRACE_ORDER", 1);
+        const bool long_queues = tr.n_jobs >= 32 * tr.n_traces;
+        bool ff_kind = false;  // k_ff_lane visits the order (FUSION_FISSION / DYNAMIC on plain records)
+        for (uint32_t i = 0; i < n_pol; ++i)
+            ff_kind |= pols[i].kind == MIG_FUSION_FISSION || pols[i].kind == MIG_DYNAMIC;
+        if (Gh && ord && ff_kind && !tr.jobs_ext && ((tr.n_traces >= 4096 && long_queues) || ord == 2) &&
+            tr.n_traces < (1ull << 32)) {
+            e = mig_scratch_alloc((void**)&order, trace_order_scratch_bytes(tr.n_traces), stream);
+            if (e == cudaSuccess)
+                e = (cudaError_t)mig_timed("sim_order", stream, [&](uint32_t* nl) {
+                    if (nl) *nl = 3;
+                    return (int)launch_trace_order(tr, Gh, pols[0].ctx_mib, order, ord == 2, sm_count, stream);
+                });
+            if (e != cudaSuccess) {
+                if (order) mig_scratch_free(order, stream);
+                mig_scratch_free(scr, stream);
+                if (pc) mig_scratch_free(pc, stream);
+                return e;
+            }
+            *launches += 3;
+        }
         cudaEvent_t fork = nullptr, join[kMaxPolicies] = {};
         if (n_side) {
             e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
@@ -1093,7 +1129,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
                                                  est_err, reinterpret_cast<uint16_t*>(scr + k * set_bytes), blocks,
                                                  sid, a7, n_a7, pc ? pc + k * pc_elems : nullptr,
                                                  reinterpret_cast<unsigned long long*>(scr + k * set_bytes + ring_bytes),
-                                                 sm_count, st, Gh);
+                                                 sm_count, st, Gh, order);
             });
             ++*launches;
         }
@@ -1105,6 +1141,7 @@ cudaError_t launch_simulate(const DevGeom* Gdev, const mig_traces& tr, const mig
             if (join[k]) cudaEventDestroy(join[k]);
         }
         if (fork) cudaEventDestroy(fork);
+        if (order) mig_scratch_free(order, stream);
         mig_scratch_free(scr, stream);
         if (pc) mig_scratch_free(pc, stream);
         return e;

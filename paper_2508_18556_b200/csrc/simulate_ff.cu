@@ -64,7 +64,8 @@ __device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
 // NS: the start slots scanned for the next event (every placement of the geometry starts below NS; A100: 7).
 // KIND: MIG_FUSION_FISSION (Scheme B: idle instances persist and are reused, fused or split) or MIG_DYNAMIC (Alg. 2
 // creates a tight slice on demand and the run's end destroys it, R10: no reuse, no fusion / fission).
-template <int NS, bool XR, bool ER, int KIND>
+// ORD: units are visited in P.order (trace_order.cu); the instantiations without it keep the plain unit counter.
+template <int NS, bool XR, bool ER, int KIND, bool ORD>
 __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom* __restrict__ Gg, const LaneParams P) {
     constexpr bool FF = KIND == MIG_FUSION_FISSION;
     __shared__ __align__(16) FFShared S;
@@ -139,9 +140,14 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
     unsigned long long* const key = &S.key[0][tid];
     constexpr unsigned long long kIdle = ~0ull;
 
-    unsigned long long tr = atomicAdd(P.counter, 1ull);
-    __shared__ unsigned long long s_next[kLaneThreads];  // the lane's next unit (taken one ahead)
-    s_next[tid] = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
+    // units are taken one ahead; s_next holds the trace of the lane's next unit (~0: none left)
+    auto take = [&]() -> unsigned long long {
+        const unsigned long long u = atomicAdd(P.counter, 1ull);
+        return ORD ? lane_unit_trace(P, u) : u;
+    };
+    unsigned long long tr = take();
+    __shared__ unsigned long long s_next[kLaneThreads];
+    s_next[tid] = tr < P.n_traces ? take() : ~0ull;
     uint64_t j0 = 0;  // index of the unit's first job record
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
     uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0;
@@ -404,7 +410,7 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                              err, a_turn, a_busy, ((unsigned long long)hh << 32) | hl, a_mem, a_waste);
             tr = s_next[tid];
             if (tr < P.n_traces) {
-                s_next[tid] = atomicAdd(P.counter, 1ull);
+                s_next[tid] = take();
                 init_unit();
             } else {
                 active = false;
@@ -599,19 +605,23 @@ cudaError_t launch_ff_lane(const DevGeom* Gdev, const LaneParams& P, uint32_t ns
                            cudaStream_t stream) {
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_lane<8, true, true, MIG_FUSION_FISSION>, kLaneThreads,
-                                                      0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ff_lane<8, true, true, MIG_FUSION_FISSION, false>,
+                                                      kLaneThreads, 0);
         if (per_sm < 1) per_sm = 1;
     }
     const dim3 grid((unsigned)std::min<uint64_t>(max_blocks, lane_blocks(per_sm, P.n_traces, sm_count))),
         block(kLaneThreads);
     const bool xr = P.ext != nullptr, er = (P.pol.flags & MIG_EARLY_RESTART) != 0;
     const bool dyn = P.pol.kind == MIG_DYNAMIC;
-#define FF_LAUNCH_K(NS_, K_)                                                                 \
-    if (xr && er) k_ff_lane<NS_, true, true, K_><<<grid, block, 0, stream>>>(Gdev, P);       \
-    else if (xr) k_ff_lane<NS_, true, false, K_><<<grid, block, 0, stream>>>(Gdev, P);       \
-    else if (er) k_ff_lane<NS_, false, true, K_><<<grid, block, 0, stream>>>(Gdev, P);       \
-    else k_ff_lane<NS_, false, false, K_><<<grid, block, 0, stream>>>(Gdev, P);
+    // the visit order is used by the plain-record instantiations (the long homogeneous queues it helps)
+    const bool ord = P.order != nullptr && !xr;
+#define FF_LAUNCH_K(NS_, K_)                                                                       \
+    if (xr && er) k_ff_lane<NS_, true, true, K_, false><<<grid, block, 0, stream>>>(Gdev, P);      \
+    else if (xr) k_ff_lane<NS_, true, false, K_, false><<<grid, block, 0, stream>>>(Gdev, P);      \
+    else if (er && ord) k_ff_lane<NS_, false, true, K_, true><<<grid, block, 0, stream>>>(Gdev, P); \
+    else if (er) k_ff_lane<NS_, false, true, K_, false><<<grid, block, 0, stream>>>(Gdev, P);      \
+    else if (ord) k_ff_lane<NS_, false, false, K_, true><<<grid, block, 0, stream>>>(Gdev, P);     \
+    else k_ff_lane<NS_, false, false, K_, false><<<grid, block, 0, stream>>>(Gdev, P);
 #define FF_LAUNCH(NS_)                           \
     if (dyn) {                                   \
         FF_LAUNCH_K(NS_, MIG_DYNAMIC)            \

@@ -942,9 +942,10 @@ cudaError_t launch_simulate_lane(const DevGeom* Gdev, const mig_traces& tr, cons
                                  const unsigned long long* est_err, uint16_t* ring, uint64_t blocks,
                                  const uint16_t* sid, const uint32_t* a7, uint32_t n_a7,
                                  uint4* pc, unsigned long long* part, int sm_count, cudaStream_t stream,
-                                 const DevGeom* Gh) {
+                                 const DevGeom* Gh, const uint32_t* order) {
     LaneParams P;
     memset(&P, 0, sizeof(P));
+    P.order = order;  // visited through by k_ff_lane only (the kind the order helps); the other kernels ignore it
     P.jobs = (const uint4*)tr.jobs;
     P.ext = (const uint4*)tr.jobs_ext;
     P.off = tr.trace_off;

@@ -36,15 +36,17 @@ print("variant OK")
 '''
 
 
-@pytest.mark.parametrize("lanes,layout,conc,fast", [("1", "narrow", "1", "1"), ("1", "narrow", "0", "1"),
-                                                    ("1", "narrow", "1", "0"), ("8", "wide", "1", "1"),
-                                                    ("8", "narrow", "1", "1"), ("32", "wide", "1", "1"),
-                                                    ("32", "narrow", "1", "1")])
-def test_variant_parity(lanes, layout, conc, fast):
+@pytest.mark.parametrize("lanes,layout,conc,fast,order", [("1", "narrow", "1", "1", "1"), ("1", "narrow", "0", "1", "1"),
+                                                          ("1", "narrow", "1", "0", "1"), ("1", "narrow", "1", "1", "2"),
+                                                          ("1", "narrow", "1", "0", "2"), ("1", "narrow", "1", "1", "0"),
+                                                          ("8", "wide", "1", "1", "1"), ("8", "narrow", "1", "1", "1"),
+                                                          ("32", "wide", "1", "1", "1"), ("32", "narrow", "1", "1", "1")])
+def test_variant_parity(lanes, layout, conc, fast, order):
     # fast = "0": the generic k_simulate_lane for FUSION_FISSION and BASELINE (MIG_FF_FAST=0) and Scheme A's grouping
-    # pass inside the lane kernel (MIG_SA_PREGROUP=0) instead of k_ff_lane / k_base_lane / k_sa_group
+    # pass inside the lane kernel (MIG_SA_PREGROUP=0) instead of k_ff_lane / k_base_lane / k_sa_group; order = "2":
+    # the traces visited in trace_order.cu's order at every size (default "1": from 4096 traces), "0": trace order
     env = dict(os.environ, MIG_LANES_PER_TRACE=lanes, MIG_JOB_LAYOUT=layout, MIG_CONCURRENT_POLICIES=conc,
-               MIG_FF_FAST=fast, MIG_SA_PREGROUP=fast)
+               MIG_FF_FAST=fast, MIG_SA_PREGROUP=fast, MIG_TRACE_ORDER=order)
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "variant OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]

@@ -25,11 +25,13 @@ def main():
 
     def build(tree, name):
         objdir = f"/tmp/ab_obj_{name}"
+        shutil.rmtree(objdir, ignore_errors=True)
         os.makedirs(objdir, exist_ok=True)
         with ThreadPoolExecutor(8) as ex:
+            srcs = [s for s in ge.MIG_SOURCES if os.path.exists(f"{tree}/{s}")]  # the tree's own sources
             objs = list(ex.map(lambda s: (subprocess.run(FLAGS + [f"-I{tree}/include", "-c", f"{tree}/{s}", "-o",
                                                                   f"{objdir}/{os.path.basename(s)}.o"], check=True),
-                                          f"{objdir}/{os.path.basename(s)}.o")[1], ge.MIG_SOURCES))
+                                          f"{objdir}/{os.path.basename(s)}.o")[1], srcs))
         subprocess.run([ge.NVCC, *ge.ARCH, "-shared", "-o", os.path.join(ROOT, f"build/var/{name}.so"), *objs, "-ldl"],
                        check=True)
         print("built", name)
