@@ -19,10 +19,18 @@ levels = torch.tensor([5120, 10240, 20480, 40960], device=dev, dtype=torch.int64
 j3 = jobs.view(n, J, 4).to(torch.int64)
 need = torch.searchsorted(levels, (j3[:, :, 0] & 0xFFFFFFFF) + 512)  # level of each job's tight fit
 K = int(os.environ.get("SIG_JOBS", "4"))
+mode = os.environ.get("SIG_MODE", "levels")
 same_t = (j3[:, :K, 3] == j3[:, :1, 3]).all(dim=1).to(torch.int64)
 key = same_t
 for k in range(K):
     key = key * 8 + need[:, k]
+if mode in ("oom", "oom_homog"):  # + the position of the first job whose estimate is below its true footprint
+    under = (j3[:, :, 0] & 0xFFFFFFFF) < (j3[:, :, 1] & 0xFFFFFFFF)
+    first = torch.where(under.any(dim=1), under.to(torch.int64).argmax(dim=1), torch.full_like(key, J))
+    key = key * 128 + first
+if mode == "oom_homog":  # + all jobs of one level and one iteration time
+    homog = ((need == need[:, :1]).all(dim=1) & (j3[:, :, 3] == j3[:, :1, 3]).all(dim=1)).to(torch.int64)
+    key = homog * (1 << 40) + key
 perm = torch.argsort(key, stable=True)
 jobs_s = jobs.view(n, J, 4)[perm].reshape(-1, 4).contiguous()
 
@@ -46,6 +54,6 @@ def run(jb, label, pols, reps=20):
 
 for pols, name in [([mig.policy(g, kind=3)], "FF"), ([mig.policy(g, kind=3), mig.policy(g, kind=0)], "FF+BASE")]:
     t0 = run(jobs, f"{name} generated order", pols)
-    t1 = run(jobs_s, f"{name} sorted (K={K})", pols)
+    t1 = run(jobs_s, f"{name} sorted (K={K}, {mode})", pols)
     assert all((t0[f] == t1[f]).all() for f in t0.dtype.names), "totals differ"
 print("classes:", int(torch.unique(key).numel()))
