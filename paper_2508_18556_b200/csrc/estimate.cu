@@ -185,7 +185,10 @@ __device__ __forceinline__ void scan_tail(const DevGeom& G, const uint2* rec_sam
             const uint32_t m = __ballot_sync(FULL, over);
             if (!m) break;
             const uint32_t src = (uint32_t)__ffs(m) - 1u;
-            const uint32_t pre = Smem + __reduce_add_sync(FULL, lane <= src ? phys : 0u);
+            // the lane id read here, on the (rare) crossing path, not kept live through the chunk loop
+            uint32_t lid;
+            asm volatile("mov.u32 %0, %%laneid;" : "=r"(lid));
+            const uint32_t pre = Smem + __reduce_add_sync(FULL, lid <= src ? phys : 0u);
 #pragma unroll
             for (int k = 0; k < kMaxLevels; ++k)
                 if ((uint32_t)k == lnext) {
