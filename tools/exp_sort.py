@@ -31,6 +31,10 @@ if mode in ("oom", "oom_homog"):  # + the position of the first job whose estima
 if mode == "oom_homog":  # + all jobs of one level and one iteration time
     homog = ((need == need[:, :1]).all(dim=1) & (j3[:, :, 3] == j3[:, :1, 3]).all(dim=1)).to(torch.int64)
     key = homog * (1 << 40) + key
+if mode in ("ticks", "ticks2"):  # + the octave of the first job's (jobs') iteration time
+    for k in range(1 if mode == "ticks" else 2):
+        lt = torch.floor(torch.log2(j3[:, k, 3].clamp(min=1).to(torch.float64))).to(torch.int64).clamp(0, 15)
+        key = key * 16 + lt
 perm = torch.argsort(key, stable=True)
 jobs_s = jobs.view(n, J, 4)[perm].reshape(-1, 4).contiguous()
 
