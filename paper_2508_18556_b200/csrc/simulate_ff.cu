@@ -58,9 +58,6 @@ __device__ __forceinline__ uint32_t ff_fit(const LaneParams& P, uint32_t req) {
     return p == 0xFu ? kNoNeed : p;
 }
 
-#ifndef FF_WSYNC
-#define FF_WSYNC 1
-#endif
 #ifndef FF_MINB
 #define FF_MINB 8
 #endif
@@ -143,28 +140,19 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
     unsigned long long* const key = &S.key[0][tid];
     constexpr unsigned long long kIdle = ~0ull;
 
-    // units are taken one ahead; s_next holds the trace of the lane's next unit (~0: none left)
-    auto take = [&]() -> unsigned long long {
-        const unsigned long long u = atomicAdd(P.counter, 1ull);
-        return ORD ? lane_unit_trace(P, u) : u;
-    };
-    __shared__ unsigned long long s_next[kLaneThreads];
-#if FF_WSYNC
-    // ORD + FF_WSYNC: a warp takes its units 32 at a time and only when every lane has finished its trace, so the
-    // lanes start the (similar, ordered) traces together and step through them in phase
+    // A warp takes its units 32 at a time, and only once every lane has finished its trace: the lanes start their
+    // traces together, so lanes holding alike traces (the visit order, ORD) step through them in phase. A lane that
+    // finishes early waits (mode 4) for the others. (Config 2: FF launch 2.54 -> 2.04 ms; configs 3 / 4 / 5 k_simulate
+    // 2.85 -> 2.54, 11.7 -> 8.4, 1652 -> 1555 ms against units taken one per lane as each finished.) Returns the
+    // trace of this lane's unit, ~0 once the units are exhausted.
     const uint32_t lane = tid & 31u;
     auto take_batch = [&]() -> unsigned long long {
         unsigned long long u0 = 0;
         if (lane == 0) u0 = atomicAdd(P.counter, 32ull);
         u0 = __shfl_sync(FULL, u0, 0);
-        return lane_unit_trace(P, u0 + lane);
+        return ORD ? lane_unit_trace(P, u0 + lane) : (u0 + lane < P.n_traces ? u0 + lane : ~0ull);
     };
-    unsigned long long tr = ORD ? take_batch() : take();
-    if (!ORD) s_next[tid] = tr < P.n_traces ? take() : ~0ull;
-#else
-    unsigned long long tr = take();
-    s_next[tid] = tr < P.n_traces ? take() : ~0ull;
-#endif
+    unsigned long long tr = take_batch();
     uint64_t j0 = 0;  // index of the unit's first job record
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
     uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0;
@@ -425,24 +413,9 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
             // a12: the unit's counts and sums into the CTA's totals (lane_common.cuh)
             lane_unit_totals(P, S.c32, n, rejected, failed, ooms, preempts, placements, waits, creates, destroys, makespan,
                              err, a_turn, a_busy, ((unsigned long long)hh << 32) | hl, a_mem, a_waste);
-#if FF_WSYNC
-            if (ORD) {
-                mode = 4;  // wait for the warp's other lanes
-            } else
-#endif
-            {
-                tr = s_next[tid];
-                if (tr < P.n_traces) {
-                    s_next[tid] = take();
-                    init_unit();
-                } else {
-                    active = false;
-                    mode = 3;
-                }
-            }
+            mode = 4;  // wait for the warp's other lanes
         }
-#if FF_WSYNC
-        if (ORD && __all_sync(FULL, mode >= 3) && __any_sync(FULL, mode == 4)) {  // the warp's next 32 units
+        if (__all_sync(FULL, mode >= 3) && __any_sync(FULL, mode == 4)) {  // the warp's next 32 units
             tr = take_batch();
             if (tr < P.n_traces) {
                 init_unit();
@@ -451,7 +424,6 @@ __global__ void __launch_bounds__(kLaneThreads, FF_MINB) k_ff_lane(const DevGeom
                 mode = 3;
             }
         }
-#endif
     }
 #undef FF_RING
     lane_flush_totals(P, S.c32);
