@@ -201,8 +201,16 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
     const uint32_t fp = G.full_prof;
 
     // ---- unit state ----
-    unsigned long long tr = atomicAdd(P.counter, 1ull);
-    unsigned long long tr_next = tr < P.n_traces ? atomicAdd(P.counter, 1ull) : ~0ull;
+    // A warp takes its units 32 at a time once every lane has finished its trace (a lane that finishes early waits in
+    // mode 5), so the lanes start their traces together (as k_ff_lane; config 5's STATIC and Scheme A launches).
+    const uint32_t lane_w = tid & 31u;
+    auto take_batch = [&]() -> unsigned long long {
+        unsigned long long u0 = 0;
+        if (lane_w == 0) u0 = atomicAdd(P.counter, 32ull);
+        u0 = __shfl_sync(FULL, u0, 0);
+        return u0 + lane_w < P.n_traces ? u0 + lane_w : ~0ull;
+    };
+    unsigned long long tr = take_batch();
     uint64_t j0 = 0;
     uint32_t n = 0, err = 0, t = 0, qh = 0, rh = 0, rn = 0, mode = 0;
     uint32_t occ = 0, SM = 0, BS = 0, BM = 0, prof4 = 0, evm = 0;
@@ -884,9 +892,11 @@ __global__ void __launch_bounds__(kLaneThreads, lane_min_blocks<KIND>())
             // a12: the unit's counts and sums into the CTA's totals (lane_common.cuh)
             lane_unit_totals(P, S.c32, n, rejected, failed, ooms, preempts, placements, waits, creates, destroys, makespan,
                              err, a_turn, a_busy, ((unsigned long long)hh << 32) | hl, a_mem, a_waste);
-            tr = tr_next;
+            mode = 5;  // wait for the warp's other lanes
+        }
+        if (__all_sync(FULL, mode == 3 || mode == 5) && __any_sync(FULL, mode == 5)) {  // the warp's next 32 units
+            tr = take_batch();
             if (tr < P.n_traces) {
-                tr_next = atomicAdd(P.counter, 1ull);
                 init_unit();
             } else {
                 active = false;
