@@ -35,6 +35,8 @@ if mode in ("ticks", "ticks2"):  # + the octave of the first job's (jobs') itera
     for k in range(1 if mode == "ticks" else 2):
         lt = torch.floor(torch.log2(j3[:, k, 3].clamp(min=1).to(torch.float64))).to(torch.int64).clamp(0, 15)
         key = key * 16 + lt
+if os.environ.get("SIG_DESC"):
+    key = -key
 perm = torch.argsort(key, stable=True)
 jobs_s = jobs.view(n, J, 4)[perm].reshape(-1, 4).contiguous()
 
